@@ -1,0 +1,1252 @@
+// ms_api.cu — system handles, the device-resident adaptive loop and the C-ABI
+// of include/mixedstep_b200.h.
+//
+// The solve (solver.cpp:226-347) runs as: stamp -> initial_step (2 binary64
+// evaluations + norms) -> cold k1 -> loop head -> one CUDA graph whose single
+// WHILE conditional node holds one attempt [k1 recompute] -> (prep, rhs) per
+// stage -> finalize. finalize's last block runs the controller and sets the
+// conditional, so the step loop never returns to the host; the host sees the
+// result only after the graph completes.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#define MS_DEFINE_STEP_KERNELS 1
+#include "ms_dispatch.h"
+
+using namespace msb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidArg : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                      std::to_string(__LINE__) + ")");                                            \
+  } while (0)
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MS_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return MS_EINVAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MS_ECUDA;
+  }
+}
+
+// ---- tableaus (solver.cpp:15-68), literal doubles as written there ----------
+struct Tableau {
+  int S;
+  double a[kMaxStages][kMaxStages];
+  double b_tilde[kMaxStages];
+  int order_high;
+  int scheme_flops;  // scheme_flops_per_component (solver.cpp:361-384)
+};
+
+Tableau make_bs32() {
+  Tableau t{};
+  t.S = 4;
+  t.a[1][0] = 0.5;
+  t.a[2][1] = 0.75;
+  t.a[3][0] = 2.0 / 9.0;
+  t.a[3][1] = 1.0 / 3.0;
+  t.a[3][2] = 4.0 / 9.0;
+  const double bt[4] = {7.0 / 24.0, 0.25, 1.0 / 3.0, 0.125};
+  for (int i = 0; i < 4; ++i) t.b_tilde[i] = bt[i];
+  t.order_high = 3;
+  return t;
+}
+
+Tableau make_dp54() {
+  Tableau t{};
+  t.S = 7;
+  t.a[1][0] = 0.2;
+  t.a[2][0] = 3.0 / 40.0;
+  t.a[2][1] = 9.0 / 40.0;
+  t.a[3][0] = 44.0 / 45.0;
+  t.a[3][1] = -56.0 / 15.0;
+  t.a[3][2] = 32.0 / 9.0;
+  t.a[4][0] = 19372.0 / 6561.0;
+  t.a[4][1] = -25360.0 / 2187.0;
+  t.a[4][2] = 64448.0 / 6561.0;
+  t.a[4][3] = -212.0 / 729.0;
+  t.a[5][0] = 9017.0 / 3168.0;
+  t.a[5][1] = -355.0 / 33.0;
+  t.a[5][2] = 46732.0 / 5247.0;
+  t.a[5][3] = 49.0 / 176.0;
+  t.a[5][4] = -5103.0 / 18656.0;
+  t.a[6][0] = 35.0 / 384.0;
+  t.a[6][2] = 500.0 / 1113.0;
+  t.a[6][3] = 125.0 / 192.0;
+  t.a[6][4] = -2187.0 / 6784.0;
+  t.a[6][5] = 11.0 / 84.0;
+  const double bt[7] = {5179.0 / 57600.0, 0.0, 7571.0 / 16695.0, 393.0 / 640.0, -92097.0 / 339200.0,
+                        187.0 / 2100.0, 1.0 / 40.0};
+  for (int i = 0; i < 7; ++i) t.b_tilde[i] = bt[i];
+  t.order_high = 5;
+  return t;
+}
+
+int scheme_flops(const Tableau& t) {
+  int flops = 0;
+  for (int l = 1; l < t.S; ++l) {
+    int nz = 0;
+    for (int m = 0; m < l; ++m) nz += t.a[l][m] != 0.0;
+    flops += 2 * nz + 1;
+  }
+  int nz = 0;
+  for (int l = 0; l < t.S; ++l) nz += t.b_tilde[l] != 0.0;
+  return flops + 2 * nz + 1 + 8;
+}
+
+const Tableau& bs32() {
+  static const Tableau t = [] {
+    Tableau x = make_bs32();
+    x.scheme_flops = scheme_flops(x);
+    return x;
+  }();
+  return t;
+}
+const Tableau& dp54() {
+  static const Tableau t = [] {
+    Tableau x = make_dp54();
+    x.scheme_flops = scheme_flops(x);
+    return x;
+  }();
+  return t;
+}
+
+bool sp_eq(const ms_stage_prec& a, const ms_stage_prec& b) {
+  return a.f_prec == b.f_prec && a.sum_prec == b.sum_prec && a.g_prec == b.g_prec;
+}
+const ms_stage_prec kDDD{MS_BINARY64, MS_BINARY64, MS_BINARY64, 0};
+
+// ---- seeded inputs: SplitMix64 (rng.hpp:13-52) ---------------------------------
+struct SplitMix64 {
+  uint64_t state;
+  double cached = 0.0;
+  bool has_cached = false;
+  SplitMix64(uint64_t seed, uint64_t stream) : state(seed + stream * 0xD1342543DE82EF95ull) {}
+  uint64_t next() {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  double uniform01() { return static_cast<double>(next() >> 11) * 0x1p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform01(); }
+  double normal() {
+    if (has_cached) {
+      has_cached = false;
+      return cached;
+    }
+    double u1 = uniform01();
+    if (u1 <= 0.0) u1 = 0x1p-53;
+    const double u2 = uniform01();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 6.283185307179586476925286766559 * u2;
+    cached = r * std::sin(a);
+    has_cached = true;
+    return r * std::cos(a);
+  }
+};
+
+// ---- device helper kernels ----------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t state0, uint64_t q) {
+  // the q-th output (0-based) of SplitMix64: the Weyl state advances first
+  uint64_t z = state0 + (q + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <int KS> __device__ __forceinline__ typename KElem<KS>::T to_k(double v);
+template <> __device__ __forceinline__ float to_k<MS_K_F32>(double v) { return __double2float_rn(v); }
+template <> __device__ __forceinline__ __half to_k<MS_K_F16>(double v) { return __double2half(v); }
+template <> __device__ __forceinline__ __nv_bfloat16 to_k<MS_K_BF16>(double v) { return __double2bfloat16(v); }
+
+template <int KS>
+__global__ void k_fill_uniform(typename KElem<KS>::T* K, int n, int row0, int rows, int64_t ld, uint64_t state0,
+                               double lo, double hi) {
+  const int64_t total = (int64_t)rows * n;
+  const double span = __dsub_rn(hi, lo);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = q / n, j = q % n;
+    const uint64_t draw = (uint64_t)(row0 + r) * (uint64_t)n + (uint64_t)j;
+    const double u = (double)(splitmix_at(state0, draw) >> 11) * 0x1p-53;
+    K[r * ld + j] = to_k<KS>(__dadd_rn(lo, __dmul_rn(span, u)));
+  }
+}
+
+template <int KS, class SRC>
+__global__ void k_convert_rows(typename KElem<KS>::T* K, const SRC* src, int n, int rows, int64_t ld) {
+  const int64_t total = (int64_t)rows * n;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = q / n, j = q % n;
+    K[r * ld + j] = to_k<KS>((double)src[q]);
+  }
+}
+
+template <int KS>
+__global__ void k_get_rows(const typename KElem<KS>::T* K, double* dst, int n, int rows, int64_t ld) {
+  const int64_t total = (int64_t)rows * n;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = q / n, j = q % n;
+    dst[q] = (double)k2f(K[r * ld + j]);
+  }
+}
+
+__global__ void k_estimate_error(int64_t n, const double* a, const double* b, const double* c, double ab, double rel,
+                                 double* out) {
+  // estimate_error, solver.cpp:399-411 (max is order-independent)
+  __shared__ double red[32];
+  const double floor_w = __ddiv_rn(ab, rel);
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double w = fmax(fmax(fabs(a[i]), fabs(b[i])), floor_w);
+    m = fmax(m, __ddiv_rn(fabs(__dsub_rn(b[i], c[i])), w));
+  }
+  for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
+    *out = r;
+  }
+}
+
+__global__ void k_adjust_step(double h, double err, double rel, double safety, double fmin, double fmax_,
+                              double ex, double* out) {
+  *out = d_adjust_step(h, err, rel, safety, fmin, fmax_, ex);
+}
+
+// prep instantiations
+template <int MODEL>
+void launch_prep_model(bool fs32, bool gs32, int grid, cudaStream_t st, const PrepArgs& p) {
+  if (fs32) {
+    if (gs32) k_prep<MODEL, float, float><<<grid, 256, 0, st>>>(p);
+    else k_prep<MODEL, float, double><<<grid, 256, 0, st>>>(p);
+  } else {
+    if (gs32) k_prep<MODEL, double, float><<<grid, 256, 0, st>>>(p);
+    else k_prep<MODEL, double, double><<<grid, 256, 0, st>>>(p);
+  }
+}
+
+}  // namespace
+
+// =====================================================================================
+struct ms_system {
+  int model = 0;      // MS_MODEL_*
+  int mkind = 0;      // MD_* (or the fixture id)
+  bool fixture = false;
+  int n = 0, d = 0, cs = 0, ld = 0;
+  int row0 = 0, row1 = 0;
+  int ks = MS_K_SCALAR, rhs_mode = MS_RHS_FAST;
+  int dev = 0, sms = kNumSMsDefault;
+  cudaStream_t stream = nullptr;
+  void* K = nullptr;
+  std::vector<void*> dev_arrays;
+  ModelDev md{};
+  int64_t flop_theta[3] = {0, 0, 0};
+  // workspace
+  bool ws_ready = false;
+  void* ws_mem = nullptr;
+  Bufs B{};
+  int fin_blocks = 1;
+  int64_t log_cap = 0;
+  Ctl* ctl_host = nullptr;  // pinned mirror
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  struct GraphEntry {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::map<std::string, GraphEntry> graphs;
+  std::mutex mu;
+
+  int64_t dn() const { return (int64_t)n * d; }
+};
+
+namespace {
+
+void set_device(ms_system* s) { CK(cudaSetDevice(s->dev)); }
+
+double* upload_array(ms_system* s, const double* host, int n) {
+  if (!host) return nullptr;
+  double* d = nullptr;
+  CK(cudaMalloc(&d, sizeof(double) * n));
+  s->dev_arrays.push_back(d);
+  CK(cudaMemcpy(d, host, sizeof(double) * n, cudaMemcpyHostToDevice));
+  return d;
+}
+
+size_t kelem_bytes(int ks) { return ks == MS_K_F32 ? 4 : 2; }
+
+void ensure_workspace(ms_system* s, int64_t log_cap) {
+  if (s->ws_ready && log_cap <= s->log_cap) return;
+  if (s->ws_ready) {
+    // grow only the log: reallocate the whole workspace (rare)
+    for (auto& kv : s->graphs) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.g) cudaGraphDestroy(kv.second.g);
+    }
+    s->graphs.clear();
+    cudaFree(s->ws_mem);
+    s->ws_ready = false;
+  }
+  const int64_t dn = s->dn();
+  s->fin_blocks = (int)std::min<int64_t>((dn + kFinThreads - 1) / kFinThreads, 2 * s->sms);
+  if (s->fin_blocks < 1) s->fin_blocks = 1;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t vec = al(sizeof(double) * dn);
+  size_t total = 0;
+  total += 2 * vec;                                  // xb
+  total += (kMaxStages + 1) * vec;                   // kb
+  total += 3 * vec;                                  // xn, xt, scratch
+  total += al(sizeof(double) * 2 * s->ld);           // gin
+  total += al(sizeof(double) * s->ld);               // rowc
+  total += al(sizeof(double) * s->n);                // fvc
+  total += al(sizeof(double) * s->fin_blocks);       // part
+  total += al(sizeof(StepLogRec) * std::max<int64_t>(log_cap, 1));
+  total += al(sizeof(Ctl));
+  char* base = nullptr;
+  CK(cudaMalloc(&base, total));
+  CK(cudaMemset(base, 0, total));
+  s->ws_mem = base;
+  char* p = base;
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += al(b);
+    return r;
+  };
+  Bufs& B = s->B;
+  for (int i = 0; i < 2; ++i) B.xb[i] = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  for (int i = 0; i < kMaxStages + 1; ++i) B.kb[i] = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  B.xn = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  B.xt = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  B.scratch = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  B.gin = take(sizeof(double) * 2 * s->ld);
+  B.rowc = take(sizeof(double) * s->ld);
+  B.fvc = reinterpret_cast<double*>(take(sizeof(double) * s->n));
+  B.part = reinterpret_cast<double*>(take(sizeof(double) * s->fin_blocks));
+  B.log = reinterpret_cast<StepLogRec*>(take(sizeof(StepLogRec) * std::max<int64_t>(log_cap, 1)));
+  B.ctl = reinterpret_cast<Ctl*>(take(sizeof(Ctl)));
+  s->log_cap = std::max<int64_t>(log_cap, 1);
+  if (!s->ctl_host) CK(cudaMallocHost(&s->ctl_host, sizeof(Ctl)));
+  s->ws_ready = true;
+}
+
+// ---- one RHS evaluation: prep + coupling sweep ---------------------------------
+struct EvalSpec {
+  int l = 0;
+  int kind = PREP_X;
+  int gate = GATE_ALWAYS;
+  int count = CNT_NONE;
+  int out_slot = SLOT_K1;
+  int nterms = 0;
+  double coef[kMaxStages] = {};
+  int slot[kMaxStages] = {};
+  int is_last = 0;
+  int round_x = 0;
+  int S = 4;
+  const double* xsrc = nullptr;
+};
+
+void launch_eval(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp,
+                 cudaEvent_t mid0 = nullptr, cudaEvent_t mid1 = nullptr) {
+  const bool fs32 = is32(sp.f_prec), ss32 = is32(sp.sum_prec), gs32 = is32(sp.g_prec);
+  PrepArgs p{};
+  p.md = s->md;
+  p.B = s->B;
+  p.S = e.S;
+  p.l = e.l;
+  p.kind = e.kind;
+  p.gate = e.gate;
+  p.count = e.count;
+  p.out_slot = e.out_slot;
+  p.nterms = e.nterms;
+  for (int i = 0; i < kMaxStages; ++i) {
+    p.coef[i] = e.coef[i];
+    p.slot[i] = e.slot[i];
+  }
+  p.is_last = e.is_last;
+  p.round_x = e.round_x;
+  p.split = (s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST) ? 1 : 0;
+  p.ws32 = (fs32 && ss32) ? 1 : 0;
+  p.fs32 = fs32 ? 1 : 0;
+  p.ld = s->ld;
+  p.xsrc = e.xsrc;
+  const int pgrid = (int)std::max<int64_t>(1, std::min<int64_t>((s->n + 255) / 256, 4 * s->sms));
+  if (s->fixture) {
+    launch_prep_model<-1>(fs32, gs32, pgrid, st, p);
+    CK(cudaGetLastError());
+    return;
+  }
+  switch (s->mkind) {
+    case MD_LCO: launch_prep_model<MD_LCO>(fs32, gs32, pgrid, st, p); break;
+    case MD_KUR: launch_prep_model<MD_KUR>(fs32, gs32, pgrid, st, p); break;
+    default: launch_prep_model<MD_CC>(fs32, gs32, pgrid, st, p); break;
+  }
+  CK(cudaGetLastError());
+  RhsArgs a{};
+  a.ctl = s->B.ctl;
+  a.nf_mask = &s->B.ctl->nf_mask;
+  a.l = e.l;
+  a.gate = e.gate;
+  a.S = e.S;
+  a.out_slot = e.out_slot;
+  a.K = s->K;
+  a.ld = s->ld;
+  a.n = s->n;
+  a.row0 = s->row0;
+  a.row1 = s->row1;
+  a.gin = s->B.gin;
+  a.rowc = s->B.rowc;
+  a.fvc = s->B.fvc;
+  for (int i = 0; i < kMaxStages + 1; ++i) a.kb[i] = s->B.kb[i];
+  a.d = s->d;
+  a.cs = s->cs;
+  a.mw = s->md.m[s->cs];
+  a.coupling_k = s->md.coupling_k;
+  a.ws32 = p.ws32;
+  RhsLaunch L{s->mkind, p.split != 0, ss32, gs32, s->ks, s->sms, st};
+  if (mid0) CK(cudaEventRecord(mid0, st));
+  if (s->rhs_mode == MS_RHS_FAST) launch_rhs_fast(L, a);
+  else launch_rhs_faithful(L, a);
+  CK(cudaGetLastError());
+  if (mid1) CK(cudaEventRecord(mid1, st));
+}
+
+// stage l of an attempt (rk_step, solver.cpp:130-154)
+EvalSpec stage_spec(const Tableau& T, int l) {
+  EvalSpec e;
+  e.S = T.S;
+  e.l = l;
+  e.kind = PREP_STAGE;
+  e.count = CNT_STAGE;
+  e.out_slot = (l == T.S - 1) ? SLOT_KLAST : l;
+  e.is_last = (l == T.S - 1) ? 1 : 0;
+  for (int m = 0; m < l; ++m) {
+    if (T.a[l][m] == 0.0) continue;
+    e.coef[e.nterms] = T.a[l][m];
+    e.slot[e.nterms] = (m == 0) ? SLOT_K1 : m;
+    ++e.nterms;
+  }
+  return e;
+}
+
+FinArgs fin_args(ms_system* s, const Tableau& T, int mode, int k1_elided) {
+  FinArgs f{};
+  f.B = s->B;
+  f.S = T.S;
+  for (int m = 0; m < T.S; ++m) {
+    if (T.b_tilde[m] == 0.0) continue;
+    f.bt[f.nbt] = T.b_tilde[m];
+    f.bslot[f.nbt] = (m == 0) ? SLOT_K1 : (m == T.S - 1 ? SLOT_KLAST : m);
+    ++f.nbt;
+  }
+  f.dn = s->dn();
+  f.mode = mode;
+  f.k1_elided = k1_elided;
+  f.write_xt = mode == FIN_STEP ? 1 : 0;
+  return f;
+}
+
+struct SolvePlan {
+  const Tableau* T;
+  ms_stage_prec rows[kMaxStages];  // rows[l-1] for stage l
+  ms_stage_prec k1_row;
+  int storage;
+  int lowest;
+  bool k1_elided;
+};
+
+// one attempt: [k1 recompute] -> stages -> finalize
+void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_handle,
+                    cudaGraphConditionalHandle h) {
+  const Tableau& T = *P.T;
+  if (!P.k1_elided) {
+    EvalSpec e;
+    e.S = T.S;
+    e.l = 0;
+    e.kind = PREP_X;
+    e.gate = GATE_NEED_K1;
+    e.count = CNT_K1;
+    e.out_slot = SLOT_K1;
+    launch_eval(s, st, e, P.k1_row);
+  }
+  for (int l = 1; l < T.S; ++l) launch_eval(s, st, stage_spec(T, l), P.rows[l - 1]);
+  FinArgs f = fin_args(s, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
+  f.has_handle = has_handle ? 1 : 0;
+  f.handle = h;
+  k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
+  CK(cudaGetLastError());
+}
+
+// initial_step + cold k1 + loop head (solver.cpp:247-269)
+void launch_init(ms_system* s, cudaStream_t st, const SolvePlan& P, bool with_k1) {
+  const Tableau& T = *P.T;
+  k_stamp_start<<<1, 1, 0, st>>>(s->B.ctl);
+  EvalSpec f0;
+  f0.S = T.S;
+  f0.l = 7;
+  f0.kind = PREP_X;
+  f0.count = CNT_DDD;
+  f0.out_slot = 1;
+  launch_eval(s, st, f0, kDDD);
+  InitArgs ia{};
+  ia.B = s->B;
+  ia.x0 = s->B.xb[0];
+  ia.dn = s->dn();
+  ia.exponent = 1.0 / static_cast<double>(T.order_high + 1);
+  k_init_a<<<1, 1024, 0, st>>>(ia);
+  CK(cudaGetLastError());
+  EvalSpec f1 = f0;
+  f1.kind = PREP_INIT_X1;
+  f1.gate = GATE_INIT2;
+  f1.out_slot = 2;
+  launch_eval(s, st, f1, kDDD);
+  k_init_b<<<1, 1024, 0, st>>>(ia);
+  CK(cudaGetLastError());
+  if (!with_k1) return;
+  EvalSpec k1;
+  k1.S = T.S;
+  k1.l = 0;
+  k1.kind = PREP_X;
+  k1.count = CNT_K1;
+  k1.out_slot = SLOT_K1;
+  k1.round_x = P.storage == MS_BINARY32 ? 1 : 0;
+  launch_eval(s, st, k1, P.k1_row);
+  k_loop_head<<<1, 1, 0, st>>>(s->B.ctl);
+  CK(cudaGetLastError());
+}
+
+void validate_cfg(const ms_solver_config& c, double t0, double tf) {  // solver.cpp:217-224
+  if (!(c.abs_tol > 0.0 && c.abs_tol <= c.rel_tol && c.rel_tol < 1.0))
+    throw InvalidArg("solver: need 0 < abs_tol <= rel_tol < 1");
+  if (!(c.fac_min < 1.0 && c.fac_max > 1.0)) throw InvalidArg("solver: need fac_min < 1 < fac_max");
+  if (!(tf > t0)) throw InvalidArg("solver: need t_final > t0");
+  if (c.record_snapshots) throw InvalidArg("solver: record_snapshots is not supported on the device");
+}
+
+void init_ctl(ms_system* s, Ctl& c, const ms_solver_config& cfg, double t0, double tf, const SolvePlan& P,
+              int64_t log_cap) {
+  std::memset(&c, 0, sizeof(Ctl));
+  c.t = t0;
+  c.t0 = t0;
+  c.tf = tf;
+  c.h_min = cfg.h_min_factor * (P.lowest == MS_BINARY32 ? 0x1p-23 : 0x1p-52);
+  c.rel_tol = cfg.rel_tol;
+  c.abs_tol = cfg.abs_tol;
+  c.safety = cfg.safety;
+  c.fac_min = cfg.fac_min;
+  c.fac_max = cfg.fac_max;
+  c.ctrl_exp = cfg.controller_exponent;
+  c.wall_clock_limit = cfg.wall_clock_limit;
+  c.slow_elapsed = cfg.slow_solver_elapsed;
+  c.slow_progress = cfg.slow_solver_progress;
+  c.max_iterations = cfg.max_iterations;
+  c.max_failed = cfg.max_failed_steps;
+  c.log_capacity = log_cap;
+  c.store32 = P.storage == MS_BINARY32 ? 1 : 0;
+  c.time_limits = cfg.time_limits_enabled ? 1 : 0;
+  c.record_log = cfg.record_step_log ? 1 : 0;
+  c.status = MS_COMPLETED;
+  (void)s;
+}
+
+std::string plan_key(const SolvePlan& P) {
+  char buf[160];
+  int o = std::snprintf(buf, sizeof(buf), "S%d:st%d:el%d:k1%d%d%d", P.T->S, P.storage, (int)P.k1_elided,
+                        P.k1_row.f_prec, P.k1_row.sum_prec, P.k1_row.g_prec);
+  for (int l = 0; l < P.T->S - 1; ++l)
+    o += std::snprintf(buf + o, sizeof(buf) - o, ":%d%d%d", P.rows[l].f_prec, P.rows[l].sum_prec, P.rows[l].g_prec);
+  return std::string(buf);
+}
+
+bool use_host_loop() {
+  const char* v = std::getenv("MS_LOOP");
+  return v && std::strcmp(v, "host") == 0;
+}
+
+cudaGraphExec_t get_loop_graph(ms_system* s, const SolvePlan& P) {
+  const std::string key = plan_key(P);
+  auto it = s->graphs.find(key);
+  if (it != s->graphs.end()) return it->second.exec;
+  ms_system::GraphEntry ge;
+  CK(cudaGraphCreate(&ge.g, 0));
+  cudaGraphConditionalHandle handle;
+  CK(cudaGraphConditionalHandleCreate(&handle, ge.g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, ge.g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(s->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  try {
+    launch_attempt(s, s->stream, P, true, handle);
+  } catch (...) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(s->stream, &dummy);
+    throw;
+  }
+  CK(cudaStreamEndCapture(s->stream, &body));
+  CK(cudaGraphInstantiate(&ge.exec, ge.g, 0));
+  s->graphs[key] = ge;
+  return ge.exec;
+}
+
+void tally(ms_system* s, const Ctl& c, const SolvePlan& P, int64_t out[3]) {
+  // FlopTally (solver.cpp:70-82) from the per-row evaluation counts
+  const int64_t n = s->n;
+  int64_t low = 0, high = 0, evals = 0;
+  auto add = [&](const ms_stage_prec& sp, int64_t cnt) {
+    if (cnt <= 0) return;
+    (is32(sp.f_prec) ? low : high) += s->flop_theta[0] * n * cnt;
+    (is32(sp.g_prec) ? low : high) += s->flop_theta[1] * n * n * cnt;
+    (is32(sp.sum_prec) ? low : high) += s->flop_theta[2] * n * n * cnt;
+    evals += cnt;
+  };
+  add(kDDD, c.evals_ddd);
+  add(P.k1_row, c.evals_k1);
+  for (int l = 1; l < P.T->S; ++l) add(P.rows[l - 1], c.evals_stage[l]);
+  high += (int64_t)P.T->scheme_flops * s->dn() * (c.n_acc + c.n_fail);
+  out[0] = evals;
+  out[1] = low;
+  out[2] = high;
+}
+
+void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf, const SolvePlan& P,
+               const ms_solver_config& cfg, ms_solve_result* res, cudaStream_t user_stream, bool out_dev) {
+  validate_cfg(cfg, t0, tf);
+  std::lock_guard<std::mutex> lk(s->mu);
+  set_device(s);
+  const int64_t cap = (cfg.record_step_log && res->step_log) ? std::max<int64_t>(res->step_log_capacity, 1) : 1;
+  ensure_workspace(s, cap);
+  cudaStream_t st = s->stream;
+  if (user_stream && user_stream != st) {
+    // order the solve after the caller's prior work on its stream
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, user_stream));
+    CK(cudaStreamWaitEvent(st, e, 0));
+    CK(cudaEventDestroy(e));
+  }
+  Ctl& c = *s->ctl_host;
+  init_ctl(s, c, cfg, t0, tf, P, cap);
+  const int64_t dn = s->dn();
+  CK(cudaMemcpyAsync(s->B.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s->B.xb[0], x0, sizeof(double) * dn, x0_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     st));
+  const bool host_loop = use_host_loop();
+  cudaGraphExec_t exec = host_loop ? nullptr : get_loop_graph(s, P);
+  CK(cudaEventRecord(s->ev0, st));
+  launch_init(s, st, P, true);
+  if (host_loop) {
+    for (;;) {
+      launch_attempt(s, st, P, false, 0);
+      CK(cudaMemcpyAsync(&c.done, &s->B.ctl->done, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (c.done) break;
+    }
+  } else {
+    CK(cudaGraphLaunch(exec, st));
+  }
+  CK(cudaEventRecord(s->ev1, st));
+  CK(cudaMemcpyAsync(&c, s->B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  if (res->final_state) {
+    CK(cudaMemcpyAsync(res->final_state, s->B.xb[c.ix], sizeof(double) * dn,
+                       out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  }
+  res->step_log_count = c.record_log ? c.log_count : 0;
+  if (res->step_log && c.record_log) {
+    const int64_t m = std::min<int64_t>(res->step_log_capacity, c.log_count);
+    if (m > 0) {
+      std::vector<StepLogRec> tmp((size_t)m);
+      CK(cudaMemcpyAsync(tmp.data(), s->B.log, sizeof(StepLogRec) * m, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int64_t i = 0; i < m; ++i) {
+        res->step_log[i].t = tmp[(size_t)i].t;
+        res->step_log[i].h = tmp[(size_t)i].h;
+        res->step_log[i].err = tmp[(size_t)i].err;
+        res->step_log[i].accepted = tmp[(size_t)i].accepted;
+      }
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  if (user_stream && user_stream != st) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, st));
+    CK(cudaStreamWaitEvent(user_stream, e, 0));
+    CK(cudaEventDestroy(e));
+  }
+  res->status = c.status;
+  res->t_reached = c.t;
+  res->n_accepted = c.n_acc;
+  res->n_failed = c.n_fail;
+  int64_t tl[3];
+  tally(s, c, P, tl);
+  res->rhs_evals = tl[0];
+  res->flops_low = tl[1];
+  res->flops_high = tl[2];
+  res->device_ms = ms;
+}
+
+SolvePlan plan_bs32(const ms_policy& pol) {
+  SolvePlan P{};
+  P.T = &bs32();
+  for (int l = 0; l < 3; ++l) P.rows[l] = pol.per_stage[l];
+  P.k1_row = pol.first_step_k1;
+  P.storage = pol.storage;
+  // PrecisionPolicy::lowest_format (precision.cpp:9-20)
+  int lowest = MS_BINARY64;
+  if (pol.storage == MS_BINARY32) lowest = MS_BINARY32;
+  const ms_stage_prec all[4] = {pol.per_stage[0], pol.per_stage[1], pol.per_stage[2], pol.first_step_k1};
+  for (const auto& sp : all)
+    if (is32(sp.f_prec) || is32(sp.sum_prec) || is32(sp.g_prec)) lowest = MS_BINARY32;
+  P.lowest = lowest;
+  // The k1 recomputed after a rejection (solver.cpp:298-306) evaluates the
+  // same autonomous field at the same x as the stored k1; when the k1 row equals
+  // the last stage's row the stored value is bit-identical, so the launch is
+  // elided (and still counted).
+  P.k1_elided = sp_eq(pol.first_step_k1, pol.per_stage[2]);
+  return P;
+}
+
+SolvePlan plan_dp54() {
+  SolvePlan P{};
+  P.T = &dp54();
+  for (int l = 0; l < 6; ++l) P.rows[l] = kDDD;
+  P.k1_row = kDDD;
+  P.storage = MS_BINARY64;
+  P.lowest = MS_BINARY64;
+  P.k1_elided = true;
+  return P;
+}
+
+void check_prec(const ms_stage_prec& sp) {
+  if (sp.f_prec > 1 || sp.sum_prec > 1 || sp.g_prec > 1) throw InvalidArg("stage precision: format must be 0 or 1");
+}
+void check_policy(const ms_policy& p) {
+  for (int l = 0; l < 3; ++l) check_prec(p.per_stage[l]);
+  check_prec(p.first_step_k1);
+  if (p.storage > 1) throw InvalidArg("policy: bad storage format");
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+int ms_abi_version(void) { return MS_ABI_VERSION; }
+const char* ms_last_error(void) { return g_err.c_str(); }
+
+int ms_abi_sizes(int64_t out[7]) {
+  out[0] = sizeof(ms_stage_prec);
+  out[1] = sizeof(ms_policy);
+  out[2] = sizeof(ms_solver_config);
+  out[3] = sizeof(ms_step_record);
+  out[4] = sizeof(ms_system_desc);
+  out[5] = sizeof(ms_solve_result);
+  out[6] = sizeof(ms_step_outcome);
+  return MS_OK;
+}
+
+int ms_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void ms_default_config(ms_solver_config* c) {  // solver.hpp:39-61
+  std::memset(c, 0, sizeof(*c));
+  c->rel_tol = 1e-6;
+  c->abs_tol = 1e-8;
+  c->h_min_factor = 100.0;
+  c->max_iterations = 100000;
+  c->max_failed_steps = 85000;
+  c->time_limits_enabled = 1;
+  c->record_step_log = 1;
+  c->wall_clock_limit = 5400.0;
+  c->slow_solver_elapsed = 2700.0;
+  c->slow_solver_progress = 0.10;
+  c->safety = 0.9;
+  c->fac_min = 0.2;
+  c->fac_max = 5.0;
+  c->controller_exponent = 1.0 / 3.0;
+  c->record_snapshots = 0;
+}
+
+int ms_policy_for(int variant, ms_policy* out) {  // precision.cpp:22-42
+  return guard([&] {
+    if (variant < MS_SINGLE || variant > MS_DOUBLE) throw InvalidArg("policy_for: unknown variant");
+    const ms_stage_prec sss{MS_BINARY32, MS_BINARY32, MS_BINARY32, 0};
+    const ms_stage_prec dds{MS_BINARY64, MS_BINARY64, MS_BINARY32, 0};
+    const ms_stage_prec ddd = kDDD;
+    std::memset(out, 0, sizeof(*out));
+    out->variant = (uint8_t)variant;
+    switch (variant) {
+      case MS_SINGLE: out->per_stage[0] = out->per_stage[1] = out->per_stage[2] = sss; break;
+      case MS_MIXED1: out->per_stage[0] = out->per_stage[1] = sss; out->per_stage[2] = dds; break;
+      case MS_MIXED2: out->per_stage[0] = out->per_stage[1] = out->per_stage[2] = dds; break;
+      default: out->per_stage[0] = out->per_stage[1] = out->per_stage[2] = ddd; break;
+    }
+    out->first_step_k1 = out->per_stage[2];
+    out->storage = variant == MS_SINGLE ? MS_BINARY32 : MS_BINARY64;
+  });
+}
+
+int ms_policy_lowest_format(const ms_policy* p) { return plan_bs32(*p).lowest; }
+
+int ms_rng_uniform(uint64_t seed, uint64_t stream, int64_t n, double lo, double hi, double* out) {
+  SplitMix64 r(seed, stream);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.uniform(lo, hi);
+  return MS_OK;
+}
+int ms_rng_normal(uint64_t seed, uint64_t stream, int64_t n, double* out) {
+  SplitMix64 r(seed, stream);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.normal();
+  return MS_OK;
+}
+
+int ms_system_create(const ms_system_desc* d, ms_system_t* out) {
+  return guard([&] {
+    if (!d || !out) throw InvalidArg("system_create: null argument");
+    auto s = std::make_unique<ms_system>();
+    const int n = d->n_agents;
+    if (n < 1) throw InvalidArg("system: N must be >= 1");  // systems.cpp:210,223,244
+    s->model = d->model;
+    switch (d->model) {
+      case MS_MODEL_LCO: s->mkind = MD_LCO; s->d = 2; break;
+      case MS_MODEL_KURAMOTO: s->mkind = MD_KUR; s->d = 1; break;
+      case MS_MODEL_CC: s->mkind = MD_CC; s->d = 4; break;
+      case MS_MODEL_SCALAR_EXP:
+      case MS_MODEL_SCALAR_ZERO:
+      case MS_MODEL_SCALAR_NAN:
+        s->mkind = d->model;
+        s->fixture = true;
+        s->d = 1;
+        break;
+      default: throw InvalidArg("system: unknown model");
+    }
+    s->n = n;
+    s->cs = d->model == MS_MODEL_LCO ? d->coupled_slot : 0;
+    if (s->cs < 0 || s->cs >= s->d) throw InvalidArg("system: bad coupled slot");
+    s->ks = d->k_storage;
+    if (s->ks < MS_K_SCALAR || s->ks > MS_K_BF16) throw InvalidArg("system: bad K storage");
+    s->rhs_mode = d->rhs_mode;
+    if (s->rhs_mode != MS_RHS_FAST && s->rhs_mode != MS_RHS_FAITHFUL) throw InvalidArg("system: bad rhs mode");
+    s->ld = (n + 7) & ~7;
+    s->row0 = d->row_begin;
+    s->row1 = d->row_end;
+    if (s->row0 == 0 && s->row1 == 0) s->row1 = n;
+    if (s->row0 < 0 || s->row1 > n || s->row0 >= s->row1) throw InvalidArg("system: bad row range");
+    if (s->mkind == MD_KUR && !d->omega) throw InvalidArg("kuramoto: omega required");
+    if (s->mkind == MD_CC && (!d->cc_k1 || !d->cc_theta_h)) throw InvalidArg("cc: k1 and theta_h required");
+    if (s->ks != MS_K_SCALAR && s->fixture) throw InvalidArg("fixture systems have no K");
+    s->dev = d->device;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw CudaError("ms_system_create: no CUDA device (the B200 path has no CPU fallback)");
+    }
+    set_device(s.get());
+    CK(cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, s->dev));
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&s->ev0));
+    CK(cudaEventCreate(&s->ev1));
+    ModelDev& md = s->md;
+    md.kind = s->mkind;
+    md.n = n;
+    md.d = s->d;
+    md.cs = s->cs;
+    for (int q = 0; q < 4; ++q) md.m[q] = 0.0;
+    if (d->m) {
+      for (int q = 0; q < s->d; ++q) md.m[q] = d->m[q];
+    } else if (!s->fixture) {
+      md.m[s->cs] = 1.0 / n;
+    }
+    md.coupling_k = d->coupling_k;
+    md.i0 = d->stimulus_i0;
+    md.omega = upload_array(s.get(), d->omega, n);
+    md.w2 = upload_array(s.get(), d->w2, n);
+    md.k1 = upload_array(s.get(), d->cc_k1, n);
+    md.th = upload_array(s.get(), d->cc_theta_h, n);
+    md.k0 = upload_array(s.get(), d->cc_k0, n);
+    md.k2 = upload_array(s.get(), d->cc_k2, n);
+    md.ca = upload_array(s.get(), d->cc_a, n);
+    md.cb = upload_array(s.get(), d->cc_b, n);
+    md.cc = upload_array(s.get(), d->cc_c, n);
+    md.eps = upload_array(s.get(), d->cc_eps, n);
+    switch (s->mkind) {  // FlopProfile (systems.cpp:217, 238, 266; test_support.hpp:23)
+      case MD_LCO: s->flop_theta[0] = 1; s->flop_theta[1] = 1; s->flop_theta[2] = 4; break;
+      case MD_KUR: s->flop_theta[0] = 1; s->flop_theta[1] = 3; s->flop_theta[2] = 2; break;
+      case MD_CC: s->flop_theta[0] = 28; s->flop_theta[1] = 10; s->flop_theta[2] = 8; break;
+      default: s->flop_theta[0] = 1; s->flop_theta[1] = 1; s->flop_theta[2] = 2; break;
+    }
+    if (s->ks != MS_K_SCALAR) {
+      const int rows = s->row1 - s->row0;
+      const size_t bytes = (size_t)rows * s->ld * kelem_bytes(s->ks);
+      CK(cudaMalloc(&s->K, bytes));
+      CK(cudaMemset(s->K, 0, bytes));
+      if (d->K) {
+        // upload in row blocks of <= 64 MiB, convert to the storage format once
+        const size_t hb = d->k_host_dtype == MS_HOST_F32 ? 4 : 8;
+        const int rb = (int)std::max<size_t>(1, (size_t(64) << 20) / ((size_t)n * hb));
+        void* stage = nullptr;
+        CK(cudaMalloc(&stage, (size_t)rb * n * hb));
+        for (int r = 0; r < rows; r += rb) {
+          const int nr = std::min(rb, rows - r);
+          const char* src = static_cast<const char*>(d->K) + ((size_t)(s->row0 + r) * n) * hb;
+          CK(cudaMemcpy(stage, src, (size_t)nr * n * hb, cudaMemcpyHostToDevice));
+          const int64_t off = (int64_t)r * s->ld;
+          const int grid = 1024;
+          if (hb == 4) {
+            const float* sp = static_cast<const float*>(stage);
+            if (s->ks == MS_K_F32) k_convert_rows<MS_K_F32, float><<<grid, 256>>>((float*)s->K + off, sp, n, nr, s->ld);
+            else if (s->ks == MS_K_F16) k_convert_rows<MS_K_F16, float><<<grid, 256>>>((__half*)s->K + off, sp, n, nr, s->ld);
+            else k_convert_rows<MS_K_BF16, float><<<grid, 256>>>((__nv_bfloat16*)s->K + off, sp, n, nr, s->ld);
+          } else {
+            const double* sp = static_cast<const double*>(stage);
+            if (s->ks == MS_K_F32) k_convert_rows<MS_K_F32, double><<<grid, 256>>>((float*)s->K + off, sp, n, nr, s->ld);
+            else if (s->ks == MS_K_F16) k_convert_rows<MS_K_F16, double><<<grid, 256>>>((__half*)s->K + off, sp, n, nr, s->ld);
+            else k_convert_rows<MS_K_BF16, double><<<grid, 256>>>((__nv_bfloat16*)s->K + off, sp, n, nr, s->ld);
+          }
+          CK(cudaGetLastError());
+          CK(cudaDeviceSynchronize());
+        }
+        CK(cudaFree(stage));
+      }
+    }
+    CK(cudaDeviceSynchronize());
+    *out = s.release();
+  });
+}
+
+int ms_system_destroy(ms_system_t s) {
+  if (!s) return MS_OK;
+  return guard([&] {
+    cudaSetDevice(s->dev);
+    for (auto& kv : s->graphs) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.g) cudaGraphDestroy(kv.second.g);
+    }
+    for (void* p : s->dev_arrays) cudaFree(p);
+    if (s->K) cudaFree(s->K);
+    if (s->ws_mem) cudaFree(s->ws_mem);
+    if (s->ctl_host) cudaFreeHost(s->ctl_host);
+    if (s->ev0) cudaEventDestroy(s->ev0);
+    if (s->ev1) cudaEventDestroy(s->ev1);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+  });
+}
+
+int ms_system_fill_k_uniform(ms_system_t s, uint64_t seed, uint64_t stream, double lo, double hi) {
+  return guard([&] {
+    if (!s || s->ks == MS_K_SCALAR) throw InvalidArg("fill_k: system has scalar coupling");
+    set_device(s);
+    const uint64_t state0 = seed + stream * 0xD1342543DE82EF95ull;
+    const int rows = s->row1 - s->row0;
+    const int grid = 8 * s->sms;
+    if (s->ks == MS_K_F32) k_fill_uniform<MS_K_F32><<<grid, 256, 0, s->stream>>>((float*)s->K, s->n, s->row0, rows, s->ld, state0, lo, hi);
+    else if (s->ks == MS_K_F16) k_fill_uniform<MS_K_F16><<<grid, 256, 0, s->stream>>>((__half*)s->K, s->n, s->row0, rows, s->ld, state0, lo, hi);
+    else k_fill_uniform<MS_K_BF16><<<grid, 256, 0, s->stream>>>((__nv_bfloat16*)s->K, s->n, s->row0, rows, s->ld, state0, lo, hi);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int ms_system_get_k(ms_system_t s, double* out) {
+  return guard([&] {
+    if (!s || s->ks == MS_K_SCALAR) throw InvalidArg("get_k: system has scalar coupling");
+    set_device(s);
+    const int rows = s->row1 - s->row0;
+    double* tmp = nullptr;
+    CK(cudaMalloc(&tmp, sizeof(double) * (size_t)rows * s->n));
+    if (s->ks == MS_K_F32) k_get_rows<MS_K_F32><<<1024, 256, 0, s->stream>>>((const float*)s->K, tmp, s->n, rows, s->ld);
+    else if (s->ks == MS_K_F16) k_get_rows<MS_K_F16><<<1024, 256, 0, s->stream>>>((const __half*)s->K, tmp, s->n, rows, s->ld);
+    else k_get_rows<MS_K_BF16><<<1024, 256, 0, s->stream>>>((const __nv_bfloat16*)s->K, tmp, s->n, rows, s->ld);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, tmp, sizeof(double) * (size_t)rows * s->n, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaFree(tmp));
+  });
+}
+
+int ms_system_dim(ms_system_t s) { return s ? s->d : -1; }
+int ms_system_agents(ms_system_t s) { return s ? s->n : -1; }
+int ms_system_flop_profile(ms_system_t s, int64_t out[4]) {
+  if (!s) return MS_EINVAL;
+  out[0] = s->flop_theta[0];
+  out[1] = s->flop_theta[1];
+  out[2] = s->flop_theta[2];
+  out[3] = s->d;
+  return MS_OK;
+}
+
+int ms_eval_rhs(ms_system_t s, double t, const double* x, ms_stage_prec sp, double* out) {
+  return guard([&] {
+    (void)t;  // every model is autonomous (systems.cpp:118,137,159,177)
+    if (!s || !x || !out) throw InvalidArg("eval_rhs: null argument");
+    check_prec(sp);
+    std::lock_guard<std::mutex> lk(s->mu);
+    set_device(s);
+    ensure_workspace(s, 1);
+    Ctl& c = *s->ctl_host;
+    std::memset(&c, 0, sizeof(Ctl));
+    const int64_t dn = s->dn();
+    CK(cudaMemcpyAsync(s->B.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->B.xb[0], x, sizeof(double) * dn, cudaMemcpyHostToDevice, s->stream));
+    EvalSpec e;
+    e.l = 0;
+    e.kind = PREP_X;
+    e.out_slot = 0;
+    launch_eval(s, s->stream, e, sp);
+    CK(cudaMemcpyAsync(out, s->B.kb[0], sizeof(double) * dn, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int ms_profile_rhs(ms_system_t s, const double* x, ms_stage_prec sp, int iters, double* rhs_ms, double* prep_ms) {
+  return guard([&] {
+    if (!s || !x || iters < 1) throw InvalidArg("profile_rhs: bad arguments");
+    check_prec(sp);
+    std::lock_guard<std::mutex> lk(s->mu);
+    set_device(s);
+    ensure_workspace(s, 1);
+    Ctl& c = *s->ctl_host;
+    std::memset(&c, 0, sizeof(Ctl));
+    cudaStream_t st = s->stream;
+    CK(cudaMemcpyAsync(s->B.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->B.xb[0], x, sizeof(double) * s->dn(), cudaMemcpyHostToDevice, st));
+    EvalSpec e;
+    e.l = 0;
+    e.kind = PREP_X;
+    e.out_slot = 0;
+    std::vector<cudaEvent_t> ev(3 * (size_t)iters);
+    for (auto& v : ev) CK(cudaEventCreate(&v));
+    launch_eval(s, st, e, sp);  // warm-up
+    for (int i = 0; i < iters; ++i) {
+      CK(cudaEventRecord(ev[3 * i], st));
+      launch_eval(s, st, e, sp, ev[3 * i + 1], ev[3 * i + 2]);
+    }
+    CK(cudaStreamSynchronize(st));
+    double tr = 0, tp = 0;
+    for (int i = 0; i < iters; ++i) {
+      float a = 0, b = 0;
+      CK(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+      CK(cudaEventElapsedTime(&b, ev[3 * i + 1], ev[3 * i + 2]));
+      tp += a;
+      tr += b;
+    }
+    for (auto& v : ev) cudaEventDestroy(v);
+    if (rhs_ms) *rhs_ms = tr / iters;
+    if (prep_ms) *prep_ms = tp / iters;
+  });
+}
+
+int ms_estimate_error(int64_t n, const double* x_n, const double* x_next, const double* x_tilde, double ab,
+                      double rel, double* err) {
+  return guard([&] {
+    if (n < 0 || !err) throw InvalidArg("estimate_error: bad arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw CudaError("ms_estimate_error: no CUDA device");
+    }
+    double* buf = nullptr;
+    const size_t b = sizeof(double) * (size_t)std::max<int64_t>(n, 1);
+    CK(cudaMalloc(&buf, 3 * b + sizeof(double)));
+    if (n > 0) {
+      CK(cudaMemcpy(buf, x_n, sizeof(double) * n, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy((char*)buf + b, x_next, sizeof(double) * n, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy((char*)buf + 2 * b, x_tilde, sizeof(double) * n, cudaMemcpyHostToDevice));
+    }
+    double* o = reinterpret_cast<double*>((char*)buf + 3 * b);
+    k_estimate_error<<<1, 1024>>>(n, buf, (double*)((char*)buf + b), (double*)((char*)buf + 2 * b), ab, rel, o);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(err, o, sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaFree(buf));
+  });
+}
+
+int ms_adjust_step(double h, double err, double rel_tol, const ms_solver_config* cfg, double* h_next) {
+  return guard([&] {
+    if (!cfg || !h_next) throw InvalidArg("adjust_step: null argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw CudaError("ms_adjust_step: no CUDA device");
+    }
+    double* o = nullptr;
+    CK(cudaMalloc(&o, sizeof(double)));
+    k_adjust_step<<<1, 1>>>(h, err, rel_tol, cfg->safety, cfg->fac_min, cfg->fac_max, cfg->controller_exponent, o);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(h_next, o, sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaFree(o));
+  });
+}
+
+int ms_initial_step(ms_system_t s, double t0, double t_final, const double* x0, const ms_solver_config* cfg,
+                    int order, double* h0, int64_t* rhs_evals) {
+  return guard([&] {
+    if (!s || !x0 || !cfg || !h0) throw InvalidArg("initial_step: null argument");
+    std::lock_guard<std::mutex> lk(s->mu);
+    set_device(s);
+    ensure_workspace(s, 1);
+    Tableau T = bs32();
+    T.order_high = order;
+    SolvePlan P{};
+    P.T = &T;
+    P.k1_row = kDDD;
+    P.storage = MS_BINARY64;
+    P.lowest = MS_BINARY64;
+    Ctl& c = *s->ctl_host;
+    init_ctl(s, c, *cfg, t0, t_final, P, 1);
+    CK(cudaMemcpyAsync(s->B.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->B.xb[0], x0, sizeof(double) * s->dn(), cudaMemcpyHostToDevice, s->stream));
+    launch_init(s, s->stream, P, false);
+    CK(cudaMemcpyAsync(&c, s->B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    *h0 = c.h;
+    if (rhs_evals) *rhs_evals = c.evals_ddd;
+  });
+}
+
+int ms_bs32_step(ms_system_t s, double t, const double* x_n, double h, const double* k1, const ms_policy* pol,
+                 const ms_solver_config* cfg, ms_step_outcome* out) {
+  return guard([&] {
+    if (!s || !x_n || !k1 || !pol || !cfg || !out) throw InvalidArg("bs32_step: null argument");
+    check_policy(*pol);
+    std::lock_guard<std::mutex> lk(s->mu);
+    set_device(s);
+    ensure_workspace(s, 1);
+    const SolvePlan P = plan_bs32(*pol);
+    const Tableau& T = *P.T;
+    Ctl& c = *s->ctl_host;
+    init_ctl(s, c, *cfg, t, t + 1.0, P, 1);
+    c.h_att = h;
+    c.h = h;
+    const int64_t dn = s->dn();
+    cudaStream_t st = s->stream;
+    CK(cudaMemcpyAsync(s->B.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->B.xb[0], x_n, sizeof(double) * dn, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->B.kb[0], k1, sizeof(double) * dn, cudaMemcpyHostToDevice, st));
+    for (int l = 1; l < T.S; ++l) launch_eval(s, st, stage_spec(T, l), P.rows[l - 1]);
+    FinArgs f = fin_args(s, T, FIN_STEP, 0);
+    k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&c, s->B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const bool store32 = P.storage == MS_BINARY32;
+    // first non-finite stage decides which outputs exist (solver.cpp:143-162)
+    int nf_stage = 0;
+    for (int l = 1; l < T.S; ++l)
+      if (c.nf_mask & (1 << l)) {
+        nf_stage = l;
+        break;
+      }
+    const bool have_xnext = nf_stage == 0 || nf_stage == T.S - 1;
+    const bool have_xstore = nf_stage == 0 || (nf_stage == T.S - 1 && store32);
+    const bool have_rest = nf_stage == 0;
+    auto get = [&](double* dst, const double* src, bool have) {
+      if (!dst) return;
+      if (have) {
+        CK(cudaMemcpyAsync(dst, src, sizeof(double) * dn, cudaMemcpyDeviceToHost, st));
+      } else {
+        for (int64_t i = 0; i < dn; ++i) dst[i] = std::numeric_limits<double>::quiet_NaN();
+      }
+    };
+    get(out->x_next, store32 ? s->B.xn : s->B.xb[1], have_xnext);
+    get(out->x_store, s->B.xb[1], have_xstore);
+    get(out->k4, s->B.kb[T.S], have_rest);
+    get(out->x_tilde, s->B.xt, have_rest);
+    CK(cudaStreamSynchronize(st));
+    out->err = c.err;
+    out->accepted = c.accepted;
+    out->h_used = h;
+    out->h_next = c.h_next;
+    int64_t evals = 0, low = 0, high = 0;
+    const int64_t n = s->n;
+    for (int l = 1; l < T.S; ++l) {
+      const int64_t cnt = c.evals_stage[l];
+      const ms_stage_prec& sp = P.rows[l - 1];
+      (is32(sp.f_prec) ? low : high) += s->flop_theta[0] * n * cnt;
+      (is32(sp.g_prec) ? low : high) += s->flop_theta[1] * n * n * cnt;
+      (is32(sp.sum_prec) ? low : high) += s->flop_theta[2] * n * n * cnt;
+      evals += cnt;
+    }
+    high += (int64_t)T.scheme_flops * dn;
+    out->rhs_evals = evals;
+    out->flops_low = low;
+    out->flops_high = high;
+  });
+}
+
+int ms_solve(ms_system_t s, const double* x0, double t0, double t_final, const ms_policy* pol,
+             const ms_solver_config* cfg, ms_solve_result* res) {
+  return guard([&] {
+    if (!s || !x0 || !pol || !cfg || !res) throw InvalidArg("solve: null argument");
+    check_policy(*pol);
+    run_solve(s, x0, false, t0, t_final, plan_bs32(*pol), *cfg, res, nullptr, false);
+  });
+}
+
+int ms_solve_device(ms_system_t s, const double* x0_dev, double t0, double t_final, const ms_policy* pol,
+                    const ms_solver_config* cfg, ms_solve_result* res, void* stream) {
+  return guard([&] {
+    if (!s || !x0_dev || !pol || !cfg || !res) throw InvalidArg("solve_device: null argument");
+    check_policy(*pol);
+    run_solve(s, x0_dev, true, t0, t_final, plan_bs32(*pol), *cfg, res, static_cast<cudaStream_t>(stream), true);
+  });
+}
+
+int ms_dp54_reference(ms_system_t s, const double* x0, double t0, double t_final, const ms_solver_config* cfg,
+                      ms_solve_result* res) {
+  return guard([&] {
+    if (!s || !x0 || !cfg || !res) throw InvalidArg("dp54_reference: null argument");
+    ms_solver_config rc = *cfg;  // solver.cpp:474-478
+    rc.rel_tol = 1e-9;
+    rc.abs_tol = 1e-9;
+    rc.controller_exponent = 1.0 / 5.0;
+    rc.record_snapshots = 0;
+    run_solve(s, x0, false, t0, t_final, plan_dp54(), rc, res, nullptr, false);
+  });
+}
+
+}  // extern "C"

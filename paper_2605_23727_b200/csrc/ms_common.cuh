@@ -1,0 +1,126 @@
+// ms_common.cuh — shared device/host definitions of the B200 integrator.
+//
+// Arithmetic contract: every floating operation below
+// is a single IEEE operation rounded once in its stated format, with no FMA
+// contraction (the translation units are compiled with -fmad=false, and the
+// hot loops spell their roundings with __fmul_rn/__fadd_rn/__dmul_rn/__dadd_rn).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/mixedstep_b200.h"
+
+namespace msb {
+
+constexpr int kMaxStages = 7;  // DP5(4) has 7 (solver.cpp:35-68)
+constexpr int kNumSMsDefault = 148;
+
+// ---- formats -------------------------------------------------------------
+__host__ __device__ inline bool is32(uint8_t f) { return f == MS_BINARY32; }
+
+// RN into f32 of a double (precision.hpp:21-24: (double)(float)x)
+__device__ __forceinline__ double rn32(double x) { return (double)__double2float_rn(x); }
+
+// Correctly-rounded-by-construction f32 transcendentals: evaluate in binary64
+// and round once. glibc's sinf/atanf (the reference's libm, systems.cpp:142,
+// 184) are correctly rounded in nearly all cases, so this is the closest
+// device counterpart; CUDA's own sinf/atanf carry up to 2 ulp.
+__device__ __forceinline__ float cr_sinf(float x) { return __double2float_rn(sin((double)x)); }
+__device__ __forceinline__ float cr_cosf(float x) { return __double2float_rn(cos((double)x)); }
+__device__ __forceinline__ float cr_atanf(float x) { return __double2float_rn(atan((double)x)); }
+
+template <class S> __device__ __forceinline__ S dsin(S x);
+template <> __device__ __forceinline__ float dsin<float>(float x) { return cr_sinf(x); }
+template <> __device__ __forceinline__ double dsin<double>(double x) { return sin(x); }
+template <class S> __device__ __forceinline__ S dcos(S x);
+template <> __device__ __forceinline__ float dcos<float>(float x) { return cr_cosf(x); }
+template <> __device__ __forceinline__ double dcos<double>(double x) { return cos(x); }
+template <class S> __device__ __forceinline__ S datan(S x);
+template <> __device__ __forceinline__ float datan<float>(float x) { return cr_atanf(x); }
+template <> __device__ __forceinline__ double datan<double>(double x) { return atan(x); }
+
+// single-rounding arithmetic in format S
+template <class S> __device__ __forceinline__ S add(S a, S b);
+template <class S> __device__ __forceinline__ S sub(S a, S b);
+template <class S> __device__ __forceinline__ S mul(S a, S b);
+template <class S> __device__ __forceinline__ S dvd(S a, S b);
+template <> __device__ __forceinline__ float add<float>(float a, float b) { return __fadd_rn(a, b); }
+template <> __device__ __forceinline__ float sub<float>(float a, float b) { return __fsub_rn(a, b); }
+template <> __device__ __forceinline__ float mul<float>(float a, float b) { return __fmul_rn(a, b); }
+template <> __device__ __forceinline__ float dvd<float>(float a, float b) { return __fdiv_rn(a, b); }
+template <> __device__ __forceinline__ double add<double>(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ double sub<double>(double a, double b) { return __dsub_rn(a, b); }
+template <> __device__ __forceinline__ double mul<double>(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ double dvd<double>(double a, double b) { return __ddiv_rn(a, b); }
+
+// RN into S of a double
+template <class S> __device__ __forceinline__ S cvt(double x);
+template <> __device__ __forceinline__ float cvt<float>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ double cvt<double>(double x) { return x; }
+
+// ---- coupling storage --------------------------------------------------------
+struct KScalar {};  // no matrix: G uses RN_S(coupling_k)
+template <int KS> struct KElem;
+template <> struct KElem<MS_K_F32> { using T = float; };
+template <> struct KElem<MS_K_F16> { using T = __half; };
+template <> struct KElem<MS_K_BF16> { using T = __nv_bfloat16; };
+
+__device__ __forceinline__ float k2f(float v) { return v; }
+__device__ __forceinline__ float k2f(__half v) { return __half2float(v); }
+__device__ __forceinline__ float k2f(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// ---- model ids for templates ------------------------------------------------
+enum : int { MD_LCO = 0, MD_KUR = 1, MD_CC = 2 };
+
+// ---- device control block (one per solve workspace) -------------------------
+// Replicated controller state of solve_core (solver.cpp:226-347); every kernel
+// reads it, only the single-thread controller sections write it.
+struct Ctl {
+  // clock and step
+  double t, h, h_att, t0, tf, h_min;
+  double h1, cap, d1;  // initial_step scratch (solver.cpp:420-451)
+  double err, h_next;
+  // config (solver.hpp:39-61)
+  double rel_tol, abs_tol, safety, fac_min, fac_max, ctrl_exp;
+  double wall_clock_limit, slow_elapsed, slow_progress;
+  int64_t max_iterations, max_failed;
+  // counters
+  int64_t n_acc, n_fail, attempts;
+  int64_t evals_ddd, evals_k1, evals_stage[kMaxStages];
+  int64_t log_count, log_capacity;
+  uint64_t t_start_ns;
+  // flags
+  int32_t status, done, need_k1, last, accepted;
+  int32_t nf_mask;        // bit l: stage l produced a non-finite value this attempt
+  int32_t ix;             // current x buffer (x = xb[ix], x_store -> xb[ix^1])
+  int32_t k1i;            // k1 slot: 0 or S (FSAL ping-pong with the last stage)
+  int32_t store32, time_limits, record_log, init_skip2;
+  int32_t any_nonfinite;  // finalize scratch
+  uint32_t ticket;        // last-block-done counter (finalize / init)
+  int32_t _pad;
+};
+
+struct StepLogRec {
+  double t, h, err;
+  int32_t accepted, _pad;
+};
+
+// Pointers of one solve workspace (device addresses).
+struct Bufs {
+  double* xb[2];                 // x / x_store ping-pong
+  double* kb[kMaxStages + 1];    // stage derivatives; slot 0 <-> slot S for FSAL
+  double* xn;                    // x_next under binary32 storage
+  double* xt;                    // x_tilde (only when requested)
+  double* scratch;               // dN terms for initial_step sums
+  void* gin;                     // GS-typed column data (2 * ld doubles)
+  void* rowc;                    // GS-typed per-row G constant (CC prefactor)
+  double* fvc;                   // F of the coupled slot, per agent
+  double* part;                  // per-block partials of finalize
+  StepLogRec* log;
+  Ctl* ctl;
+};
+
+}  // namespace msb

@@ -1,0 +1,871 @@
+// ms_kernels.cuh — sm_100a kernels of the mixed-precision BS3(2) hot path.
+//
+//   prep        stage combination of rk_step (solver.cpp:130-149, 86-104) fused
+//               with the per-agent part of eval_core: F_i in FS, the GS cast of
+//               the coupled slot (or sin/cos of it for the Kuramoto split), the
+//               CC prefactor, and the uncoupled output slots (systems.cpp:35-62)
+//   rhs_fast    the all-pairs coupling sweep (systems.cpp:50-57) as a K-row
+//               stream: 128-bit loads of K, column data staged in shared memory
+//               by cp.async.bulk (TMA) through an mbarrier ring, warp-shuffle
+//               row reductions. HBM-bound at large N.
+//   rhs_faithful  the same sum in the reference's exact order: one thread per
+//               row, ascending j including j = i, per-pair G (parity mode)
+//   finalize    x_tilde, weighted max-norm error, accept/reject, adjust_step and
+//               the loop bookkeeping of solve_core (solver.cpp:188-214,
+//               272-342, 399-418), last-block-done over a grid reduction
+//   init_a/b    initial_step norms (solver.cpp:420-451)
+#pragma once
+
+#include "ms_common.cuh"
+
+namespace msb {
+
+// ------------------------------------------------------------------------------
+// model parameters on the device
+struct ModelDev {
+  int kind;     // MD_* or a fixture MS_MODEL_SCALAR_*
+  int n, d, cs; // agents, dim, coupled slot
+  double m[4];  // per-slot weights (systems.hpp:71)
+  double coupling_k, i0;
+  const double* omega;
+  const double* w2;
+  const double* k1;
+  const double* th;
+  const double* k0;
+  const double* k2;
+  const double* ca;
+  const double* cb;
+  const double* cc;
+  const double* eps;
+};
+
+// reference CcConstants (systems.hpp:32-43)
+constexpr double kCcK0 = 2.0, kCcK2 = 0.144832, kCcA = 2.0, kCcB = 0.7, kCcC = 0.8,
+                 kCcEps = 0.228249;
+
+enum : int { PREP_X = 0, PREP_STAGE = 1, PREP_INIT_X1 = 2 };
+enum : int { GATE_ALWAYS = 0, GATE_NEED_K1 = 1, GATE_INIT2 = 2 };
+enum : int { CNT_DDD = 0, CNT_K1 = 1, CNT_STAGE = 2, CNT_NONE = 3 };
+// k-buffer references resolved at run time through ctl->k1i
+enum : int { SLOT_K1 = -1, SLOT_KLAST = -2 };
+
+struct PrepArgs {
+  ModelDev md;
+  Bufs B;
+  int S;          // tableau stages
+  int l;          // stage index in rk_step (0 = k1 / plain evaluation)
+  int kind;       // PREP_*
+  int gate;       // GATE_*
+  int count;      // CNT_*
+  int out_slot;   // k-buffer receiving the evaluation (SLOT_* or index)
+  int nterms;
+  double coef[kMaxStages];
+  int slot[kMaxStages];
+  int is_last;    // FSAL last stage: x_next (and binary32 x_store) is the argument
+  int round_x;    // binary32 storage cold start: x <- RN32(x) in place
+  int split;      // Kuramoto split column data (sin, cos)
+  int ws32;       // WS = wider(FS, SS) is binary32
+  int fs32;       // F precision is binary32 (fixtures: round_to(x, f_prec))
+  int ld;         // padded column count
+  const double* xsrc;  // PREP_X source (NULL = xb[ix])
+};
+
+struct RhsArgs {
+  const Ctl* ctl;
+  int* nf_mask;
+  int l, gate, S, out_slot;
+  const void* K;
+  int64_t ld;
+  int n, row0, row1;
+  const void* gin;
+  const void* rowc;
+  const double* fvc;
+  double* kb[kMaxStages + 1];
+  int d, cs;
+  double mw;
+  double coupling_k;
+  int ws32;
+};
+
+__device__ __forceinline__ double* resolve_slot(const Bufs& B, int S, int slot, int k1i) {
+  if (slot == SLOT_K1) return B.kb[k1i];
+  if (slot == SLOT_KLAST) return B.kb[S - k1i];
+  return B.kb[slot];
+}
+
+// Shared skip rule of every kernel of stage l (prep and rhs decide alike).
+__device__ __forceinline__ bool stage_skip(const Ctl* c, int l, int gate) {
+  if (c->done) return true;
+  if (gate == GATE_NEED_K1 && !c->need_k1) return true;
+  if (gate == GATE_INIT2 && c->init_skip2) return true;
+  if (l > 0 && (c->nf_mask & ((1 << l) - 1))) return true;
+  return false;
+}
+
+// ------------------------------------------------------------------------------
+// F_i in FS (systems.cpp:117-120, 136-139, 159-174 + D2/D4 extensions)
+template <class S>
+__device__ __forceinline__ void model_f(const ModelDev& md, int i, const double* a, S* f) {
+  if (md.kind == MD_LCO) {
+    const S x0 = cvt<S>(a[0]), x1 = cvt<S>(a[1]);
+    f[0] = x1;
+    f[1] = md.w2 ? -mul<S>(cvt<S>(md.w2[i]), x0) : -x0;
+  } else if (md.kind == MD_KUR) {
+    f[0] = cvt<S>(md.omega[i]);
+  } else {
+    const S x1 = cvt<S>(a[0]), x2 = cvt<S>(a[1]), x3 = cvt<S>(a[2]), x4 = cvt<S>(a[3]);
+    const S th = cvt<S>(md.th[i]);
+    const S k0 = cvt<S>(md.k0 ? md.k0[i] : kCcK0);
+    const S ca = cvt<S>(md.ca ? md.ca[i] : kCcA);
+    const S x2sq = mul<S>(x2, x2);
+    const S x2h = mul<S>(x2sq, x2sq);
+    // ((k0*th)/(th+x2h)) * ((a*x1)*x1 + 1) - k1*x1
+    f[0] = sub<S>(mul<S>(dvd<S>(mul<S>(k0, th), add<S>(th, x2h)),
+                         add<S>(mul<S>(mul<S>(ca, x1), x1), S(1))),
+                  mul<S>(cvt<S>(md.k1[i]), x1));
+    f[1] = mul<S>(cvt<S>(md.k2 ? md.k2[i] : kCcK2), sub<S>(x1, x2));
+    const S x1sq = mul<S>(x1, x1);
+    // (x3*(1 - (x3*x3)/3) - x4) + I0*(1 - 4/(4 + x1sq)); k3^2 = 4 fixed
+    f[2] = add<S>(sub<S>(mul<S>(x3, sub<S>(S(1), dvd<S>(mul<S>(x3, x3), S(3)))), x4),
+                  mul<S>(cvt<S>(md.i0), sub<S>(S(1), dvd<S>(S(4), add<S>(S(4), x1sq)))));
+    // eps*((x3 + b) - c*x4)
+    f[3] = mul<S>(cvt<S>(md.eps ? md.eps[i] : kCcEps),
+                  sub<S>(add<S>(x3, cvt<S>(md.cb ? md.cb[i] : kCcB)),
+                         mul<S>(cvt<S>(md.cc ? md.cc[i] : kCcC), x4)));
+  }
+}
+
+// CC row constant pref = ((k0*th)*a)/(th + x2sq*x2sq) in GS (systems.cpp:176-186):
+// row-invariant, so hoisting it out of the j loop is bitwise safe.
+template <class S>
+__device__ __forceinline__ S cc_pref(const ModelDev& md, int i, double x2d) {
+  const S x2 = cvt<S>(x2d);
+  const S x2sq = mul<S>(x2, x2);
+  const S th = cvt<S>(md.th[i]);
+  const S k0 = cvt<S>(md.k0 ? md.k0[i] : kCcK0);
+  const S ca = cvt<S>(md.ca ? md.ca[i] : kCcA);
+  return dvd<S>(mul<S>(mul<S>(k0, th), ca), add<S>(th, mul<S>(x2sq, x2sq)));
+}
+
+__device__ __forceinline__ double ws_add(double fval, double coupling, int ws32) {
+  // out = (double)((WS)f + (WS)acc), systems.cpp:59-62
+  if (ws32) return (double)__fadd_rn((float)fval, (float)coupling);
+  return __dadd_rn(fval, coupling);
+}
+
+// ------------------------------------------------------------------------------
+// prep: one thread per agent.
+template <int MODEL, class FS, class GS>
+__global__ void __launch_bounds__(256) k_prep(PrepArgs p) {
+  Ctl* ctl = p.B.ctl;
+  if (stage_skip(ctl, p.l, p.gate)) return;
+  const int n = p.md.n, d = p.md.d;
+  const int k1i = ctl->k1i, ix = ctl->ix;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.count == CNT_DDD) ctl->evals_ddd += 1;
+    else if (p.count == CNT_K1) ctl->evals_k1 += 1;
+    else if (p.count == CNT_STAGE) ctl->evals_stage[p.l] += 1;
+  }
+  double* x = p.B.xb[ix];
+  const double* xs = p.xsrc ? p.xsrc : x;
+  double* out = resolve_slot(p.B, p.S, p.out_slot, k1i);
+  const double h = p.kind == PREP_INIT_X1 ? ctl->h1 : ctl->h_att;
+  const bool store32 = ctl->store32 != 0;
+  bool nonfinite = false;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double a[4];
+    for (int s = 0; s < d; ++s) {
+      const int64_t e = (int64_t)i * d + s;
+      double v;
+      if (p.kind == PREP_X) {
+        v = xs[e];
+        if (p.round_x) {
+          v = rn32(v);
+          x[e] = v;
+        }
+      } else if (p.kind == PREP_INIT_X1) {
+        v = __dadd_rn(xs[e], __dmul_rn(h, p.B.kb[1][e]));  // x0 + h1 * f0 (solver.cpp:435)
+      } else {
+        // combo = a_l0*k_0 (+ a_lm*k_m ...), arg = x + h*combo (solver.cpp:130-142)
+        double c = __dmul_rn(p.coef[0], resolve_slot(p.B, p.S, p.slot[0], k1i)[e]);
+        for (int t = 1; t < p.nterms; ++t)
+          c = __dadd_rn(c, __dmul_rn(p.coef[t], resolve_slot(p.B, p.S, p.slot[t], k1i)[e]));
+        v = __dadd_rn(xs[e], __dmul_rn(h, c));
+        if (p.is_last) {
+          if (store32) {
+            // combine_binary32 (solver.cpp:86-104)
+            const float hf = __double2float_rn(h);
+            float acc = __double2float_rn(xs[e]);
+            for (int t = 0; t < p.nterms; ++t) {
+              const float cf = __fmul_rn(hf, __double2float_rn(p.coef[t]));
+              acc = __fadd_rn(acc, __fmul_rn(cf, __double2float_rn(
+                                                     resolve_slot(p.B, p.S, p.slot[t], k1i)[e])));
+            }
+            p.B.xn[e] = v;  // x_next
+            v = (double)acc;
+          }
+          p.B.xb[ix ^ 1][e] = v;  // x_store (= x_next under binary64 storage)
+        }
+      }
+      a[s] = v;
+    }
+    if (MODEL < 0) {
+      // reference test fixtures (test_support.hpp:21-53): the whole RHS is F
+      const int kind = p.md.kind;
+      for (int s = 0; s < d; ++s) {
+        const int64_t e = (int64_t)i * d + s;
+        double o;
+        if (kind == MS_MODEL_SCALAR_EXP) o = p.fs32 ? rn32(a[s]) : a[s];  // round_to(x, f_prec)
+        else if (kind == MS_MODEL_SCALAR_ZERO) o = 0.0;
+        else o = __longlong_as_double(0x7ff8000000000000ll);
+        out[e] = o;
+        nonfinite |= !isfinite(o);
+      }
+      continue;
+    }
+    FS f[4];
+    model_f<FS>(p.md, i, a, f);
+    const int cs = p.md.cs;
+    for (int s = 0; s < d; ++s) {
+      if (s == cs) continue;
+      const double o = ws_add((double)f[s], 0.0, p.ws32);  // acc of an uncoupled slot is +0
+      out[(int64_t)i * d + s] = o;
+      nonfinite |= !isfinite(o);
+    }
+    p.B.fvc[i] = (double)f[cs];
+    GS* gin = reinterpret_cast<GS*>(p.B.gin);
+    const GS xg = cvt<GS>(a[cs]);
+    if (p.split) {
+      gin[i] = dsin<GS>(xg);
+      gin[p.ld + i] = dcos<GS>(xg);
+    } else {
+      gin[i] = xg;
+    }
+    if (MODEL == MD_CC) reinterpret_cast<GS*>(p.B.rowc)[i] = cc_pref<GS>(p.md, i, a[1]);
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(&ctl->nf_mask, 1 << p.l);
+}
+
+// ------------------------------------------------------------------------------
+// mbarrier / bulk-copy helpers (sm_90+ PTX, used on sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint4 ldg_stream(const void* ptr) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr));
+  return r;
+}
+
+template <class T> __device__ __forceinline__ T shfl_xor(T v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+
+// K element j of a 16-byte vector as f32 (exact for every storage format)
+template <int KS> struct KVec;
+template <> struct KVec<MS_K_F32> {
+  static constexpr int N = 4;
+  __device__ __forceinline__ static void unpack(const uint4& v, float* o) {
+    o[0] = __uint_as_float(v.x); o[1] = __uint_as_float(v.y);
+    o[2] = __uint_as_float(v.z); o[3] = __uint_as_float(v.w);
+  }
+};
+template <> struct KVec<MS_K_F16> {
+  static constexpr int N = 8;
+  __device__ __forceinline__ static void unpack(const uint4& v, float* o) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
+      o[2 * q] = f.x; o[2 * q + 1] = f.y;
+    }
+  }
+};
+template <> struct KVec<MS_K_BF16> {
+  static constexpr int N = 8;
+  __device__ __forceinline__ static void unpack(const uint4& v, float* o) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      o[2 * q] = __uint_as_float(w[q] << 16);
+      o[2 * q + 1] = __uint_as_float(w[q] & 0xffff0000u);
+    }
+  }
+};
+template <> struct KVec<MS_K_SCALAR> {
+  static constexpr int N = 4;
+};
+
+constexpr int kFastThreads = 512;  // 16 warps, one CTA per SM
+constexpr int kFastWarps = kFastThreads / 32;
+constexpr int kChunkCols = 1024;   // columns per staged chunk
+constexpr int kStagesNS = 4;       // mbarrier ring depth
+
+template <class GS, bool SPLIT>
+constexpr size_t fast_smem_bytes() {
+  return (size_t)kStagesNS * (SPLIT ? 2 : 1) * kChunkCols * sizeof(GS) + 2 * kStagesNS * sizeof(uint64_t);
+}
+
+// Rows per warp per sweep.
+template <class SS, class GS> struct FastRows { static constexpr int R = (sizeof(GS) == 8 || sizeof(SS) == 8) ? 4 : 8; };
+
+// ------------------------------------------------------------------------------
+// rhs_fast: one persistent CTA per SM; the CTA owns a contiguous balanced row
+// range; its 16 warps take rows round-robin and sweep all columns together,
+// R rows per warp per sweep, so each staged chunk of column data is shared by
+// 16*R rows. Per lane: one 128-bit K load per row per step. Row totals come
+// from a warp-shuffle tree; the order of every row's sum depends only on N
+// (not on the row partition), so sharded runs are bitwise identical.
+template <int MODEL, bool SPLIT, class SS, class GS, int KS>
+__global__ void __launch_bounds__(kFastThreads, 1) k_rhs_fast(RhsArgs a) {
+  if (stage_skip(a.ctl, a.l, a.gate)) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int NCOL = SPLIT ? 2 : 1;
+  constexpr int VEC = KVec<KS>::N;
+  constexpr int COLS_IT = 32 * VEC;
+  constexpr int R = FastRows<SS, GS>::R;
+  GS* stage_buf = reinterpret_cast<GS*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStagesNS * NCOL * kChunkCols * sizeof(GS));
+  uint64_t* empty = full + kStagesNS;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = a.row1 - a.row0;
+  const int rb = a.row0 + (int)(total * blockIdx.x / gridDim.x);
+  const int re = a.row0 + (int)(total * (blockIdx.x + 1) / gridDim.x);
+  const int nrows = re - rb;
+  const int per_warp = (nrows + kFastWarps - 1) / kFastWarps;
+  const int nsweeps = (per_warp + R - 1) / R;
+  const int ld = (int)a.ld;
+  const int nchunks = (ld + kChunkCols - 1) / kChunkCols;
+  const int Q = nsweeps * nchunks;
+  const GS* gin = reinterpret_cast<const GS*>(a.gin);
+
+  auto chunk_cols = [&](int c) { return min(kChunkCols, ld - c * kChunkCols); };
+  auto issue = [&](int q) {
+    const int c = q % nchunks, st = q % kStagesNS;
+    const int cc = chunk_cols(c);
+    const uint32_t bytes = (uint32_t)(cc * sizeof(GS));
+    mbar_expect_tx(&full[st], bytes * NCOL);
+    for (int t = 0; t < NCOL; ++t)
+      bulk_g2s(stage_buf + (size_t)(st * NCOL + t) * kChunkCols, gin + (size_t)t * ld + (size_t)c * kChunkCols,
+               bytes, &full[st]);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStagesNS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kFastWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < min(kStagesNS, Q); ++q) issue(q);
+
+  const SS mw = cvt<SS>(a.mw);
+  const GS kscal = cvt<GS>(a.coupling_k);
+  using KT = typename KElem<KS == MS_K_SCALAR ? MS_K_F32 : KS>::T;
+  const KT* Kbase = reinterpret_cast<const KT*>(a.K);
+  double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
+  bool nonfinite = false;
+
+  int q = 0;
+  for (int sw = 0; sw < nsweeps; ++sw) {
+    int rows[R];
+    GS xi[R], pref[R];
+    int nr = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = rb + warp + kFastWarps * (sw * R + k);
+      rows[k] = r < re ? r : -1;
+      if (r < re) nr = k + 1;
+      xi[k] = GS(0);
+      pref[k] = GS(0);
+      if (!SPLIT && r < re) {
+        xi[k] = gin[r];
+        if (MODEL == MD_CC) pref[k] = reinterpret_cast<const GS*>(a.rowc)[r];
+      }
+    }
+    SS A[R], B[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) { A[k] = SS(0); B[k] = SS(0); }
+
+    for (int c = 0; c < nchunks; ++c, ++q) {
+      const int st = q % kStagesNS;
+      const int cc = chunk_cols(c);
+      mbar_wait(&full[st], (q / kStagesNS) & 1);
+      const GS* sv = stage_buf + (size_t)(st * NCOL) * kChunkCols;
+      const GS* cv = sv + kChunkCols;
+      if (nr > 0) {
+        const int c0 = c * kChunkCols;
+        for (int col = lane * VEC; col < cc; col += COLS_IT) {
+          GS s_loc[VEC], c_loc[VEC];
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            s_loc[v] = sv[col + v];
+            if (SPLIT) c_loc[v] = cv[col + v];
+          }
+          if constexpr (KS == MS_K_SCALAR) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              if (k >= nr) break;
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) {
+                if (SPLIT) {
+                  A[k] = add<SS>(A[k], (SS)mul<GS>(kscal, s_loc[v]));
+                  B[k] = add<SS>(B[k], (SS)mul<GS>(kscal, c_loc[v]));
+                } else if (c0 + col + v < a.n) {
+                  GS g;
+                  if (MODEL == MD_LCO) g = mul<GS>(kscal, sub<GS>(s_loc[v], xi[k]));
+                  else g = mul<GS>(pref[k], mul<GS>(kscal, datan<GS>(sub<GS>(s_loc[v], xi[k]))));
+                  A[k] = add<SS>(A[k], (SS)g);
+                }
+              }
+            }
+          } else {
+            uint4 kv[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k)
+              if (k < nr) kv[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + col);
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              if (k < nr) {
+                float kf[VEC];
+                KVec<KS>::unpack(kv[k], kf);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                  const GS kg = (GS)kf[v];
+                  if (SPLIT) {
+                    A[k] = add<SS>(A[k], (SS)mul<GS>(kg, s_loc[v]));
+                    B[k] = add<SS>(B[k], (SS)mul<GS>(kg, c_loc[v]));
+                  } else {
+                    GS g;
+                    if (MODEL == MD_LCO) g = mul<GS>(kg, sub<GS>(s_loc[v], xi[k]));
+                    else g = mul<GS>(pref[k], mul<GS>(kg, datan<GS>(sub<GS>(s_loc[v], xi[k]))));
+                    A[k] = add<SS>(A[k], (SS)g);
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (warp == 0) {
+        if (lane == 0 && q + kStagesNS < Q) {
+          mbar_wait(&empty[st], (q / kStagesNS) & 1);
+          issue(q + kStagesNS);
+        }
+        __syncwarp();
+      }
+    }
+    // warp-shuffle reduction of every row, then lane k writes row k
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) {
+        A[k] = add<SS>(A[k], shfl_xor(A[k], m));
+        if (SPLIT) B[k] = add<SS>(B[k], shfl_xor(B[k], m));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (lane == k && k < nr) {
+        const int r = rows[k];
+        SS coup;
+        if (SPLIT) {
+          const SS si = (SS)gin[r], ci = (SS)gin[ld + r];
+          coup = mul<SS>(mw, sub<SS>(mul<SS>(ci, A[k]), mul<SS>(si, B[k])));
+        } else {
+          coup = mul<SS>(mw, A[k]);
+        }
+        const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
+        out[(int64_t)r * a.d + a.cs] = o;
+        nonfinite |= !isfinite(o);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
+}
+
+// ------------------------------------------------------------------------------
+// rhs_faithful: eval_core's exact order (systems.cpp:50-57): per row, ascending
+// j including j = i, acc = acc + mw * (SS)G_ij, G in GS with RN_GS(K_ij).
+template <int MODEL, class SS, class GS, int KS>
+__global__ void __launch_bounds__(128) k_rhs_faithful(RhsArgs a) {
+  if (stage_skip(a.ctl, a.l, a.gate)) return;
+  const int r = a.row0 + blockIdx.x * blockDim.x + threadIdx.x;
+  bool nonfinite = false;
+  if (r < a.row1) {
+    const GS* gin = reinterpret_cast<const GS*>(a.gin);
+    const GS xi = gin[r];
+    const GS pref = MODEL == MD_CC ? reinterpret_cast<const GS*>(a.rowc)[r] : GS(0);
+    const SS mw = cvt<SS>(a.mw);
+    const GS kscal = cvt<GS>(a.coupling_k);
+    using KT = typename KElem<KS == MS_K_SCALAR ? MS_K_F32 : KS>::T;
+    const KT* Krow = reinterpret_cast<const KT*>(a.K) + (size_t)(r - a.row0) * a.ld;
+    SS acc = SS(0);
+    for (int j = 0; j < a.n; ++j) {
+      GS kg;
+      if constexpr (KS == MS_K_SCALAR) kg = kscal;
+      else kg = (GS)k2f(Krow[j]);
+      const GS diff = sub<GS>(__ldg(gin + j), xi);
+      GS g;
+      if (MODEL == MD_LCO) g = mul<GS>(kg, diff);
+      else if (MODEL == MD_KUR) g = mul<GS>(kg, dsin<GS>(diff));
+      else g = mul<GS>(pref, mul<GS>(kg, datan<GS>(diff)));
+      acc = add<SS>(acc, mul<SS>(mw, (SS)g));
+    }
+    double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
+    const double o = ws_add(a.fvc[r], (double)acc, a.ws32);
+    out[(int64_t)r * a.d + a.cs] = o;
+    nonfinite = !isfinite(o);
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(a.nf_mask, 1 << a.l);
+}
+
+// ------------------------------------------------------------------------------
+// controller helpers (solver.cpp:413-418, 272-314)
+__device__ __forceinline__ double d_clamp(double v, double lo, double hi) {
+  return v < lo ? lo : (hi < v ? hi : v);  // std::clamp
+}
+__device__ __forceinline__ double d_adjust_step(double h, double err, double rel, double safety,
+                                                double fac_min, double fac_max, double ctrl_exp) {
+  if (err <= 0.0) return __dmul_rn(h, fac_max);
+  const double fac = __dmul_rn(safety, pow(__ddiv_rn(rel, err), ctrl_exp));
+  return __dmul_rn(h, d_clamp(fac, fac_min, fac_max));
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef MS_DEFINE_STEP_KERNELS
+// top of the solve_core loop (solver.cpp:273-296) and the final-step clip (:309-314)
+__device__ void loop_check(Ctl* c) {
+  if (c->n_acc + c->n_fail >= c->max_iterations) {
+    c->status = MS_MAX_ITERATIONS; c->done = 1; return;
+  }
+  if (c->n_fail >= c->max_failed) {
+    c->status = MS_MAX_FAILED_STEPS; c->done = 1; return;
+  }
+  if (c->time_limits) {
+    const double el = (double)(globaltimer_ns() - c->t_start_ns) * 1e-9;
+    if (el > c->wall_clock_limit) {
+      c->status = MS_WALL_CLOCK; c->done = 1; return;
+    }
+    if (el > c->slow_elapsed &&
+        __dsub_rn(c->t, c->t0) < __dmul_rn(c->slow_progress, __dsub_rn(c->tf, c->t0))) {
+      c->status = MS_SLOW_SOLVER; c->done = 1; return;
+    }
+  }
+  if (c->h <= c->h_min) {
+    c->status = MS_STEP_TOO_SMALL; c->done = 1; return;
+  }
+  c->last = 0;
+  c->h_att = c->h;
+  if (__dadd_rn(c->t, __dmul_rn(1.01, c->h)) >= c->tf) {
+    c->h_att = __dsub_rn(c->tf, c->t);
+    c->last = 1;
+  }
+}
+
+enum : int { FIN_SOLVE = 0, FIN_STEP = 1 };
+
+struct FinArgs {
+  Bufs B;
+  int S;
+  int nbt;
+  double bt[kMaxStages];
+  int bslot[kMaxStages];
+  int64_t dn;
+  int mode;
+  int k1_elided;
+  int write_xt;
+  int has_handle;
+  cudaGraphConditionalHandle handle;
+};
+
+constexpr int kFinThreads = 256;
+
+__device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+__global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
+  Ctl* c = f.B.ctl;
+  const bool dead = c->done != 0;
+  const bool stage_nf = c->nf_mask != 0;
+  __shared__ double red[kFinThreads / 32];
+  __shared__ int red_nf[kFinThreads / 32];
+  double m = 0.0;
+  bool nf = false;
+  if (!dead && !stage_nf) {
+    const int ix = c->ix, k1i = c->k1i;
+    const double* x = f.B.xb[ix];
+    const double* xst = f.B.xb[ix ^ 1];
+    const double* xnx = c->store32 ? f.B.xn : xst;
+    const double h = c->h_att;
+    const double floor_w = __ddiv_rn(c->abs_tol, c->rel_tol);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < f.dn; e += (int64_t)gridDim.x * blockDim.x) {
+      // x_tilde = x + h * (sum b~_l k_l), solver.cpp:188-199
+      double comb = __dmul_rn(f.bt[0], resolve_slot(f.B, f.S, f.bslot[0], k1i)[e]);
+      for (int t = 1; t < f.nbt; ++t)
+        comb = __dadd_rn(comb, __dmul_rn(f.bt[t], resolve_slot(f.B, f.S, f.bslot[t], k1i)[e]));
+      const double xt = __dadd_rn(x[e], __dmul_rn(h, comb));
+      if (f.write_xt) f.B.xt[e] = xt;
+      const double xn = xnx[e];
+      nf |= !isfinite(xn) || !isfinite(xt) || !isfinite(xst[e]);
+      // estimate_error, solver.cpp:399-411
+      const double w = fmax(fmax(fabs(x[e]), fabs(xn)), floor_w);
+      m = fmax(m, __ddiv_rn(fabs(__dsub_rn(xn, xt)), w));
+    }
+  }
+  for (int o = 16; o >= 1; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    nf = __any_sync(0xffffffffu, nf);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { red[warp] = m; red_nf[warp] = nf; }
+  __syncthreads();
+  __shared__ bool is_last;
+  if (threadIdx.x == 0) {
+    double bm = 0.0;
+    int bnf = 0;
+    for (int w = 0; w < kFinThreads / 32; ++w) { bm = fmax(bm, red[w]); bnf |= red_nf[w]; }
+    f.B.part[blockIdx.x] = bm;
+    if (bnf) atomicOr(&c->any_nonfinite, 1);
+    __threadfence();
+    const unsigned t = atomicAdd(&c->ticket, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last || threadIdx.x != 0) return;
+  __threadfence();
+  c->ticket = 0;
+  const bool any_nf = atomicAdd(&c->any_nonfinite, 0) != 0;
+  c->any_nonfinite = 0;
+
+  if (f.mode == FIN_SOLVE && dead) {
+    if (f.has_handle) cudaGraphSetConditional(f.handle, 0);
+    return;
+  }
+  // the need_k1 recompute of this attempt (solver.cpp:298-306)
+  if (f.mode == FIN_SOLVE && c->need_k1) {
+    if (f.k1_elided) c->evals_k1 += 1;
+    else if (c->nf_mask & 1) {
+      c->status = MS_NON_FINITE;
+      c->done = 1;
+      c->nf_mask = 0;
+      if (f.has_handle) cudaGraphSetConditional(f.handle, 0);
+      return;
+    }
+  }
+  double err = nan64(), h_next;
+  bool accepted = false;
+  const double h = c->h_att;
+  if (stage_nf || any_nf) {
+    h_next = __dmul_rn(__dmul_rn(h, c->fac_min), 0.5);  // solver.cpp:158-162, 201-211
+  } else {
+    double e = 0.0;
+    const int nb = gridDim.x;
+    for (int b = 0; b < nb; ++b) e = fmax(e, f.B.part[b]);
+    err = e;
+    if (!isfinite(err)) {
+      h_next = __dmul_rn(__dmul_rn(h, c->fac_min), 0.5);
+    } else {
+      accepted = err <= c->rel_tol;  // solver.cpp:212
+      h_next = d_adjust_step(h, err, c->rel_tol, c->safety, c->fac_min, c->fac_max, c->ctrl_exp);
+    }
+  }
+  c->err = err;
+  c->accepted = accepted;
+  c->h_next = h_next;
+  if (f.mode == FIN_STEP) {
+    return;  // bs32_step: nf_mask is read back by the host
+  }
+  c->attempts += 1;
+  if (c->record_log) {
+    if (c->log_count < c->log_capacity) {
+      StepLogRec& r = f.B.log[c->log_count];
+      r.t = c->t; r.h = h; r.err = err; r.accepted = accepted;
+    }
+    c->log_count += 1;
+  }
+  c->need_k1 = 0;
+  c->nf_mask = 0;
+  if (accepted) {  // solver.cpp:321-336
+    c->n_acc += 1;
+    c->ix ^= 1;
+    const double tn = __dadd_rn(c->t, h);
+    c->t = c->last ? c->tf : (c->store32 ? rn32(tn) : tn);
+    c->k1i = f.S - c->k1i;  // FSAL: k1 <- k_last
+    c->h = h_next;
+    if (c->t >= c->tf) {
+      c->status = MS_COMPLETED;
+      c->done = 1;
+    }
+  } else {  // solver.cpp:337-341
+    c->n_fail += 1;
+    c->h = h_next;
+    c->need_k1 = 1;
+  }
+  if (!c->done) loop_check(c);
+  if (f.has_handle) cudaGraphSetConditional(f.handle, c->done ? 0 : 1);
+}
+
+// ------------------------------------------------------------------------------
+// initial_step (solver.cpp:420-451). The per-element terms are formed in
+// parallel; each of the three sums is then added by one thread in ascending
+// order (the oracle's fixed order).
+struct InitArgs {
+  Bufs B;
+  const double* x0;
+  int64_t dn;
+  double exponent;  // 1/(order+1)
+};
+
+__device__ double seq_sum(const double* v, int64_t n) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s = __dadd_rn(s, v[i]);
+  return s;
+}
+
+__global__ void __launch_bounds__(1024) k_init_a(InitArgs a) {
+  Ctl* c = a.B.ctl;
+  if (c->done) return;
+  __shared__ int nf;
+  if (threadIdx.x == 0) nf = 0;
+  __syncthreads();
+  const double* f0 = a.B.kb[1];
+  double* t0 = a.B.scratch;
+  double* t1 = a.B.xn;
+  bool mynf = false;
+  for (int64_t e = threadIdx.x; e < a.dn; e += blockDim.x) {
+    const double sk = __dadd_rn(c->abs_tol, __dmul_rn(c->rel_tol, fabs(a.x0[e])));
+    const double q0 = __ddiv_rn(a.x0[e], sk);
+    const double q1 = __ddiv_rn(f0[e], sk);
+    t0[e] = __dmul_rn(q0, q0);
+    t1[e] = __dmul_rn(q1, q1);
+    mynf |= !isfinite(f0[e]);
+  }
+  if (mynf) atomicOr(&nf, 1);
+  __syncthreads();
+  __shared__ double s01[2];
+  if (threadIdx.x == 0) s01[0] = seq_sum(t0, a.dn);
+  if (threadIdx.x == 32) s01[1] = seq_sum(t1, a.dn);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  c->cap = __ddiv_rn(__dsub_rn(c->tf, c->t0), 10.0);
+  if (nf) {  // solver.cpp:426
+    c->h = nan64();
+    c->init_skip2 = 1;
+    return;
+  }
+  const double inv_n = __ddiv_rn(1.0, (double)a.dn);
+  const double d0 = __dsqrt_rn(__dmul_rn(s01[0], inv_n));
+  const double d1 = __dsqrt_rn(__dmul_rn(s01[1], inv_n));
+  c->d1 = d1;
+  if (d1 < 1e-12) {
+    c->h = c->cap;
+    c->init_skip2 = 1;
+    return;
+  }
+  c->h1 = (d0 >= 1e-8) ? __ddiv_rn(__dmul_rn(0.01, d0), d1) : 1e-6;
+  c->init_skip2 = 0;
+}
+
+__global__ void __launch_bounds__(1024) k_init_b(InitArgs a) {
+  Ctl* c = a.B.ctl;
+  if (c->done) return;
+  const bool skip2 = c->init_skip2 != 0;
+  __shared__ int nf;
+  if (threadIdx.x == 0) nf = 0;
+  __syncthreads();
+  const double* f0 = a.B.kb[1];
+  const double* f1 = a.B.kb[2];
+  double* t2 = a.B.scratch;
+  if (!skip2) {
+    bool mynf = false;
+    for (int64_t e = threadIdx.x; e < a.dn; e += blockDim.x) {
+      const double sk = __dadd_rn(c->abs_tol, __dmul_rn(c->rel_tol, fabs(a.x0[e])));
+      const double q2 = __ddiv_rn(__dsub_rn(f1[e], f0[e]), sk);
+      t2[e] = __dmul_rn(q2, q2);
+      mynf |= !isfinite(f1[e]);
+    }
+    if (mynf) atomicOr(&nf, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double h0;
+  if (skip2) {
+    h0 = c->h;
+  } else {
+    const double h1 = c->h1;
+    double h2;
+    if (nf) {
+      h2 = __dmul_rn(h1, 1e-3);
+    } else {
+      const double inv_n = __ddiv_rn(1.0, (double)a.dn);
+      const double d2 = __ddiv_rn(__dsqrt_rn(__dmul_rn(seq_sum(t2, a.dn), inv_n)), h1);
+      const double der = c->d1 < d2 ? d2 : c->d1;  // std::max
+      h2 = der < 1e-12 ? c->cap : pow(__ddiv_rn(0.01, der), a.exponent);
+    }
+    // std::min({100*h1, h2, cap})
+    h0 = __dmul_rn(100.0, h1);
+    if (h2 < h0) h0 = h2;
+    if (c->cap < h0) h0 = c->cap;
+  }
+  c->h = h0;
+  c->init_skip2 = 0;
+  if (!isfinite(h0)) {  // solver.cpp:256-259
+    c->status = MS_NON_FINITE;
+    c->done = 1;
+  }
+}
+
+// after the cold k1 (solver.cpp:263-269) and before the first attempt
+__global__ void k_loop_head(Ctl* c) {
+  if (c->done) return;
+  if (c->nf_mask & 1) {
+    c->status = MS_NON_FINITE;
+    c->done = 1;
+    c->nf_mask = 0;
+    return;
+  }
+  c->nf_mask = 0;
+  loop_check(c);
+}
+
+__global__ void k_stamp_start(Ctl* c) { c->t_start_ns = globaltimer_ns(); }
+
+#endif  // MS_DEFINE_STEP_KERNELS
+
+}  // namespace msb

@@ -1,0 +1,63 @@
+// ms_rhs_fast.cu — instantiation and launch of k_rhs_fast for every
+// (model, SS, GS, K storage) combination a policy row can ask for.
+#include <stdexcept>
+#include <string>
+
+#include "ms_dispatch.h"
+
+namespace msb {
+
+namespace {
+
+template <int MODEL, bool SPLIT, class SS, class GS, int KS>
+void go(const RhsLaunch& L, const RhsArgs& a) {
+  auto kern = k_rhs_fast<MODEL, SPLIT, SS, GS, KS>;
+  constexpr size_t smem = fast_smem_bytes<GS, SPLIT>();
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_fast attribute: ") + cudaGetErrorString(e));
+    attr_done = true;
+  }
+  const int rows = a.row1 - a.row0;
+  const int grid = rows < L.num_sms ? rows : L.num_sms;
+  kern<<<grid, kFastThreads, smem, L.stream>>>(a);
+}
+
+template <int MODEL, bool SPLIT, class SS, class GS>
+void by_k(const RhsLaunch& L, const RhsArgs& a) {
+  switch (L.ks) {
+    case MS_K_SCALAR: go<MODEL, SPLIT, SS, GS, MS_K_SCALAR>(L, a); break;
+    case MS_K_F32: go<MODEL, SPLIT, SS, GS, MS_K_F32>(L, a); break;
+    case MS_K_F16: go<MODEL, SPLIT, SS, GS, MS_K_F16>(L, a); break;
+    case MS_K_BF16: go<MODEL, SPLIT, SS, GS, MS_K_BF16>(L, a); break;
+    default: throw std::invalid_argument("rhs_fast: bad K storage");
+  }
+}
+
+template <int MODEL, bool SPLIT>
+void by_prec(const RhsLaunch& L, const RhsArgs& a) {
+  if (L.ss32) {
+    if (L.gs32) by_k<MODEL, SPLIT, float, float>(L, a);
+    else by_k<MODEL, SPLIT, float, double>(L, a);
+  } else {
+    if (L.gs32) by_k<MODEL, SPLIT, double, float>(L, a);
+    else by_k<MODEL, SPLIT, double, double>(L, a);
+  }
+}
+
+}  // namespace
+
+void launch_rhs_fast(const RhsLaunch& L, const RhsArgs& a) {
+  switch (L.model) {
+    case MD_LCO: by_prec<MD_LCO, false>(L, a); break;
+    case MD_KUR:
+      if (!L.split) throw std::invalid_argument("rhs_fast: Kuramoto runs split");
+      by_prec<MD_KUR, true>(L, a);
+      break;
+    case MD_CC: by_prec<MD_CC, false>(L, a); break;
+    default: throw std::invalid_argument("rhs_fast: bad model");
+  }
+}
+
+}  // namespace msb

@@ -1,0 +1,230 @@
+"""BS3(2) solver API on the B200 — mirror of proj/include/mixedstep/solver.hpp
+(SolverConfig :39-61, SolveStatus :63-71, StepOutcome :75-86, StepRecord :88-93,
+FlopTally :104-113, SolveResult :115-126, and the entry points :128-163).
+
+Config errors raise ``ValueError`` where the reference throws
+``std::invalid_argument`` (solver.cpp:217-224); numerical failure is reported
+in ``SolveResult.status`` and never raised (solver.hpp:151-153).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import _abi
+from .precision import PrecisionPolicy
+from .systems import DeviceSystem
+
+kSchemeFlopsBs32 = 30  # solver.hpp:37
+
+
+class SolveStatus(enum.IntEnum):  # solver.hpp:63-71
+    Completed = _abi.MS_COMPLETED
+    MaxIterations = _abi.MS_MAX_ITERATIONS
+    MaxFailedSteps = _abi.MS_MAX_FAILED_STEPS
+    WallClock = _abi.MS_WALL_CLOCK
+    SlowSolver = _abi.MS_SLOW_SOLVER
+    StepTooSmall = _abi.MS_STEP_TOO_SMALL
+    NonFinite = _abi.MS_NON_FINITE
+
+
+def status_name(s: SolveStatus) -> str:
+    return SolveStatus(s).name
+
+
+@dataclass
+class SolverConfig:  # solver.hpp:39-61
+    rel_tol: float = 1e-6
+    abs_tol: float = 1e-8
+    h_min_factor: float = 100.0
+    max_iterations: int = 100000
+    max_failed_steps: int = 85000
+    time_limits_enabled: bool = True
+    wall_clock_limit: float = 5400.0
+    slow_solver_elapsed: float = 2700.0
+    slow_solver_progress: float = 0.10
+    safety: float = 0.9
+    fac_min: float = 0.2
+    fac_max: float = 5.0
+    controller_exponent: float = 1.0 / 3.0
+    record_step_log: bool = True
+    record_snapshots: bool = False
+
+    def c(self) -> _abi.SolverConfigC:
+        c = _abi.SolverConfigC()
+        for f in fields(self):
+            v = getattr(self, f.name)
+            setattr(c, f.name, int(v) if isinstance(v, bool) else v)
+        return c
+
+
+@dataclass
+class StepRecord:  # solver.hpp:88-93
+    t: float
+    h: float
+    err: float
+    accepted: bool
+
+
+@dataclass
+class FlopTally:  # solver.hpp:104-113
+    low: int = 0
+    high: int = 0
+    rhs_evals: int = 0
+
+    def low_fraction(self) -> float:
+        tot = float(self.low) + float(self.high)
+        return float(self.low) / tot if tot > 0 else 0.0
+
+
+@dataclass
+class SolveResult:  # solver.hpp:115-126
+    status: SolveStatus
+    final_state: np.ndarray
+    t_reached: float
+    n_accepted: int
+    n_failed: int
+    step_log: list
+    flops: FlopTally
+    device_ms: float = 0.0
+    step_log_count: int = 0
+
+    def total_steps(self) -> int:
+        return self.n_accepted + self.n_failed
+
+
+@dataclass
+class StepOutcome:  # solver.hpp:75-86
+    x_next: np.ndarray
+    x_tilde: np.ndarray
+    err: float
+    accepted: bool
+    k4: np.ndarray
+    x_store: np.ndarray
+    h_used: float
+    h_next: float
+    flops: FlopTally = field(default_factory=FlopTally)
+
+
+def _f64(x):
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def estimate_error(x_n, x_next, x_tilde, ab: float, rel: float) -> float:
+    """solver.cpp:399-411 (device reduction)."""
+    a, b, c = _f64(x_n), _f64(x_next), _f64(x_tilde)
+    if not (a.shape == b.shape == c.shape):
+        raise ValueError("estimate_error: length mismatch")
+    out = C.c_double()
+    _abi.check(_abi.lib().ms_estimate_error(a.size, _abi.dptr(a), _abi.dptr(b), _abi.dptr(c), ab, rel,
+                                            C.byref(out)), "ms_estimate_error")
+    return out.value
+
+
+def adjust_step(h: float, err: float, rel_tol: float, cfg: SolverConfig) -> float:
+    """solver.cpp:413-418 (device arithmetic)."""
+    out = C.c_double()
+    cc = cfg.c()
+    _abi.check(_abi.lib().ms_adjust_step(h, err, rel_tol, C.byref(cc), C.byref(out)), "ms_adjust_step")
+    return out.value
+
+
+def initial_step(sys: DeviceSystem, t0: float, t_final: float, x0, cfg: SolverConfig, order: int = 3,
+                 tally: FlopTally | None = None) -> float:
+    """solver.cpp:420-451: two binary64 evaluations on the device."""
+    x0 = _f64(x0)
+    h0 = C.c_double()
+    ev = C.c_int64()
+    cc = cfg.c()
+    _abi.check(_abi.lib().ms_initial_step(sys.handle, t0, t_final, _abi.dptr(x0), C.byref(cc), order,
+                                          C.byref(h0), C.byref(ev)), "ms_initial_step")
+    if tally is not None:
+        tally.rhs_evals += ev.value
+    return h0.value
+
+
+def bs32_step(sys: DeviceSystem, t: float, x_n, h: float, k1, policy: PrecisionPolicy,
+              cfg: SolverConfig) -> StepOutcome:
+    """One BS3(2) attempt with supplied k1 (solver.cpp:453-460)."""
+    x_n, k1 = _f64(x_n), _f64(k1)
+    n = x_n.size
+    bufs = [np.empty(n) for _ in range(4)]
+    o = _abi.StepOutcomeC()
+    o.x_next, o.x_tilde, o.k4, o.x_store = (_abi.dptr(b) for b in bufs)
+    pol, cc = policy.c(), cfg.c()
+    _abi.check(_abi.lib().ms_bs32_step(sys.handle, t, _abi.dptr(x_n), h, _abi.dptr(k1), C.byref(pol),
+                                       C.byref(cc), C.byref(o)), "ms_bs32_step")
+    return StepOutcome(bufs[0], bufs[1], o.err, bool(o.accepted), bufs[2], bufs[3], o.h_used, o.h_next,
+                       FlopTally(o.flops_low, o.flops_high, o.rhs_evals))
+
+
+def _result(r: _abi.SolveResultC, final: np.ndarray, log: np.ndarray | None) -> SolveResult:
+    steps = []
+    if log is not None:
+        m = min(len(log), r.step_log_count)
+        steps = [StepRecord(float(e.t), float(e.h), float(e.err), bool(e.accepted)) for e in log[:m]]
+    return SolveResult(SolveStatus(r.status), final, r.t_reached, r.n_accepted, r.n_failed, steps,
+                       FlopTally(r.flops_low, r.flops_high, r.rhs_evals), r.device_ms, r.step_log_count)
+
+
+def _log_buffer(cfg: SolverConfig, capacity: int | None):
+    if not cfg.record_step_log:
+        return None, None
+    cap = int(capacity if capacity is not None else min(cfg.max_iterations, 1 << 20))
+    arr = (_abi.StepRecordC * max(cap, 1))()
+    return arr, cap
+
+
+def solve(sys: DeviceSystem, x0, t0: float, t_final: float, policy: PrecisionPolicy, cfg: SolverConfig,
+          log_capacity: int | None = None) -> SolveResult:
+    """Adaptive BS3(2) solve (solver.cpp:462-470); the step loop runs on the device."""
+    x0 = _f64(x0)
+    final = np.empty_like(x0)
+    log, cap = _log_buffer(cfg, log_capacity)
+    r = _abi.SolveResultC()
+    r.final_state = _abi.dptr(final)
+    if log is not None:
+        r.step_log = C.cast(log, C.POINTER(_abi.StepRecordC))
+        r.step_log_capacity = cap
+    pol, cc = policy.c(), cfg.c()
+    _abi.check(_abi.lib().ms_solve(sys.handle, _abi.dptr(x0), t0, t_final, C.byref(pol), C.byref(cc),
+                                   C.byref(r)), "ms_solve")
+    return _result(r, final, log)
+
+
+def solve_device(sys: DeviceSystem, x0_dev_ptr: int, final_dev_ptr: int, t0: float, t_final: float,
+                 policy: PrecisionPolicy, cfg: SolverConfig, stream: int = 0,
+                 log_capacity: int | None = 0) -> SolveResult:
+    """solve() on device-resident buffers (raw CUDA pointers, e.g. torch
+    ``tensor.data_ptr()``); ``stream`` is a cudaStream_t handle or 0."""
+    log, cap = _log_buffer(cfg, log_capacity) if log_capacity else (None, None)
+    r = _abi.SolveResultC()
+    r.final_state = C.cast(C.c_void_p(final_dev_ptr), _abi._DP)
+    if log is not None:
+        r.step_log = C.cast(log, C.POINTER(_abi.StepRecordC))
+        r.step_log_capacity = cap
+    pol, cc = policy.c(), cfg.c()
+    _abi.check(_abi.lib().ms_solve_device(sys.handle, C.c_void_p(x0_dev_ptr), t0, t_final, C.byref(pol),
+                                          C.byref(cc), C.byref(r), C.c_void_p(stream)), "ms_solve_device")
+    return _result(r, np.empty(0), log)
+
+
+def dp54_reference(sys: DeviceSystem, x0, t0: float, t_final: float, cfg: SolverConfig | None = None,
+                   log_capacity: int | None = None) -> SolveResult:
+    """All-binary64 DP5(4) at rel = abs = 1e-9 (solver.cpp:472-483), on the device."""
+    cfg = cfg or SolverConfig()
+    x0 = _f64(x0)
+    final = np.empty_like(x0)
+    log, cap = _log_buffer(cfg, log_capacity)
+    r = _abi.SolveResultC()
+    r.final_state = _abi.dptr(final)
+    if log is not None:
+        r.step_log = C.cast(log, C.POINTER(_abi.StepRecordC))
+        r.step_log_capacity = cap
+    cc = cfg.c()
+    _abi.check(_abi.lib().ms_dp54_reference(sys.handle, _abi.dptr(x0), t0, t_final, C.byref(cc), C.byref(r)),
+               "ms_dp54_reference")
+    return _result(r, final, log)

@@ -1,0 +1,153 @@
+"""Device eval_rhs (the all-pairs hot path, systems.cpp:30-64) against the CPU
+oracle on the same seeded inputs, through the C-ABI.
+
+FAITHFUL mode sums in the reference's exact order: transcendental-free paths
+(LCO) must be bit-identical; sin/atan paths may differ by the libm-vs-device
+ulp of G only. FAST mode reorders the j-sum (blocked warp tree, Kuramoto
+sin/cos split): it is held to the worst-case bound of reordering a sum in the
+accumulation format, TOL = 2 N eps_SS mw sum_j |G_ij| + 4 eps_WS |out|.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from paper_2605_23727_b200.configs import TWO_PI, rng_uniform
+from paper_2605_23727_b200.precision import B32, B64, StagePrecision
+from paper_2605_23727_b200.systems import DeviceSystem, SystemSpec
+
+pytestmark = pytest.mark.gpu
+
+ALL_ROWS = [StagePrecision(f, s, g) for f, s, g in itertools.product((B32, B64), repeat=3)]
+
+
+def eps(fmt):
+    return 2.0 ** -23 if fmt == B32 else 2.0 ** -52
+
+
+def pair(spec):
+    return DeviceSystem(spec), O.OracleSystem(spec)
+
+
+def kur_spec(n, k_storage="f32", mode="fast", seed=11, coupling_k=1.0):
+    om = rng_uniform(seed, 0, n, -1.0, 1.0)
+    kw = {} if k_storage == "scalar" else {"k_uniform": (seed, 2, 0.0, 2.0)}
+    return SystemSpec("kuramoto", n, k_storage=k_storage, rhs_mode=mode, omega=om, coupling_k=coupling_k, **kw)
+
+
+def reorder_tol(sp, n, out, gabs_rowsum):
+    ws = B32 if (sp.f_prec == B32 and sp.sum_prec == B32) else B64
+    tol = 2.0 * n * eps(sp.sum_prec) * gabs_rowsum / n + 4.0 * eps(ws) * np.abs(out)
+    if sp.g_prec == B32:
+        tol = tol + 4.0 * eps(B32) * gabs_rowsum / n  # product rounded in GS
+    return tol + 1e-300
+
+
+@pytest.mark.parametrize("n", [1, 2, 17, 100, 513])
+@pytest.mark.parametrize("sp", ALL_ROWS, ids=str)
+def test_lco_reference_form_faithful_bitwise(gpu, n, sp):
+    """make_lco (systems.cpp:209-218) + eval_core order: bit-identical."""
+    spec = SystemSpec("lco", n, rhs_mode="faithful", coupling_k=1.0)
+    dev, orc = pair(spec)
+    x = rng_uniform(99, 0, 2 * n, -2.0, 2.0)
+    assert np.array_equal(dev.eval_rhs(0.0, x, sp), orc.eval_rhs(0.0, x, sp))
+
+
+@pytest.mark.parametrize("k_storage", ["f32", "f16", "bf16"])
+@pytest.mark.parametrize("sp", ALL_ROWS, ids=str)
+def test_lco_config1_dense_faithful_bitwise(gpu, k_storage, sp):
+    """C1 form (coupling on the velocity slot, w_i^2, dense symmetric K)."""
+    from paper_2605_23727_b200.configs import config1_lco
+    w = config1_lco(n=96, k_storage=k_storage, rhs_mode="faithful")
+    dev, orc = pair(w.spec)
+    assert np.array_equal(dev.get_k(), orc.get_k())
+    assert np.array_equal(dev.eval_rhs(0.0, w.x0, sp), orc.eval_rhs(0.0, w.x0, sp))
+
+
+@pytest.mark.parametrize("n", [1, 7, 64, 300])
+@pytest.mark.parametrize("sp", ALL_ROWS, ids=str)
+def test_kuramoto_faithful(gpu, n, sp):
+    """Order-faithful Kuramoto: only the sin of G can differ (<= 1 ulp of G per pair)."""
+    spec = kur_spec(n, "f32", "faithful")
+    dev, orc = pair(spec)
+    x = rng_uniform(5, 1, n, 0.0, TWO_PI)
+    a, b = dev.eval_rhs(0.0, x, sp), orc.eval_rhs(0.0, x, sp)
+    gsum = np.abs(orc.get_k()).sum(axis=1)
+    ws = B32 if (sp.f_prec == B32 and sp.sum_prec == B32) else B64
+    # a differing sin moves one term by <= 2 ulp(GS); the sequential sum can
+    # then round differently at each later add (<= N ulp(SS) of the row scale)
+    tol = (2.0 * eps(sp.g_prec) + 2.0 * n * eps(sp.sum_prec)) * gsum / n + 4.0 * eps(ws) * np.abs(b)
+    assert np.all(np.abs(a - b) <= tol + 1e-300), float(np.max(np.abs(a - b) / (tol + 1e-300)))
+
+
+@pytest.mark.parametrize("k_storage", ["scalar", "f32", "f16", "bf16"])
+@pytest.mark.parametrize("n", [1, 3, 64, 1000, 4096])
+@pytest.mark.parametrize("sp", ALL_ROWS, ids=str)
+def test_kuramoto_fast_split(gpu, k_storage, n, sp):
+    """Fast path (sin/cos split, blocked sum) vs the oracle's split semantics."""
+    if n == 4096 and k_storage == "bf16" and sp.g_prec == B64:
+        pytest.skip("covered by the other storage formats")
+    spec = kur_spec(n, k_storage, "fast", coupling_k=1.3)
+    dev, orc = pair(spec)
+    x = rng_uniform(6, 1, n, 0.0, 50.0)
+    a, b = dev.eval_rhs(0.0, x, sp), orc.eval_rhs(0.0, x, sp)
+    gsum = (np.abs(orc.get_k()).sum(axis=1) if k_storage != "scalar" else np.full(n, 1.3 * n)) * 2.0
+    tol = reorder_tol(sp, n, b, gsum)
+    assert np.all(np.abs(a - b) <= tol), float(np.max(np.abs(a - b) / tol))
+
+
+@pytest.mark.parametrize("mode", ["fast", "faithful"])
+@pytest.mark.parametrize("k_storage", ["scalar", "f32", "f16"])
+@pytest.mark.parametrize("sp", ALL_ROWS, ids=str)
+def test_cc(gpu, mode, k_storage, sp):
+    from paper_2605_23727_b200.configs import config3_cc
+    w = config3_cc(n=200, k_storage=k_storage if k_storage != "scalar" else "f32", rhs_mode=mode)
+    spec = w.spec
+    if k_storage == "scalar":
+        spec.k_storage, spec.k_uniform, spec.coupling_k = "scalar", None, 0.8
+    dev, orc = pair(spec)
+    x = w.x0
+    a, b = dev.eval_rhs(0.0, x, sp), orc.eval_rhs(0.0, x, sp)
+    n = spec.n_agents
+    K = orc.get_k() if k_storage != "scalar" else np.full((n, n), 0.8)
+    pref = 2.0 * 2.0 * 2.0  # |k0 th a/(th+x2^4)| <= k0 a
+    gsum = np.abs(K).sum(axis=1) * 1.6 * pref
+    tol = np.repeat(reorder_tol(sp, n, b[0::4], gsum), 4)
+    tol = np.maximum(tol, 4.0 * eps(B32 if sp.f_prec == B32 else B64) * (np.abs(b) + 1.0))
+    assert np.all(np.abs(a - b) <= tol), float(np.max(np.abs(a - b) / tol))
+    # uncoupled slots are F alone: identical formula, identical order
+    for s in (1, 2, 3):
+        assert np.array_equal(a[s::4], b[s::4])
+
+
+def test_device_k_generation_bit_identical(gpu):
+    for ks in ("f32", "f16", "bf16"):
+        spec = kur_spec(333, ks)
+        dev, orc = pair(spec)
+        assert np.array_equal(dev.get_k(), orc.get_k())
+
+
+def test_host_k_upload_bit_identical(gpu):
+    n = 77
+    K = rng_uniform(3, 2, n * n, -3.0, 3.0).reshape(n, n)
+    for ks in ("f32", "f16", "bf16"):
+        for host in (K, K.astype(np.float32)):
+            spec = SystemSpec("kuramoto", n, k_storage=ks, omega=np.zeros(n), K=host)
+            dev, orc = pair(spec)
+            assert np.array_equal(dev.get_k(), orc.get_k())
+
+
+def test_row_sharded_rhs_is_bitwise_the_unsharded_rows(gpu):
+    """Each row's reduction order depends only on N: a row-range handle
+    (one rank of a row-sharded K) reproduces the full evaluation bitwise."""
+    n = 1000
+    full = DeviceSystem(kur_spec(n, "f32"))
+    x = rng_uniform(8, 1, n, 0.0, TWO_PI)
+    ref = full.eval_rhs(0.0, x, StagePrecision(B32, B32, B32))
+    for r0, r1 in ((0, 250), (250, 500), (500, 999), (999, 1000)):
+        spec = kur_spec(n, "f32")
+        spec.row_begin, spec.row_end = r0, r1
+        part = DeviceSystem(spec)
+        got = part.eval_rhs(0.0, x, StagePrecision(B32, B32, B32))
+        assert np.array_equal(got[r0:r1], ref[r0:r1])

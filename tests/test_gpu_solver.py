@@ -1,0 +1,261 @@
+"""The device-resident BS3(2) loop against the oracle and the reference KATs,
+through the C-ABI. The KATs are those of proj/tests/test_solver.cpp, run on the
+reference's own test fixtures (ScalarExp/Zero/Nan) as device systems."""
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from paper_2605_23727_b200 import solver as S
+from paper_2605_23727_b200.configs import TWO_PI, config1_lco, config2_kuramoto, config3_cc, reference_ic, rng_uniform
+from paper_2605_23727_b200.precision import (B32, B64, DDD, PolicyVariant, custom_policy, kAllBinary32,
+                                             kAllBinary64, policy_for)
+from paper_2605_23727_b200.solver import SolverConfig, SolveStatus
+from paper_2605_23727_b200.systems import DeviceSystem, SystemSpec, make_kuramoto, make_lco, scalar_fixture
+
+pytestmark = pytest.mark.gpu
+GOLD = json.loads((Path(__file__).parent / "golden" / "reference_kats.json").read_text())
+PI = 3.14159265358979323846
+D = policy_for(PolicyVariant.Double)
+
+
+def test_estimate_error_kats(gpu):  # test_solver.cpp:55-75
+    assert S.estimate_error([0.0], [0.0], [0.0], 1e-2, 1.0) == 0.0
+    assert S.estimate_error([0.0], [0.0], [1e-6], 1e-2, 1.0) == pytest.approx(1e-4, rel=1e-12)
+    xn, xnext, xt = np.array([2.0, -3.0]), np.array([2.1, -3.1]), np.array([2.1000004, -3.0999996])
+    assert S.estimate_error(xn, xnext, xt, 1e-8, 1e-2) == pytest.approx(
+        S.estimate_error(10 * xn, 10 * xnext, 10 * xt, 1e-8, 1e-2), rel=1e-9)
+    with pytest.raises(ValueError):
+        S.estimate_error([0.0], [0.0], [0.0, 1.0], 1e-2, 1.0)
+    # bit-identical to the oracle on a large random case
+    a, b = rng_uniform(1, 0, 100000, -5, 5), rng_uniform(2, 0, 100000, -5, 5)
+    c = b + rng_uniform(3, 0, 100000, -1e-5, 1e-5)
+    assert S.estimate_error(a, b, c, 1e-9, 1e-6) == O.estimate_error(a, b, c, 1e-9, 1e-6)
+
+
+def test_adjust_step_kats(gpu):  # test_solver.cpp:77-87
+    cfg = SolverConfig()
+    tol = cfg.rel_tol
+    assert S.adjust_step(1.0, tol, tol, cfg) == pytest.approx(0.9, rel=1e-15)
+    assert S.adjust_step(2.0, 8.0 * tol, tol, cfg) == pytest.approx(0.9, rel=1e-14)
+    assert S.adjust_step(1.0, 0.0, tol, cfg) == 5.0
+    assert S.adjust_step(1.0, 1e9 * tol, tol, cfg) == 0.2
+    assert S.adjust_step(1.0, 1e-12 * tol, tol, cfg) == 5.0
+    for err in rng_uniform(4, 0, 200, 1e-9, 1e-5):
+        a, b = S.adjust_step(0.01, err, tol, cfg), O.adjust_step(0.01, err, tol, cfg)
+        assert abs(a - b) <= 2 * 2.0 ** -52 * abs(b)  # device pow vs glibc pow: <= 2 ulp
+
+
+def test_initial_step_kats(gpu):  # test_solver.cpp:89-109
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-8)
+    assert S.initial_step(scalar_fixture("zero"), 0.0, 5.0, [1.0], cfg) == 0.5
+    assert 0.0 < S.initial_step(scalar_fixture("exp"), 0.0, 1.0, [1.0], cfg) <= 0.1
+    assert 0.0 < S.initial_step(scalar_fixture("exp"), 0.0, 50.0, [1.0], cfg) <= 0.1
+    assert math.isnan(S.initial_step(scalar_fixture("nan"), 0.0, 1.0, [1.0], cfg))
+
+
+def test_bs32_step_exp_kat(gpu):  # test_solver.cpp:111-133
+    g = GOLD["bs32_exp_step"]
+    sys = scalar_fixture("exp")
+    o = S.bs32_step(sys, 0.0, [1.0], 0.1, [1.0], D, SolverConfig(rel_tol=1e-2, abs_tol=1e-2))
+    assert o.x_next[0] == pytest.approx(g["x_next"], rel=1e-15)
+    assert o.x_tilde[0] == pytest.approx(g["x_tilde"], rel=1e-15)
+    assert o.err == pytest.approx(g["err"], rel=1e-12)
+    assert o.k4[0] == o.x_next[0] and o.accepted
+    o = S.bs32_step(sys, 0.0, [1.0], 0.1, [1.0], D, SolverConfig(rel_tol=1e-2, abs_tol=1e-1))
+    assert o.err == pytest.approx(g["err_floor10"], rel=1e-12)
+
+
+def test_bs32_step_zero_kat(gpu):  # test_solver.cpp:135-148
+    o = S.bs32_step(scalar_fixture("zero"), 0.0, [1.0], 1.0, [0.0], policy_for(PolicyVariant.Single), SolverConfig())
+    assert o.x_next[0] == 1.0 and o.x_tilde[0] == 1.0 and o.err == 0.0 and o.accepted and o.h_next == 5.0
+
+
+def test_solve_to_e(gpu):  # test_solver.cpp:150-168
+    cfg = SolverConfig(rel_tol=1e-8, abs_tol=1e-10)
+    r = S.solve(scalar_fixture("exp"), [1.0], 0.0, 1.0, D, cfg)
+    assert r.status == SolveStatus.Completed and r.t_reached == 1.0
+    assert abs(r.final_state[0] - math.e) / math.e <= 1e-6
+    for rec in r.step_log:
+        assert (rec.err <= cfg.rel_tol) if rec.accepted else (rec.err > cfg.rel_tol or not math.isfinite(rec.err))
+    o = O.solve(O.OracleSystem(SystemSpec("scalar_exp", 1)), [1.0], 0.0, 1.0, D, cfg)
+    assert (r.n_accepted, r.n_failed, r.flops.rhs_evals) == (o.n_accepted, o.n_failed, o.flops.rhs_evals)
+    assert abs(r.final_state[0] - o.final_state[0]) <= 4e-16 * abs(o.final_state[0])
+
+
+def test_fsal_budget_and_bitwise_k4(gpu):  # test_solver.cpp:213-237
+    cfg = SolverConfig(rel_tol=1e-5, abs_tol=1e-7)
+    r = S.solve(scalar_fixture("exp"), [1.0], 0.0, 1.0, D, cfg)
+    assert r.status == SolveStatus.Completed and r.n_failed == 0
+    assert r.flops.rhs_evals == 3 + 3 * r.n_accepted
+    lco = DeviceSystem(SystemSpec("lco", 3, rhs_mode="faithful"))
+    y = np.array([0.3, 1.1, -0.4, 0.2, 1.7, 0.9])
+    pol = policy_for(PolicyVariant.Mixed1)
+    k1 = lco.eval_rhs(0.0, y, pol.first_step_k1)
+    o = S.bs32_step(lco, 0.0, y, 0.005, k1, pol, cfg)
+    assert o.accepted
+    assert np.array_equal(o.k4, lco.eval_rhs(0.005, o.x_next, pol.stage(4)))
+    # and the whole step is bit-identical to the oracle's (transcendental-free)
+    orc = O.OracleSystem(SystemSpec("lco", 3, rhs_mode="faithful"))
+    q = O.bs32_step(orc, 0.0, y, 0.005, k1, pol, cfg)
+    for f in ("x_next", "x_tilde", "k4", "x_store"):
+        assert np.array_equal(getattr(o, f), getattr(q, f)), f
+    assert o.err == q.err and o.accepted == q.accepted
+
+
+@pytest.mark.parametrize("variant", list(PolicyVariant)[:4])
+def test_bs32_step_lco_bitwise_all_policies(gpu, variant):
+    """rk_step + combine_binary32 + estimate_error: identical arithmetic order."""
+    n = 40
+    spec = SystemSpec("lco", n, rhs_mode="faithful")
+    dev, orc = DeviceSystem(spec), O.OracleSystem(spec)
+    x = rng_uniform(12, 1, 2 * n, -1.0, 1.0)
+    pol = policy_for(variant)
+    k1 = orc.eval_rhs(0.0, x, pol.first_step_k1)
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9)
+    for h in (1e-3, 0.05, 0.4):
+        a = S.bs32_step(dev, 0.0, x, h, k1, pol, cfg)
+        b = O.bs32_step(orc, 0.0, x, h, k1, pol, cfg)
+        for f in ("x_next", "x_tilde", "k4", "x_store"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), (f, h)
+        assert a.err == b.err and a.accepted == b.accepted
+        assert abs(a.h_next - b.h_next) <= 2 * 2.0 ** -52 * abs(b.h_next)
+        assert a.flops.rhs_evals == b.flops.rhs_evals == 3
+        assert (a.flops.low, a.flops.high) == (b.flops.low, b.flops.high)
+
+
+def test_nonfinite_stage_outcome(gpu):  # solver.cpp:150-162
+    o = S.bs32_step(scalar_fixture("nan"), 0.0, [1.0], 0.1, [1.0], D, SolverConfig())
+    assert not o.accepted and math.isnan(o.err)
+    assert o.h_next == 0.1 * 0.2 * 0.5
+    assert math.isnan(o.x_next[0]) and math.isnan(o.k4[0])
+
+
+def test_failure_statuses(gpu):  # test_solver.cpp:320-359
+    sys = DeviceSystem(SystemSpec("lco", 4, rhs_mode="faithful"))
+    x0 = rng_uniform(6, 0, 8, 0.0, 2.0)
+    r = S.solve(sys, x0, 0.0, 1e4, D, SolverConfig(rel_tol=1e-8, abs_tol=1e-10, max_iterations=5))
+    assert r.status == SolveStatus.MaxIterations and r.total_steps() <= 5
+    r = S.solve(sys, x0, 0.0, 1e4, D, SolverConfig(rel_tol=1e-8, abs_tol=1e-10, wall_clock_limit=0.0))
+    assert r.status == SolveStatus.WallClock
+    r = S.solve(sys, x0, 0.0, 1e4, D, SolverConfig(rel_tol=1e-8, abs_tol=1e-10, slow_solver_elapsed=0.0))
+    assert r.status == SolveStatus.SlowSolver
+    r = S.solve(scalar_fixture("nan"), [1.0], 0.0, 1.0, D, SolverConfig(rel_tol=1e-8, abs_tol=1e-10))
+    assert r.status == SolveStatus.NonFinite
+    with pytest.raises(ValueError):
+        S.solve(sys, x0, 0.0, 1.0, D, SolverConfig(rel_tol=1e-8, abs_tol=1.0))
+    with pytest.raises(ValueError):
+        S.solve(sys, x0, 1.0, 1.0, D, SolverConfig())
+    r = S.solve(sys, x0, 0.0, 10.0, policy_for(PolicyVariant.Single), SolverConfig(rel_tol=1e-12, abs_tol=1e-14))
+    assert r.status == SolveStatus.StepTooSmall and r.t_reached < 10.0  # test_solver.cpp:183-195
+
+
+def test_max_failed_steps(gpu):
+    sys = DeviceSystem(SystemSpec("lco", 4, rhs_mode="faithful"))
+    x0 = rng_uniform(6, 0, 8, 0.0, 2.0)
+    cfg = SolverConfig(rel_tol=1e-12, abs_tol=1e-14, max_failed_steps=0)
+    r = S.solve(sys, x0, 0.0, 10.0, D, cfg)
+    o = O.solve(O.OracleSystem(SystemSpec("lco", 4, rhs_mode="faithful")), x0, 0.0, 10.0, D, cfg)
+    assert r.status == o.status == SolveStatus.MaxFailedSteps
+
+
+def _same_run(r, o, rtol_state, exact_counts=True):
+    assert r.status == o.status
+    if exact_counts:
+        assert (r.n_accepted, r.n_failed) == (o.n_accepted, o.n_failed)
+    else:
+        for a, b in ((r.n_accepted, o.n_accepted), (r.n_failed, o.n_failed)):
+            assert abs(a - b) <= max(1, 0.01 * b)
+    assert r.t_reached == o.t_reached
+    scale = np.maximum(np.abs(o.final_state), 1e-3)
+    assert np.all(np.abs(r.final_state - o.final_state) <= rtol_state * scale), \
+        float(np.max(np.abs(r.final_state - o.final_state) / scale))
+
+
+def test_lco_periodic_return_and_oracle(gpu):  # test_solver.cpp:170-181
+    sys = DeviceSystem(SystemSpec("lco", 4, rhs_mode="faithful"))
+    x0 = np.tile([1.0, 0.0], 4)
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-8)
+    r = S.solve(sys, x0, 0.0, 2.0 * PI, D, cfg)
+    assert r.status == SolveStatus.Completed and np.all(np.abs(r.final_state - x0) <= 1e-4)
+
+
+def test_all_d_policy_bitwise_equals_double(gpu):  # test_solver.cpp:239-265
+    sys = make_kuramoto(12, 0.6, 0.9, 8, rhs_mode="faithful")
+    x0 = rng_uniform(9, 0, 12, 0.0, 2 * PI)
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-8)
+    a = S.solve(sys, x0, 0.0, 20.0, D, cfg)
+    b = S.solve(sys, x0, 0.0, 20.0, custom_policy((DDD, DDD, DDD), DDD, B64), cfg)
+    assert a.status == b.status and np.array_equal(a.final_state, b.final_state)
+    assert [(s.t, s.h, s.err, s.accepted) for s in a.step_log] == [(s.t, s.h, s.err, s.accepted) for s in b.step_log]
+
+
+def test_determinism(gpu):  # test_solver.cpp:267-291 (repeated device solves are bit-identical)
+    w = config3_cc(n=64, k_storage="f32")
+    sys = DeviceSystem(w.spec)
+    cfg = SolverConfig(rel_tol=1e-5, abs_tol=1e-7, time_limits_enabled=False)
+    pol = policy_for(PolicyVariant.Mixed2)
+    a = S.solve(sys, w.x0, 0.0, 30.0, pol, cfg)
+    b = S.solve(sys, w.x0, 0.0, 30.0, pol, cfg)
+    assert (a.status, a.n_accepted, a.n_failed) == (b.status, b.n_accepted, b.n_failed)
+    assert np.array_equal(a.final_state, b.final_state)
+    assert [s.err for s in a.step_log] == [s.err for s in b.step_log]
+
+
+@pytest.mark.parametrize("variant", list(PolicyVariant)[:4])
+def test_lco_solve_matches_oracle(gpu, variant):
+    """Reference-form LCO, faithful order: same step sequence as the oracle;
+    only pow in the controller may differ by an ulp."""
+    n = 20
+    spec = SystemSpec("lco", n, rhs_mode="faithful")
+    dev, orc = DeviceSystem(spec), O.OracleSystem(spec)
+    x0 = reference_ic("lco", n, 7)
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-8)
+    r = S.solve(dev, x0, 0.0, 10.0 * PI, policy_for(variant), cfg)
+    o = O.solve(orc, x0, 0.0, 10.0 * PI, policy_for(variant), cfg)
+    _same_run(r, o, 1e-10)
+    assert r.flops.rhs_evals == o.flops.rhs_evals
+    assert (r.flops.low, r.flops.high) == (o.flops.low, o.flops.high)
+
+
+def test_dp54_reference(gpu):  # test_solver.cpp:197-211 + oracle parity
+    r = S.dp54_reference(scalar_fixture("exp"), [1.0], 0.0, 1.0)
+    assert r.status == SolveStatus.Completed and abs(r.final_state[0] - math.e) / math.e <= 1e-8
+    spec = SystemSpec("lco", 4, rhs_mode="faithful")
+    y0 = np.tile([1.0, 0.0], 4)
+    p = S.dp54_reference(DeviceSystem(spec), y0, 0.0, 2.0 * PI)
+    q = O.dp54_reference(O.OracleSystem(spec), y0, 0.0, 2.0 * PI)
+    assert p.status == SolveStatus.Completed and np.all(np.abs(p.final_state - y0) <= 1e-7)
+    _same_run(p, q, 1e-12)
+
+
+# ---- BASELINE configs at reduced size: device vs oracle under the same policy ----------
+def _parity(w, rtol_state, exact_counts=False):
+    dev, orc = DeviceSystem(w.spec), O.OracleSystem(w.spec)
+    O.set_threads(8)
+    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg)
+    o = O.solve(orc, w.x0, w.t0, w.tf, w.policy, w.cfg)
+    _same_run(r, o, rtol_state, exact_counts)
+    return r, o
+
+
+@pytest.mark.parametrize("mode", ["faithful", "fast"])
+def test_config1_lco_reduced(gpu, mode):
+    w = config1_lco(n=256, rhs_mode=mode)
+    _parity(w, 1e-5)
+
+
+@pytest.mark.parametrize("ks", ["f32", "f16"])
+def test_config2_kuramoto_reduced(gpu, ks):
+    w = config2_kuramoto(n=512, rtol=1e-6, k_storage=ks)
+    w.tf = 10.0
+    _parity(w, 1e-5)
+
+
+def test_config3_cc_reduced(gpu):
+    w = config3_cc(n=128)
+    w.tf = 24.0
+    _parity(w, 1e-5)
