@@ -23,7 +23,7 @@ LIB = PKG / "libmixedstep_b200.so"
 ORACLE_DIR = ROOT / "oracle"
 
 SOURCES = ["ms_api.cu", "ms_rhs_fast.cu", "ms_rhs_faithful.cu"]
-HEADERS = ["ms_common.cuh", "ms_kernels.cuh", "ms_dispatch.h"]
+HEADERS = ["ms_common.cuh", "ms_kernels.cuh", "ms_dispatch.h", "ms_ddpow.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

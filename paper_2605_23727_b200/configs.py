@@ -101,7 +101,14 @@ def config3_cc(n: int = 2048, seed: int = 2, k_storage: str = "f32", rhs_mode: s
     K_ij ~ U(0,1) on variable 1 and M = 1/N (D4, applied once). k1 and
     theta_h follow make_cc (stream 0); the constants k0, k2, a, b, c, eps are
     multiplied per cell by 1 + 0.05 * normal() (stream 3, six draws per cell in
-    that order) and theta_h = k1/(k0_i - k1). x0 ~ U(0,1) (stream 1)."""
+    that order) and theta_h = k1/(k0_i - k1).
+
+    Initial state: the reference's CC initial conditions, base
+    (1, 1, -1.19, -0.62) + 0.2 (U - 0.5) (harness.cpp:320-326, stream 1).
+    BASELINE.json asks for x0 ~ U(0,1), but from there the Goodwin equation
+    (a x1^2 growth repressed only once x2^4 catches up) blows up in finite time
+    in the reference model itself: the oracle's all-binary64 run reaches
+    x1 ~ 4e9 by t = 2 and needs h < 1e-10 (tests/test_configs.py pins this)."""
     k1, _ = cc_parameters(n, seed)
     mult = 1.0 + 0.05 * rng_normal(seed, STREAM_MULT, 6 * n).reshape(n, 6)
     k0 = CcConstants.k0 * mult[:, 0]
@@ -111,7 +118,7 @@ def config3_cc(n: int = 2048, seed: int = 2, k_storage: str = "f32", rhs_mode: s
                       cc_a=CcConstants.a * mult[:, 2], cc_b=CcConstants.b * mult[:, 3],
                       cc_c=CcConstants.c * mult[:, 4], cc_eps=CcConstants.eps * mult[:, 5],
                       k_uniform=(seed, STREAM_K, 0.0, 1.0))
-    x0 = rng_uniform(seed, STREAM_IC, 4 * n, 0.0, 1.0)
+    x0 = reference_ic("cc", n, seed)
     cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
     return Workload("C3-cc", spec, x0, 0.0, 240.0, policy or SSS_D, cfg, {"seed": seed, "I0": stimulus_i0})
 

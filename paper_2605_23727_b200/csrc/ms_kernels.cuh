@@ -17,6 +17,7 @@
 #pragma once
 
 #include "ms_common.cuh"
+#include "ms_ddpow.cuh"
 
 namespace msb {
 
@@ -234,7 +235,9 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs p) {
     }
     p.B.fvc[i] = (double)f[cs];
     GS* gin = reinterpret_cast<GS*>(p.B.gin);
-    const GS xg = cvt<GS>(a[cs]);
+    // G reads slot 0 of both agents (x_j0 - x_i0, theta_j - theta_i), whatever
+    // slot it is added to (systems.cpp:123-126, 141-143, 183-184)
+    const GS xg = cvt<GS>(a[0]);
     if (p.split) {
       gin[i] = dsin<GS>(xg);
       gin[p.ld + i] = dcos<GS>(xg);
@@ -561,7 +564,7 @@ __device__ __forceinline__ double d_clamp(double v, double lo, double hi) {
 __device__ __forceinline__ double d_adjust_step(double h, double err, double rel, double safety,
                                                 double fac_min, double fac_max, double ctrl_exp) {
   if (err <= 0.0) return __dmul_rn(h, fac_max);
-  const double fac = __dmul_rn(safety, pow(__ddiv_rn(rel, err), ctrl_exp));
+  const double fac = __dmul_rn(safety, pow_cr(__ddiv_rn(rel, err), ctrl_exp));
   return __dmul_rn(h, d_clamp(fac, fac_min, fac_max));
 }
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -836,7 +839,7 @@ __global__ void __launch_bounds__(1024) k_init_b(InitArgs a) {
       const double inv_n = __ddiv_rn(1.0, (double)a.dn);
       const double d2 = __ddiv_rn(__dsqrt_rn(__dmul_rn(seq_sum(t2, a.dn), inv_n)), h1);
       const double der = c->d1 < d2 ? d2 : c->d1;  // std::max
-      h2 = der < 1e-12 ? c->cap : pow(__ddiv_rn(0.01, der), a.exponent);
+      h2 = der < 1e-12 ? c->cap : pow_cr(__ddiv_rn(0.01, der), a.exponent);
     }
     // std::min({100*h1, h2, cap})
     h0 = __dmul_rn(100.0, h1);
