@@ -167,33 +167,50 @@ def run_ours(args):
     from paper_2605_23727_b200.systems import DeviceSystem
 
     n = args.n
+    shard = ws > 1 or args.shard
     w = config4_kuramoto(n=n, seed=args.seed, k_storage=args.kdtype)
     w.spec.device = local
-    # replicas: each rank solves the full system (row-sharded K: --shard)
-    dev = DeviceSystem(w.spec)
-    x0_d = torch.from_numpy(w.x0).to(f"cuda:{local}")
-    xf_d = torch.empty_like(x0_d)
-    stream = torch.cuda.current_stream()
+    rows = n
+    if shard:
+        from paper_2605_23727_b200.sharded import DeviceEngine, ShardedSolver, TorchComm, row_range
+        if ws == 1 and not torch.distributed.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            torch.distributed.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+        r0, r1 = row_range(n, rank, ws)
+        w.spec.row_begin, w.spec.row_end = r0, r1
+        rows = r1 - r0
+    dev = DeviceSystem(w.spec)  # K (this rank's rows) generated on the device, resident
+    stream = torch.cuda.Stream()
 
-    def one():
-        return S.solve_device(dev, x0_d.data_ptr(), xf_d.data_ptr(), w.t0, w.tf, w.policy, w.cfg,
-                              stream=stream.cuda_stream, log_capacity=0)
+    if shard:
+        solver = ShardedSolver(DeviceEngine(dev), TorchComm(), check_every=args.check_every)
 
-    for _ in range(args.warmup):
-        r = one()
-    torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    results = []
-    with ClockSampler(local) as clk:
+        def one():
+            return solver.solve(w.x0, w.t0, w.tf, w.policy, w.cfg, log_capacity=0)
+    else:
+        x0_d = torch.from_numpy(w.x0).to(f"cuda:{local}")
+        xf_d = torch.empty_like(x0_d)
+
+        def one():
+            return S.solve_device(dev, x0_d.data_ptr(), xf_d.data_ptr(), w.t0, w.tf, w.policy, w.cfg,
+                                  stream=stream.cuda_stream, log_capacity=0)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            one()
         torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            results.append(one())
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+        if ws > 1:
+            torch.distributed.barrier()
+        results = []
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize()
+            for _ in range(args.steps):
+                results.append(one())
+            torch.cuda.synchronize()
+    # device time of each solve: CUDA events recorded by the library on its stream
+    # around the whole adaptive loop (initial step included)
+    ms = float(sum(r.device_ms for r in results))
     if ws > 1:
         t = torch.tensor([ms], device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -201,21 +218,30 @@ def run_ours(args):
     acc = sum(r.n_accepted for r in results)
     att = sum(r.n_accepted + r.n_failed for r in results)
     evals = sum(r.flops.rhs_evals for r in results)
-    value = acc * ws / (ms / 1e3)
+    launched_evals = evals - sum(r.n_failed for r in results)  # elided k1 recomputes are counted, not run
+    # sharded: all ranks cooperate on one solve (strong scaling); replicas would multiply
+    value = acc / (ms / 1e3)
     ms_per_step = ms / args.steps
 
-    # e2e: the public C-ABI call with host buffers (H2D x0, D2H final state + log)
+    # e2e: the public call with host buffers (H2D x0, D2H final state (+ log on 1 GPU))
+    if ws > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     e2e_res = []
     for _ in range(args.steps):
-        e2e_res.append(S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg))
+        if shard:
+            e2e_res.append(solver.solve(w.x0, w.t0, w.tf, w.policy, w.cfg, log_capacity=None))
+        else:
+            e2e_res.append(S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg))
     e2e_s = time.perf_counter() - t0
-    e2e_acc = sum(r.n_accepted for r in e2e_res)
-    e2e_value = e2e_acc * ws / e2e_s
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = sum(r.n_accepted for r in e2e_res) / e2e_s
     log_bytes = max(r.step_log_count for r in e2e_res) * 32
 
-    # roofline of the dominant kernel (the K sweep), timed live with CUDA events
-    # on the stream it is launched on
+    # roofline of the dominant kernel (this rank's K sweep), CUDA events on its stream
     from paper_2605_23727_b200.precision import SSS
     import ctypes as C
     from paper_2605_23727_b200 import _abi
@@ -224,40 +250,40 @@ def run_ours(args):
     _abi.check(_abi.lib().ms_profile_rhs(dev.handle, _abi.dptr(x0c), SSS.c(), 20, C.byref(rhs_ms), C.byref(prep_ms)),
                "profile_rhs")
     ks_bytes = {"f32": 4, "f16": 2, "bf16": 2}[args.kdtype]
-    bpe = bytes_per_eval(n, n, ks_bytes)
+    bpe = bytes_per_eval(n, rows, ks_bytes)
     peak, peak_kind = peaks()
     achieved = bpe / (rhs_ms.value * 1e-3) / 1e9
-    solve_gbs = evals / args.steps * bpe / (ms_per_step * 1e-3) / 1e9
+    solve_gbs = launched_evals / args.steps * bpe / (ms_per_step * 1e-3) / 1e9
 
     # accuracy: device SSS solve vs the same-tolerance all-binary64 device solve
     err = {}
     if not args.no_accuracy:
         D = custom_policy((DDD, DDD, DDD), DDD, B64)
-        rd = S.solve(dev, w.x0, w.t0, w.tf, D, w.cfg)
-        r0 = e2e_res[0]
-        diff = np.abs(r0.final_state - rd.final_state)
+        rd = solver.solve(w.x0, w.t0, w.tf, D, w.cfg) if shard else S.solve(dev, w.x0, w.t0, w.tf, D, w.cfg)
+        r0_ = e2e_res[0]
+        diff = np.abs(r0_.final_state - rd.final_state)
         err = {"vs": "device all-binary64 BS3(2), same rtol/atol",
                "max_abs": float(diff.max()),
                "max_rel_weighted": float(np.max(diff / np.maximum(np.abs(rd.final_state), w.cfg.abs_tol / w.cfg.rel_tol))),
-               "l2_over_sqrtN": float(np.linalg.norm(r0.final_state - rd.final_state) / np.sqrt(n)),
+               "l2_over_sqrtN": float(np.linalg.norm(r0_.final_state - rd.final_state) / np.sqrt(n)),
                "double_steps": [rd.n_accepted, rd.n_failed]}
 
-    launches_per_attempt = 7  # 3 x (prep + sweep) + finalize
-    gpu_launches = sum(10 + launches_per_attempt * (r.n_accepted + r.n_failed) for r in results)
+    per_attempt = 11 if shard else 7  # (prep + sweep [+ scan]) x 3 + finalize [+ fsal copy]
+    gpu_launches = sum(10 + per_attempt * (r.n_accepted + r.n_failed) for r in results)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak" if ws > 1 else "weak",
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "f32 (RHS, K) / f64 (stages, error control)",
         "data": "synthetic (seeded SplitMix64: omega~N(0,1), K~U(0,2), theta0~U(0,2pi))",
         "config": {"workload": f"C4 Kuramoto N={n} K {args.kdtype} (BASELINE configs[3])", "n_agents": n,
                    "t_final": 20.0, "rtol": 1e-6, "atol": 1e-9, "policy": "SSS x3 rows, binary64 storage",
                    "step": "one full adaptive solve", "l2": "K (4 GiB) > L2: no flush needed",
-                   "parallelism": "replicas" if ws > 1 else "single"},
+                   "parallelism": f"row-shard x{ws} (NCCL all-gather per stage)" if shard else "single GPU"},
         "accepted_steps_per_solve": results[0].n_accepted, "rejected_per_solve": results[0].n_failed,
         "rhs_evals_per_solve": results[0].flops.rhs_evals,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "k_rhs_fast<Kuramoto split, f32, f32, K f32>",
+                     "kernel": f"k_rhs_fast<Kuramoto split, f32, f32, K {args.kdtype}>",
                      "bytes_per_launch": bpe, "launch_ms": rhs_ms.value, "prep_ms": prep_ms.value,
                      "solve_effective_GBps": solve_gbs},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,
@@ -271,11 +297,10 @@ def run_ours(args):
                                 "kind": "port",
                                 "sample": f"1 BS3(2) attempt (3 RHS evals) of C4 N={args.cpu_n or n} from theta0 at h0, "
                                           "oracle restatement, OpenMP rows"}
-    with_clk = clk.summary()
-    line["clocks"] = with_clk
+    line["clocks"] = clk.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
     dev.close()
     return 0
@@ -293,6 +318,8 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-accuracy", action="store_true")
+    ap.add_argument("--shard", action="store_true", help="use the row-sharded loop even on 1 GPU")
+    ap.add_argument("--check-every", type=int, default=8)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -207,8 +207,8 @@ int ms_abi_version(void);
 const char* ms_last_error(void);
 /* sizeof of the ABI structs, in declaration order: ms_stage_prec, ms_policy,
  * ms_solver_config, ms_step_record, ms_system_desc, ms_solve_result,
- * ms_step_outcome (binding self-check) */
-int ms_abi_sizes(int64_t out[7]);
+ * ms_step_outcome, ms_exchange (binding self-check) */
+int ms_abi_sizes(int64_t out[8]);
 /* device count visible to the library (0 without a GPU; never an error) */
 int ms_device_count(void);
 void ms_default_config(ms_solver_config* cfg);
@@ -255,6 +255,33 @@ int ms_solve(ms_system_t sys, const double* x0, double t0, double t_final, const
 int ms_solve_device(ms_system_t sys, const double* x0_dev, double t0, double t_final,
                     const ms_policy* policy, const ms_solver_config* cfg, ms_solve_result* res,
                     void* stream);
+/* ---- host-driven loop with exchange points (row-sharded solves) --------
+ * The same attempt as ms_solve, cut into segments so a caller can all-gather
+ * the stage derivative rows of a row-sharded handle between sweeps (NCCL).
+ * Segments of list 0 (start-up: initial_step + cold k1) run once; those of
+ * list 1 form one attempt. After a segment with exch->needed = 1 the caller
+ * must make buf[0, total) identical on every rank (each rank owns
+ * [offset, offset + count)); the next segment re-checks finiteness on the
+ * gathered vector, so every rank takes identical decisions. Kernels are
+ * enqueued on `stream` (cudaStream_t, NULL = the handle's stream); nothing
+ * in a segment synchronizes, so segments and collectives can be captured into
+ * a CUDA graph. ms_loop_done synchronizes and reads the loop flag. */
+typedef struct {
+  int32_t needed;
+  int32_t _pad;
+  double* buf;    /* device pointer, dN doubles */
+  int64_t offset; /* first element owned by this handle */
+  int64_t count;  /* elements owned by this handle */
+  int64_t total;  /* dN */
+} ms_exchange;
+int ms_loop_begin(ms_system_t sys, const double* x0, int x0_on_device, double t0, double t_final,
+                  const ms_policy* policy, const ms_solver_config* cfg, int64_t step_log_capacity,
+                  void* stream);
+int ms_loop_segment_count(ms_system_t sys, int list, int* count);
+int ms_loop_run_segment(ms_system_t sys, int list, int index, void* stream, ms_exchange* exch);
+int ms_loop_done(ms_system_t sys, void* stream, int* done);
+int ms_loop_end(ms_system_t sys, ms_solve_result* res, int final_on_device, void* stream);
+
 /* Measurement hook (no reference counterpart): times `iters` evaluations of
  * the RHS at host state x under row sp with CUDA events on the handle's
  * stream, returning the mean device time of the coupling sweep kernel and of

@@ -86,6 +86,11 @@ class StepOutcomeC(C.Structure):
     ]
 
 
+class ExchangeC(C.Structure):
+    _fields_ = [("needed", C.c_int32), ("_pad", C.c_int32), ("buf", C.c_void_p), ("offset", C.c_int64),
+                ("count", C.c_int64), ("total", C.c_int64)]
+
+
 # (name, restype, argtypes) of every symbol include/mixedstep_b200.h declares
 SIGNATURES = [
     ("ms_abi_version", C.c_int, []),
@@ -115,6 +120,12 @@ SIGNATURES = [
                            C.POINTER(SolveResultC)]),
     ("ms_solve_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.POINTER(Policy),
                                   C.POINTER(SolverConfigC), C.POINTER(SolveResultC), C.c_void_p]),
+    ("ms_loop_begin", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double, C.POINTER(Policy),
+                                C.POINTER(SolverConfigC), C.c_int64, C.c_void_p]),
+    ("ms_loop_segment_count", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int)]),
+    ("ms_loop_run_segment", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(ExchangeC)]),
+    ("ms_loop_done", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]),
+    ("ms_loop_end", C.c_int, [C.c_void_p, C.POINTER(SolveResultC), C.c_int, C.c_void_p]),
     ("ms_profile_rhs", C.c_int, [C.c_void_p, _DP, StagePrec, C.c_int, _DP, _DP]),
     ("ms_dp54_reference", C.c_int, [C.c_void_p, _DP, C.c_double, C.c_double, C.POINTER(SolverConfigC),
                                     C.POINTER(SolveResultC)]),

@@ -259,6 +259,7 @@ void launch_prep_model(bool fs32, bool gs32, int grid, cudaStream_t st, const Pr
 
 }  // namespace
 
+struct SolvePlanStore;
 // =====================================================================================
 struct ms_system {
   int model = 0;      // MS_MODEL_*
@@ -287,6 +288,9 @@ struct ms_system {
   };
   std::map<std::string, GraphEntry> graphs;
   std::mutex mu;
+  // host-driven (sharded) loop
+  bool loop_active = false;
+  SolvePlanStore* loop_plan = nullptr;
 
   int64_t dn() const { return (int64_t)n * d; }
 };
@@ -755,6 +759,133 @@ SolvePlan plan_dp54() {
   return P;
 }
 
+}  // namespace
+
+struct SolvePlanStore {
+  SolvePlan P;
+  ms_solver_config cfg;
+  int64_t log_cap;
+};
+
+namespace {
+
+cudaStream_t pick_stream(ms_system* s, void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : s->stream;
+}
+
+void set_exch(ms_system* s, ms_exchange* ex, double* buf) {
+  if (!ex) return;
+  ex->needed = 1;
+  ex->buf = buf;
+  ex->offset = (int64_t)s->row0 * s->d;
+  ex->count = (int64_t)(s->row1 - s->row0) * s->d;
+  ex->total = s->dn();
+}
+
+void launch_scan(ms_system* s, cudaStream_t st, const double* buf, int l) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((s->dn() + 255) / 256, 2 * s->sms));
+  k_nf_scan<<<grid, 256, 0, st>>>(s->B.ctl, buf, s->dn(), l);
+  CK(cudaGetLastError());
+}
+
+// segment lists of the host-driven loop (ms_loop_* in the header)
+int loop_segments(const SolvePlan& P, int list) {
+  if (list == 0) return 4;
+  return (P.k1_elided ? 0 : 1) + (P.T->S - 1) + 1;
+}
+
+void loop_run(ms_system* s, const SolvePlan& P, int list, int index, cudaStream_t st, ms_exchange* ex) {
+  const Tableau& T = *P.T;
+  if (ex) std::memset(ex, 0, sizeof(*ex));
+  const int S = T.S;
+  if (list == 0) {
+    InitArgs ia{};
+    ia.B = s->B;
+    ia.x0 = s->B.xb[0];
+    ia.dn = s->dn();
+    ia.exponent = 1.0 / static_cast<double>(T.order_high + 1);
+    EvalSpec f;
+    f.S = S;
+    f.l = 7;
+    f.kind = PREP_X;
+    f.count = CNT_DDD;
+    switch (index) {
+      case 0:
+        k_stamp_start<<<1, 1, 0, st>>>(s->B.ctl);
+        f.out_slot = 1;
+        launch_eval(s, st, f, kDDD);
+        set_exch(s, ex, s->B.kb[1]);
+        return;
+      case 1:
+        launch_scan(s, st, s->B.kb[1], 7);
+        k_init_a<<<1, 1024, 0, st>>>(ia);
+        CK(cudaGetLastError());
+        f.kind = PREP_INIT_X1;
+        f.gate = GATE_INIT2;
+        f.out_slot = 2;
+        launch_eval(s, st, f, kDDD);
+        set_exch(s, ex, s->B.kb[2]);
+        return;
+      case 2: {
+        k_init_b<<<1, 1024, 0, st>>>(ia);
+        CK(cudaGetLastError());
+        EvalSpec k1;
+        k1.S = S;
+        k1.l = 0;
+        k1.kind = PREP_X;
+        k1.count = CNT_K1;
+        k1.out_slot = 0;
+        k1.round_x = P.storage == MS_BINARY32 ? 1 : 0;
+        launch_eval(s, st, k1, P.k1_row);
+        set_exch(s, ex, s->B.kb[0]);
+        return;
+      }
+      case 3:
+        launch_scan(s, st, s->B.kb[0], 0);
+        k_loop_head<<<1, 1, 0, st>>>(s->B.ctl);
+        CK(cudaGetLastError());
+        return;
+      default: throw InvalidArg("loop: bad init segment");
+    }
+  }
+  int idx = index;
+  if (!P.k1_elided) {
+    if (idx == 0) {
+      EvalSpec e;
+      e.S = S;
+      e.l = 0;
+      e.kind = PREP_X;
+      e.gate = GATE_NEED_K1;
+      e.count = CNT_K1;
+      e.out_slot = 0;
+      launch_eval(s, st, e, P.k1_row);
+      set_exch(s, ex, s->B.kb[0]);
+      return;
+    }
+    --idx;
+  }
+  // k1 stays in slot 0 (k1i == 0 throughout), the last stage writes slot S
+  auto out_of = [&](int l) { return l == S - 1 ? s->B.kb[S] : s->B.kb[l]; };
+  const int l = idx + 1;
+  if (l < S) {
+    if (l > 1) launch_scan(s, st, out_of(l - 1), l - 1);
+    else if (!P.k1_elided) launch_scan(s, st, s->B.kb[0], 0);
+    launch_eval(s, st, stage_spec(T, l), P.rows[l - 1]);
+    set_exch(s, ex, out_of(l));
+    return;
+  }
+  if (l != S) throw InvalidArg("loop: bad attempt segment");
+  launch_scan(s, st, out_of(S - 1), S - 1);
+  FinArgs f = fin_args(s, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
+  f.fixed_k1 = 1;
+  k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
+  CK(cudaGetLastError());
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((s->dn() + 255) / 256, 2 * s->sms));
+  k_fsal_copy<<<grid, 256, 0, st>>>(s->B.ctl, s->B.kb[0], s->B.kb[S], s->dn());
+  CK(cudaGetLastError());
+}
+
+
 void check_prec(const ms_stage_prec& sp) {
   if (sp.f_prec > 1 || sp.sum_prec > 1 || sp.g_prec > 1) throw InvalidArg("stage precision: format must be 0 or 1");
 }
@@ -772,7 +903,7 @@ extern "C" {
 int ms_abi_version(void) { return MS_ABI_VERSION; }
 const char* ms_last_error(void) { return g_err.c_str(); }
 
-int ms_abi_sizes(int64_t out[7]) {
+int ms_abi_sizes(int64_t out[8]) {
   out[0] = sizeof(ms_stage_prec);
   out[1] = sizeof(ms_policy);
   out[2] = sizeof(ms_solver_config);
@@ -780,6 +911,7 @@ int ms_abi_sizes(int64_t out[7]) {
   out[4] = sizeof(ms_system_desc);
   out[5] = sizeof(ms_solve_result);
   out[6] = sizeof(ms_step_outcome);
+  out[7] = sizeof(ms_exchange);
   return MS_OK;
 }
 
@@ -969,6 +1101,7 @@ int ms_system_destroy(ms_system_t s) {
     if (s->K) cudaFree(s->K);
     if (s->ws_mem) cudaFree(s->ws_mem);
     if (s->ctl_host) cudaFreeHost(s->ctl_host);
+    delete s->loop_plan;
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     if (s->stream) cudaStreamDestroy(s->stream);
@@ -1235,6 +1368,106 @@ int ms_solve_device(ms_system_t s, const double* x0_dev, double t0, double t_fin
     run_solve(s, x0_dev, true, t0, t_final, plan_bs32(*pol), *cfg, res, static_cast<cudaStream_t>(stream), true);
   });
 }
+
+int ms_loop_begin(ms_system_t s, const double* x0, int x0_on_device, double t0, double t_final,
+                  const ms_policy* pol, const ms_solver_config* cfg, int64_t log_cap, void* stream) {
+  return guard([&] {
+    if (!s || !x0 || !pol || !cfg) throw InvalidArg("loop_begin: null argument");
+    check_policy(*pol);
+    validate_cfg(*cfg, t0, t_final);
+    std::lock_guard<std::mutex> lk(s->mu);
+    set_device(s);
+    const int64_t cap = (cfg->record_step_log && log_cap > 0) ? log_cap : 1;
+    ensure_workspace(s, cap);
+    if (!s->loop_plan) s->loop_plan = new SolvePlanStore();
+    s->loop_plan->P = plan_bs32(*pol);
+    s->loop_plan->cfg = *cfg;
+    s->loop_plan->log_cap = cap;
+    cudaStream_t st = pick_stream(s, stream);
+    Ctl& c = *s->ctl_host;
+    init_ctl(s, c, *cfg, t0, t_final, s->loop_plan->P, cap);
+    CK(cudaMemcpyAsync(s->B.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->B.xb[0], x0, sizeof(double) * s->dn(),
+                       x0_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(s->ev0, st));
+    s->loop_active = true;
+  });
+}
+
+int ms_loop_segment_count(ms_system_t s, int list, int* count) {
+  return guard([&] {
+    if (!s || !count || !s->loop_active) throw InvalidArg("loop_segment_count: no active loop");
+    if (list != 0 && list != 1) throw InvalidArg("loop_segment_count: list is 0 or 1");
+    *count = loop_segments(s->loop_plan->P, list);
+  });
+}
+
+int ms_loop_run_segment(ms_system_t s, int list, int index, void* stream, ms_exchange* ex) {
+  return guard([&] {
+    if (!s || !s->loop_active) throw InvalidArg("loop_run_segment: no active loop");
+    if (list != 0 && list != 1) throw InvalidArg("loop_run_segment: list is 0 or 1");
+    if (index < 0 || index >= loop_segments(s->loop_plan->P, list)) throw InvalidArg("loop_run_segment: bad index");
+    set_device(s);
+    loop_run(s, s->loop_plan->P, list, index, pick_stream(s, stream), ex);
+  });
+}
+
+int ms_loop_done(ms_system_t s, void* stream, int* done) {
+  return guard([&] {
+    if (!s || !done || !s->loop_active) throw InvalidArg("loop_done: no active loop");
+    set_device(s);
+    cudaStream_t st = pick_stream(s, stream);
+    CK(cudaMemcpyAsync(&s->ctl_host->done, &s->B.ctl->done, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *done = s->ctl_host->done;
+  });
+}
+
+int ms_loop_end(ms_system_t s, ms_solve_result* res, int final_on_device, void* stream) {
+  return guard([&] {
+    if (!s || !res || !s->loop_active) throw InvalidArg("loop_end: no active loop");
+    set_device(s);
+    cudaStream_t st = pick_stream(s, stream);
+    CK(cudaEventRecord(s->ev1, st));
+    Ctl& c = *s->ctl_host;
+    CK(cudaMemcpyAsync(&c, s->B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+    const int64_t dn = s->dn();
+    if (res->final_state)
+      CK(cudaMemcpyAsync(res->final_state, s->B.xb[c.ix], sizeof(double) * dn,
+                         final_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    res->step_log_count = c.record_log ? c.log_count : 0;
+    if (res->step_log && c.record_log) {
+      const int64_t m = std::min<int64_t>(std::min<int64_t>(res->step_log_capacity, c.log_count), s->log_cap);
+      if (m > 0) {
+        std::vector<StepLogRec> tmp((size_t)m);
+        CK(cudaMemcpyAsync(tmp.data(), s->B.log, sizeof(StepLogRec) * m, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int64_t i = 0; i < m; ++i) {
+          res->step_log[i].t = tmp[(size_t)i].t;
+          res->step_log[i].h = tmp[(size_t)i].h;
+          res->step_log[i].err = tmp[(size_t)i].err;
+          res->step_log[i].accepted = tmp[(size_t)i].accepted;
+        }
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+    res->status = c.status;
+    res->t_reached = c.t;
+    res->n_accepted = c.n_acc;
+    res->n_failed = c.n_fail;
+    int64_t tl[3];
+    tally(s, c, s->loop_plan->P, tl);
+    res->rhs_evals = tl[0];
+    res->flops_low = tl[1];
+    res->flops_high = tl[2];
+    res->device_ms = ms;
+    s->loop_active = false;
+  });
+}
+
 
 int ms_dp54_reference(ms_system_t s, const double* x0, double t0, double t_final, const ms_solver_config* cfg,
                       ms_solve_result* res) {

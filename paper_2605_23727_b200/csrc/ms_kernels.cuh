@@ -615,6 +615,7 @@ struct FinArgs {
   int k1_elided;
   int write_xt;
   int has_handle;
+  int fixed_k1;  // host-driven sharded loop: k1 stays in slot 0 (k_fsal_copy), no ping-pong
   cudaGraphConditionalHandle handle;
 };
 
@@ -729,7 +730,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
     c->ix ^= 1;
     const double tn = __dadd_rn(c->t, h);
     c->t = c->last ? c->tf : (c->store32 ? rn32(tn) : tn);
-    c->k1i = f.S - c->k1i;  // FSAL: k1 <- k_last
+    if (!f.fixed_k1) c->k1i = f.S - c->k1i;  // FSAL: k1 <- k_last
     c->h = h_next;
     if (c->t >= c->tf) {
       c->status = MS_COMPLETED;
@@ -868,6 +869,21 @@ __global__ void k_loop_head(Ctl* c) {
 }
 
 __global__ void k_stamp_start(Ctl* c) { c->t_start_ns = globaltimer_ns(); }
+
+// sharded loop: finiteness of a gathered stage vector, identical on every rank
+__global__ void k_nf_scan(Ctl* c, const double* v, int64_t n, int l) {
+  bool nf = false;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    nf |= !isfinite(v[e]);
+  if (__any_sync(0xffffffffu, nf) && (threadIdx.x & 31) == 0) atomicOr(&c->nf_mask, 1 << l);
+}
+
+// sharded loop: FSAL k1 <- k_last on an accepted attempt (slot 0 stays k1)
+__global__ void k_fsal_copy(const Ctl* c, double* k1, const double* klast, int64_t n) {
+  if (!c->accepted) return;  // set by this attempt's k_finalize (stale only once done)
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    k1[e] = klast[e];
+}
 
 #endif  // MS_DEFINE_STEP_KERNELS
 

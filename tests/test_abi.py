@@ -34,10 +34,10 @@ def test_library_loads_and_exports_every_declared_symbol():
 
 
 def test_struct_layouts_match():
-    out = (C.c_int64 * 7)()
+    out = (C.c_int64 * 8)()
     assert _abi.lib().ms_abi_sizes(out) == 0
     py = [_abi.StagePrec, _abi.Policy, _abi.SolverConfigC, _abi.StepRecordC, _abi.SystemDesc, _abi.SolveResultC,
-          _abi.StepOutcomeC]
+          _abi.StepOutcomeC, _abi.ExchangeC]
     assert list(out) == [C.sizeof(t) for t in py]
 
 
