@@ -282,6 +282,33 @@ int ms_loop_run_segment(ms_system_t sys, int list, int index, void* stream, ms_e
 int ms_loop_done(ms_system_t sys, void* stream, int* done);
 int ms_loop_end(ms_system_t sys, ms_solve_result* res, int final_on_device, void* stream);
 
+/* ---- batched ensembles sharing one K (BASELINE.json configs[4]) ---------
+ * B Kuramoto trajectories (own omega_b, theta0_b, own adaptive controller)
+ * over the K of a Kuramoto system handle. Each trajectory follows the
+ * reference's solve (solver.cpp:226-347) exactly; all advance in lock-step
+ * attempts so that one stage evaluates the whole ensemble as one dense
+ * contraction K [S|C]. With tensor_cores = 1 (K stored f16 or bf16), stage
+ * rows with F, sum and G in binary32 run as a tcgen05 GEMM: sin/cos operands
+ * rounded to K's 16-bit format, exact products, binary32 accumulation; other
+ * rows (binary64 sums, initial_step) run the exact split on CUDA cores.
+ * Arrays are trajectory-major [B][N]; result arrays are caller-owned. */
+typedef struct ms_batch* ms_batch_t;
+typedef struct {
+  int32_t* status;     /* [B] or NULL */
+  double* t_reached;   /* [B] or NULL */
+  int64_t* n_accepted; /* [B] or NULL */
+  int64_t* n_failed;   /* [B] or NULL */
+  int64_t* rhs_evals;  /* [B] or NULL */
+  double* final_state; /* [B][N] host or NULL */
+  int64_t attempts;    /* out: lock-step attempts */
+  double device_ms;    /* out */
+} ms_batch_result;
+int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t tensor_cores, ms_batch_t* out);
+int ms_batch_destroy(ms_batch_t b);
+int ms_batch_eval_rhs(ms_batch_t b, const double* x, ms_stage_prec sp, double* out);
+int ms_batch_solve(ms_batch_t b, const double* x0, double t0, double t_final, const ms_policy* policy,
+                   const ms_solver_config* cfg, ms_batch_result* res);
+
 /* Measurement hook (no reference counterpart): times `iters` evaluations of
  * the RHS at host state x under row sp with CUDA events on the handle's
  * stream, returning the mean device time of the coupling sweep kernel and of

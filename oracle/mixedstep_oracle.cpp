@@ -151,6 +151,20 @@ void eval_kuramoto_split(const ModelParams& p, const Vec& x, Vec& out) {
     s[static_cast<std::size_t>(j)] = std::sin(xg);
     c[static_cast<std::size_t>(j)] = std::cos(xg);
   }
+  // tensor-core ensemble semantics (ms_batch_*): the GEMM operands are the
+  // binary32 sin/cos rounded once to K's 16-bit format; the epilogue keeps them
+  std::vector<GS> so = s, co = c;
+  if (p.op_round && sizeof(SS) == 4 && sizeof(GS) == 4) {
+    for (std::size_t j = 0; j < so.size(); ++j) {
+      if (p.op_round == 2) {
+        so[j] = static_cast<GS>(static_cast<_Float16>(static_cast<float>(s[j])));
+        co[j] = static_cast<GS>(static_cast<_Float16>(static_cast<float>(c[j])));
+      } else {
+        so[j] = static_cast<GS>(static_cast<__bf16>(static_cast<float>(s[j])));
+        co[j] = static_cast<GS>(static_cast<__bf16>(static_cast<float>(c[j])));
+      }
+    }
+  }
   const SS mw = static_cast<SS>(p.m[0]);
   const float* K = p.K ? p.K->data() : nullptr;
   using WS = wider_t<FS, SS>;
@@ -160,8 +174,8 @@ void eval_kuramoto_split(const ModelParams& p, const Vec& x, Vec& out) {
     SS A = SS(0), B = SS(0);
     for (int j = 0; j < n; ++j) {
       const GS k = kij<GS, HasK>(p, K, i, j);
-      A = A + static_cast<SS>(k * s[static_cast<std::size_t>(j)]);
-      B = B + static_cast<SS>(k * c[static_cast<std::size_t>(j)]);
+      A = A + static_cast<SS>(k * so[static_cast<std::size_t>(j)]);
+      B = B + static_cast<SS>(k * co[static_cast<std::size_t>(j)]);
     }
     const SS coup = mw * ((static_cast<SS>(c[static_cast<std::size_t>(i)]) * A) -
                           (static_cast<SS>(s[static_cast<std::size_t>(i)]) * B));

@@ -170,6 +170,7 @@ struct ModelParams {
   double stimulus_i0 = 0.0;
   std::shared_ptr<const std::vector<float>> K;  // row-major n x n; null = scalar coupling_k
   bool split = false;
+  int op_round = 0;  // batched tensor-core semantics: binary32 sin/cos GEMM operands rounded to f16 (2) / bf16 (3)
 };
 
 void set_threads(int n);

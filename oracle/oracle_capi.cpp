@@ -236,6 +236,23 @@ int orc_system_fill_k_uniform(void* h, uint64_t seed, uint64_t stream, double lo
   });
 }
 
+// batched tensor-core semantics for this system: 0 off, MS_K_F16 / MS_K_BF16
+int orc_system_set_op_round(void* h, int ks) {
+  return guard([&] {
+    auto* s = static_cast<OrcSystem*>(h);
+    s->p.op_round = ks;
+    s->rebuild();
+  });
+}
+// per-trajectory frequencies (ensemble members share K)
+int orc_system_set_omega(void* h, const double* omega) {
+  return guard([&] {
+    auto* s = static_cast<OrcSystem*>(h);
+    s->p.omega.assign(omega, omega + s->p.n);
+    s->rebuild();
+  });
+}
+
 int orc_system_get_k(void* h, double* out) {
   auto* s = static_cast<OrcSystem*>(h);
   if (!s->p.K) return MS_EINVAL;

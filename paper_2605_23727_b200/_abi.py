@@ -12,7 +12,8 @@ import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libmixedstep_b200.so"
+# MS_LIB_PATH: an alternative build of the same sources (kernel-geometry tuning runs)
+LIB_PATH = Path(os.environ["MS_LIB_PATH"]) if os.environ.get("MS_LIB_PATH") else PKG / "libmixedstep_b200.so"
 
 MS_OK, MS_EINVAL, MS_ECUDA = 0, 1, 2
 MS_BINARY32, MS_BINARY64 = 0, 1
@@ -86,6 +87,12 @@ class StepOutcomeC(C.Structure):
     ]
 
 
+class BatchResultC(C.Structure):
+    _fields_ = [("status", C.POINTER(C.c_int32)), ("t_reached", _DP), ("n_accepted", C.POINTER(C.c_int64)),
+                ("n_failed", C.POINTER(C.c_int64)), ("rhs_evals", C.POINTER(C.c_int64)), ("final_state", _DP),
+                ("attempts", C.c_int64), ("device_ms", C.c_double)]
+
+
 class ExchangeC(C.Structure):
     _fields_ = [("needed", C.c_int32), ("_pad", C.c_int32), ("buf", C.c_void_p), ("offset", C.c_int64),
                 ("count", C.c_int64), ("total", C.c_int64)]
@@ -126,6 +133,11 @@ SIGNATURES = [
     ("ms_loop_run_segment", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(ExchangeC)]),
     ("ms_loop_done", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]),
     ("ms_loop_end", C.c_int, [C.c_void_p, C.POINTER(SolveResultC), C.c_int, C.c_void_p]),
+    ("ms_batch_create", C.c_int, [C.c_void_p, C.c_int32, _DP, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("ms_batch_destroy", C.c_int, [C.c_void_p]),
+    ("ms_batch_eval_rhs", C.c_int, [C.c_void_p, _DP, StagePrec, _DP]),
+    ("ms_batch_solve", C.c_int, [C.c_void_p, _DP, C.c_double, C.c_double, C.POINTER(Policy),
+                                 C.POINTER(SolverConfigC), C.POINTER(BatchResultC)]),
     ("ms_profile_rhs", C.c_int, [C.c_void_p, _DP, StagePrec, C.c_int, _DP, _DP]),
     ("ms_dp54_reference", C.c_int, [C.c_void_p, _DP, C.c_double, C.c_double, C.POINTER(SolverConfigC),
                                     C.POINTER(SolveResultC)]),

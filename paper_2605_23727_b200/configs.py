@@ -132,3 +132,28 @@ def reference_ic(model: str, n: int, test_id: int) -> np.ndarray:
     u = rng_uniform(test_id, STREAM_IC, 4 * n, 0.0, 1.0).reshape(n, 4)
     base = np.array([1.0, 1.0, -1.19, -0.62])
     return (base + 0.2 * (u - 0.5)).reshape(-1)
+
+
+@dataclass
+class BatchWorkload:
+    name: str
+    spec: SystemSpec          # the shared-K Kuramoto system
+    omega: np.ndarray         # [B][N]
+    x0: np.ndarray            # [B][N]
+    t0: float
+    tf: float
+    policy: PrecisionPolicy
+    cfg: SolverConfig
+
+
+def config5_batch(batch: int = 1024, n: int = 2048, seed: int = 4, k_storage: str = "bf16", tf: float = 20.0,
+                  rtol: float = 1e-6, atol: float = 1e-9, policy: PrecisionPolicy | None = None) -> BatchWorkload:
+    """C5: B trajectories sharing K_ij ~ U(0,2) (stream 2, stored bf16), each with
+    omega_b,i ~ N(0,1) (stream 0) and theta0_b,i ~ U(0,2pi) (stream 1), drawn in
+    trajectory-major order. BASELINE.json gives no time span: t in [0,20] as C4;
+    atol = 1e-9 (D8)."""
+    omega = rng_normal(seed, STREAM_PARAMS, batch * n).reshape(batch, n)
+    x0 = rng_uniform(seed, STREAM_IC, batch * n, 0.0, TWO_PI).reshape(batch, n)
+    spec = SystemSpec("kuramoto", n, k_storage=k_storage, omega=np.zeros(n), k_uniform=(seed, STREAM_K, 0.0, 2.0))
+    cfg = SolverConfig(rel_tol=rtol, abs_tol=atol, time_limits_enabled=False)
+    return BatchWorkload("C5-batch", spec, omega, x0, 0.0, tf, policy or SSS_D, cfg)

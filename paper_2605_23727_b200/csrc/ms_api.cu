@@ -22,6 +22,7 @@
 
 #define MS_DEFINE_STEP_KERNELS 1
 #include "ms_dispatch.h"
+#include "ms_internal.h"
 
 using namespace msb;
 
@@ -896,6 +897,25 @@ void check_policy(const ms_policy& p) {
 }
 
 }  // namespace
+
+void msb::set_last_error(const char* msg) { g_err = msg; }
+
+msb::SysView msb::sys_view(ms_system_t s) {
+  SysView v{};
+  v.mkind = s->mkind;
+  v.n = s->n;
+  v.d = s->d;
+  v.ld = s->ld;
+  v.row0 = s->row0;
+  v.row1 = s->row1;
+  v.ks = s->ks;
+  v.dev = s->dev;
+  v.sms = s->sms;
+  v.K = s->K;
+  v.coupling_k = s->md.coupling_k;
+  v.stream = s->stream;
+  return v;
+}
 
 // =====================================================================================
 extern "C" {

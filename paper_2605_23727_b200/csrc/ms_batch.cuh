@@ -1,0 +1,204 @@
+// ms_batch.cuh — batched Kuramoto ensembles that share one coupling matrix K
+// (BASELINE.json configs[4]: B trajectories, each with its own omega_b and
+// theta0_b, each integrated by its own adaptive BS3(2) controller).
+//
+// The reference runs B independent solves (harness.cpp:113-121 pattern); here
+// all trajectories advance in lock-step attempts — each attempt is one BS3(2)
+// attempt of every unfinished trajectory with its own h, t, FSAL k1, status —
+// so one stage evaluation of the whole ensemble is the dense contraction
+//   A[i][b] = sum_j K_ij sin(theta_bj),  B[i][b] = sum_j K_ij cos(theta_bj)
+// (the Kuramoto sin/cos split) over all b at once.
+#pragma once
+
+#include "ms_kernels.cuh"
+
+namespace msb {
+
+// Device view of one ensemble (all [B][N] arrays trajectory-major, N = n).
+struct BatchDev {
+  int B, n, ld;
+  const void* K;  // the system's K (rows 0..n), storage ks
+  int ks;
+  const double* omega;            // [B][n]
+  double* xb[2];                  // x / x_store ping-pong, selected per trajectory by ctl[b].ix
+  double* kb[kMaxStages + 1];     // stage derivatives, k1 <-> k_last via ctl[b].k1i
+  double* xn;                     // x_next under binary32 storage
+  double* scr0;                   // initial_step terms
+  double* scr1;
+  void* sc;                       // GS-typed s (first B*n) and c (next B*n)
+  void* op;                       // GEMM operand [B][2][ld] in K's 16-bit format (s row, c row)
+  double* fvc;                    // F (omega in FS) [B][n]
+  Ctl* ctl;                       // [B]
+  int* flag;                      // [1] any trajectory still running (host loop / conditional)
+  double mw;                      // 1/N
+};
+
+__device__ __forceinline__ double* bslot(const BatchDev& d, int S, int slot, const Ctl* c) {
+  if (slot == SLOT_K1) return d.kb[c->k1i];
+  if (slot == SLOT_KLAST) return d.kb[S - c->k1i];
+  return d.kb[slot];
+}
+
+template <int KS> struct K16;
+template <> struct K16<MS_K_F16> {
+  using T = __half;
+  __device__ static T from(float v) { return __float2half_rn(v); }
+};
+template <> struct K16<MS_K_BF16> {
+  using T = __nv_bfloat16;
+  __device__ static T from(float v) { return __float2bfloat16_rn(v); }
+};
+
+struct BPrepArgs {
+  BatchDev d;
+  int S, l, kind, gate, count, out_slot, nterms;
+  double coef[kMaxStages];
+  int slot[kMaxStages];
+  int is_last, round_x, ws32, fs32;
+  int op_ks;  // 0: no GEMM operand; MS_K_F16 / MS_K_BF16: write the rounded operand
+};
+
+// stage combination + F + sin/cos (+ rounded GEMM operand) for every
+// trajectory: grid (ceil(n/256), B)
+template <class FS, class GS>
+__global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
+  const int b = blockIdx.y;
+  const BatchDev& d = p.d;
+  Ctl* c = d.ctl + b;
+  if (stage_skip(c, p.l, p.gate)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.count == CNT_DDD) c->evals_ddd += 1;
+    else if (p.count == CNT_K1) c->evals_k1 += 1;
+    else if (p.count == CNT_STAGE) c->evals_stage[p.l] += 1;
+  }
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.n) return;
+  const int64_t e = (int64_t)b * d.n + i;
+  const int ix = c->ix;
+  double* x = d.xb[ix];
+  double v;
+  const double h = p.kind == PREP_INIT_X1 ? c->h1 : c->h_att;
+  if (p.kind == PREP_X) {
+    v = x[e];
+    if (p.round_x) {
+      v = rn32(v);
+      x[e] = v;
+    }
+  } else if (p.kind == PREP_INIT_X1) {
+    v = __dadd_rn(x[e], __dmul_rn(h, d.kb[1][e]));
+  } else {
+    double cm = __dmul_rn(p.coef[0], bslot(d, p.S, p.slot[0], c)[e]);
+    for (int t = 1; t < p.nterms; ++t) cm = __dadd_rn(cm, __dmul_rn(p.coef[t], bslot(d, p.S, p.slot[t], c)[e]));
+    v = __dadd_rn(x[e], __dmul_rn(h, cm));
+    if (p.is_last) {
+      if (c->store32) {
+        const float hf = __double2float_rn(h);
+        float acc = __double2float_rn(x[e]);
+        for (int t = 0; t < p.nterms; ++t) {
+          const float cf = __fmul_rn(hf, __double2float_rn(p.coef[t]));
+          acc = __fadd_rn(acc, __fmul_rn(cf, __double2float_rn(bslot(d, p.S, p.slot[t], c)[e])));
+        }
+        d.xn[e] = v;
+        v = (double)acc;
+      }
+      d.xb[ix ^ 1][e] = v;
+    }
+  }
+  d.fvc[e] = (double)cvt<FS>(d.omega[e]);
+  const GS xg = cvt<GS>(v);
+  const GS sv = dsin<GS>(xg), cv = dcos<GS>(xg);
+  GS* sc = reinterpret_cast<GS*>(d.sc);
+  sc[e] = sv;
+  sc[(int64_t)d.B * d.n + e] = cv;
+  if (p.op_ks == MS_K_BF16) {
+    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(d.op) + (int64_t)b * 2 * d.ld;
+    op[i] = __float2bfloat16_rn((float)sv);
+    op[d.ld + i] = __float2bfloat16_rn((float)cv);
+  } else if (p.op_ks == MS_K_F16) {
+    __half* op = reinterpret_cast<__half*>(d.op) + (int64_t)b * 2 * d.ld;
+    op[i] = __float2half_rn((float)sv);
+    op[d.ld + i] = __float2half_rn((float)cv);
+  }
+}
+
+struct BRhsArgs {
+  BatchDev d;
+  int S, l, gate, out_slot, ws32;
+};
+
+// coupling epilogue of one (row i, trajectory b): k = (double)(RN_WS(omega) +
+// RN_WS(mw (c_i A - s_i B))), SS arithmetic
+template <class SS, class GS>
+__device__ __forceinline__ void b_epilogue(const BRhsArgs& a, int i, int b, SS A, SS Bv) {
+  const BatchDev& d = a.d;
+  Ctl* c = d.ctl + b;
+  if (stage_skip(c, a.l, a.gate)) return;
+  const int64_t e = (int64_t)b * d.n + i;
+  const GS* sc = reinterpret_cast<const GS*>(d.sc);
+  const SS si = (SS)sc[e], ci = (SS)sc[(int64_t)d.B * d.n + e];
+  const SS coup = mul<SS>(cvt<SS>(d.mw), sub<SS>(mul<SS>(ci, A), mul<SS>(si, Bv)));
+  const double o = ws_add(d.fvc[e], (double)coup, a.ws32);
+  bslot(d, a.S, a.out_slot, c)[i + (int64_t)b * d.n] = o;
+  if (!isfinite(o)) atomicOr(&c->nf_mask, 1 << a.l);
+}
+
+// CUDA-core batched sweep: 64 rows x 32 trajectories per CTA, j in chunks of
+// 32 through shared memory; each (i, b) sums j in ascending order — the
+// oracle's split order, so with binary64 or binary32 sin/cos it matches it
+// up to the libm ulp of sin/cos.
+constexpr int kBT_I = 64, kBT_B = 32, kBT_J = 32;
+template <class SS, class GS, int KS>
+__global__ void __launch_bounds__(256) kb_rhs_cc(BRhsArgs a) {
+  const BatchDev& d = a.d;
+  __shared__ GS Ks[kBT_I][kBT_J + 1];
+  __shared__ GS Ss[kBT_B][kBT_J + 1];
+  __shared__ GS Cs[kBT_B][kBT_J + 1];
+  const int i0 = blockIdx.x * kBT_I, b0 = blockIdx.y * kBT_B;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16
+  using KT = typename KElem<KS>::T;
+  const KT* K = reinterpret_cast<const KT*>(d.K);
+  const GS* S = reinterpret_cast<const GS*>(d.sc);
+  const GS* Cc = S + (int64_t)d.B * d.n;
+  SS A[4][2], Bv[4][2];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) { A[r][q] = SS(0); Bv[r][q] = SS(0); }
+  for (int j0 = 0; j0 < d.n; j0 += kBT_J) {
+    for (int t = threadIdx.x; t < kBT_I * kBT_J; t += 256) {
+      const int r = t / kBT_J, jj = t % kBT_J;
+      const int i = i0 + r, j = j0 + jj;
+      Ks[r][jj] = (i < d.n && j < d.n) ? (GS)k2f(K[(int64_t)i * d.ld + j]) : GS(0);
+    }
+    for (int t = threadIdx.x; t < kBT_B * kBT_J; t += 256) {
+      const int q = t / kBT_J, jj = t % kBT_J;
+      const int b = b0 + q, j = j0 + jj;
+      const bool ok = b < d.B && j < d.n;
+      Ss[q][jj] = ok ? S[(int64_t)b * d.n + j] : GS(0);
+      Cs[q][jj] = ok ? Cc[(int64_t)b * d.n + j] : GS(0);
+    }
+    __syncthreads();
+    const int jn = min(kBT_J, d.n - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const GS kv = Ks[ty * 4 + r][jj];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          A[r][q] = add<SS>(A[r][q], (SS)mul<GS>(kv, Ss[tx * 2 + q][jj]));
+          Bv[r][q] = add<SS>(Bv[r][q], (SS)mul<GS>(kv, Cs[tx * 2 + q][jj]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = i0 + ty * 4 + r, b = b0 + tx * 2 + q;
+      if (i < d.n && b < d.B) b_epilogue<SS, GS>(a, i, b, A[r][q], Bv[r][q]);
+    }
+}
+
+}  // namespace msb

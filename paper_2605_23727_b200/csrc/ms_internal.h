@@ -1,0 +1,20 @@
+// ms_internal.h — what other translation units may know of a system handle.
+#pragma once
+#include <cuda_runtime.h>
+#include "../../include/mixedstep_b200.h"
+
+namespace msb {
+struct SysView {
+  int mkind;        // MD_* (or a fixture id)
+  int n, d, ld;
+  int row0, row1;
+  int ks;           // MS_K_*
+  int dev, sms;
+  const void* K;
+  double coupling_k;
+  cudaStream_t stream;
+};
+SysView sys_view(ms_system_t s);
+// the thread-local message behind ms_last_error()
+void set_last_error(const char* msg);
+}  // namespace msb

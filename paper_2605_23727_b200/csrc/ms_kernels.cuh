@@ -324,12 +324,32 @@ template <> struct KVec<MS_K_BF16> {
 };
 template <> struct KVec<MS_K_SCALAR> {
   static constexpr int N = 4;
+  __device__ __forceinline__ static void unpack(const uint4&, float* o) {  // never reached (no matrix)
+    o[0] = o[1] = o[2] = o[3] = 0.f;
+  }
 };
 
-constexpr int kFastThreads = 512;  // 16 warps, one CTA per SM
+// Sweep geometry (overridable at build time for tuning sweeps)
+#ifndef MS_FAST_THREADS
+#define MS_FAST_THREADS 512  // 16 warps
+#endif
+#ifndef MS_FAST_MINB
+#define MS_FAST_MINB 1       // resident CTAs per SM (grid = SMs x MINB)
+#endif
+#ifndef MS_FAST_R
+#define MS_FAST_R 8          // rows per warp per sweep (fp32 accumulation)
+#endif
+#ifndef MS_CHUNK
+#define MS_CHUNK 2048        // columns per staged chunk
+#endif
+#ifndef MS_NS
+#define MS_NS 4              // mbarrier ring depth
+#endif
+constexpr int kFastThreads = MS_FAST_THREADS;
+constexpr int kFastMinBlocks = MS_FAST_MINB;
 constexpr int kFastWarps = kFastThreads / 32;
-constexpr int kChunkCols = 1024;   // columns per staged chunk
-constexpr int kStagesNS = 4;       // mbarrier ring depth
+constexpr int kChunkCols = MS_CHUNK;
+constexpr int kStagesNS = MS_NS;
 
 template <class GS, bool SPLIT>
 constexpr size_t fast_smem_bytes() {
@@ -337,7 +357,37 @@ constexpr size_t fast_smem_bytes() {
 }
 
 // Rows per warp per sweep.
-template <class SS, class GS> struct FastRows { static constexpr int R = (sizeof(GS) == 8 || sizeof(SS) == 8) ? 4 : 8; };
+template <class SS, class GS> struct FastRows {
+  static constexpr int R = (sizeof(GS) == 8 || sizeof(SS) == 8) ? (MS_FAST_R > 4 ? 4 : MS_FAST_R) : MS_FAST_R;
+};
+
+// one 128-bit K vector per row against VEC staged columns (split: A += K s, B += K c;
+// per-pair: A += G(x_i, x_j, K))
+template <int MODEL, bool SPLIT, class SS, class GS, int KS, int R, int VEC>
+__device__ __forceinline__ void sweep_step(const uint4 (&kv)[R], int nr, const GS (&s_loc)[VEC],
+                                           const GS (&c_loc)[VEC], const GS (&xi)[R], const GS (&pref)[R],
+                                           SS (&A)[R], SS (&B)[R]) {
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (k < nr) {
+      float kf[VEC];
+      KVec<KS>::unpack(kv[k], kf);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const GS kg = (GS)kf[v];
+        if (SPLIT) {
+          A[k] = add<SS>(A[k], (SS)mul<GS>(kg, s_loc[v]));
+          B[k] = add<SS>(B[k], (SS)mul<GS>(kg, c_loc[v]));
+        } else {
+          GS g;
+          if (MODEL == MD_LCO) g = mul<GS>(kg, sub<GS>(s_loc[v], xi[k]));
+          else g = mul<GS>(pref[k], mul<GS>(kg, datan<GS>(sub<GS>(s_loc[v], xi[k]))));
+          A[k] = add<SS>(A[k], (SS)g);
+        }
+      }
+    }
+  }
+}
 
 // ------------------------------------------------------------------------------
 // rhs_fast: one persistent CTA per SM; the CTA owns a contiguous balanced row
@@ -347,7 +397,7 @@ template <class SS, class GS> struct FastRows { static constexpr int R = (sizeof
 // from a warp-shuffle tree; the order of every row's sum depends only on N
 // (not on the row partition), so sharded runs are bitwise identical.
 template <int MODEL, bool SPLIT, class SS, class GS, int KS>
-__global__ void __launch_bounds__(kFastThreads, 1) k_rhs_fast(RhsArgs a) {
+__global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsArgs a) {
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NCOL = SPLIT ? 2 : 1;
@@ -427,7 +477,38 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_rhs_fast(RhsArgs a) {
       mbar_wait(&full[st], (q / kStagesNS) & 1);
       const GS* sv = stage_buf + (size_t)(st * NCOL) * kChunkCols;
       const GS* cv = sv + kChunkCols;
-      if (nr > 0) {
+#ifndef MS_PREFETCH
+#define MS_PREFETCH 0
+#endif
+      // fp64 accumulation (R = 4) gains from software pipelining, fp32 (R = 8)
+      // from more rows in flight (tools/tune_rhs.py, profiles/r1_tune_rhs.txt)
+      constexpr bool kPrefetch = MS_PREFETCH || (sizeof(SS) == 8 || sizeof(GS) == 8);
+      if (nr > 0 && kPrefetch && KS != MS_K_SCALAR) {
+        // software-pipelined: the next step's K vectors are in flight while
+        // the current ones are consumed
+        const int c0 = c * kChunkCols;
+        int col = lane * VEC;
+        uint4 kv[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (k < nr && col < cc) kv[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + col);
+        for (; col < cc; col += COLS_IT) {
+          uint4 kn[R];
+          const int nc = col + COLS_IT;
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (k < nr && nc < cc) kn[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + nc);
+          GS s_loc[VEC], c_loc[VEC];
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            s_loc[v] = sv[col + v];
+            if (SPLIT) c_loc[v] = cv[col + v];
+          }
+          sweep_step<MODEL, SPLIT, SS, GS, KS, R, VEC>(kv, nr, s_loc, c_loc, xi, pref, A, B);
+#pragma unroll
+          for (int k = 0; k < R; ++k) kv[k] = kn[k];
+        }
+      } else if (nr > 0) {
         const int c0 = c * kChunkCols;
         for (int col = lane * VEC; col < cc; col += COLS_IT) {
           GS s_loc[VEC], c_loc[VEC];
@@ -458,26 +539,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_rhs_fast(RhsArgs a) {
 #pragma unroll
             for (int k = 0; k < R; ++k)
               if (k < nr) kv[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + col);
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-              if (k < nr) {
-                float kf[VEC];
-                KVec<KS>::unpack(kv[k], kf);
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) {
-                  const GS kg = (GS)kf[v];
-                  if (SPLIT) {
-                    A[k] = add<SS>(A[k], (SS)mul<GS>(kg, s_loc[v]));
-                    B[k] = add<SS>(B[k], (SS)mul<GS>(kg, c_loc[v]));
-                  } else {
-                    GS g;
-                    if (MODEL == MD_LCO) g = mul<GS>(kg, sub<GS>(s_loc[v], xi[k]));
-                    else g = mul<GS>(pref[k], mul<GS>(kg, datan<GS>(sub<GS>(s_loc[v], xi[k]))));
-                    A[k] = add<SS>(A[k], (SS)g);
-                  }
-                }
-              }
-            }
+            sweep_step<MODEL, SPLIT, SS, GS, KS, R, VEC>(kv, nr, s_loc, c_loc, xi, pref, A, B);
           }
         }
       }
@@ -572,9 +634,8 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#ifdef MS_DEFINE_STEP_KERNELS
 // top of the solve_core loop (solver.cpp:273-296) and the final-step clip (:309-314)
-__device__ void loop_check(Ctl* c) {
+__device__ inline void loop_check(Ctl* c) {
   if (c->n_acc + c->n_fail >= c->max_iterations) {
     c->status = MS_MAX_ITERATIONS; c->done = 1; return;
   }
@@ -623,6 +684,84 @@ constexpr int kFinThreads = 256;
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000ll); }
 
+// The controller of one attempt (rk_step tail, solver.cpp:158-162, 201-214, and
+// the solve_core bookkeeping, :298-342), run by one thread once the weighted
+// max-norm err_max of the attempt is known. Returns whether the loop goes on.
+__device__ inline bool attempt_controller(Ctl* c, int S, int mode, int k1_elided, int fixed_k1, bool dead, bool stage_nf,
+                                   bool any_nf, double err_max, StepLogRec* log) {
+  if (mode == FIN_SOLVE && dead) return false;
+  // the need_k1 recompute of this attempt (solver.cpp:298-306)
+  if (mode == FIN_SOLVE && c->need_k1) {
+    if (k1_elided) c->evals_k1 += 1;
+    else if (c->nf_mask & 1) {
+      c->status = MS_NON_FINITE;
+      c->done = 1;
+      c->nf_mask = 0;
+      return false;
+    }
+  }
+  double err = nan64(), h_next;
+  bool accepted = false;
+  const double h = c->h_att;
+  if (stage_nf || any_nf) {
+    h_next = __dmul_rn(__dmul_rn(h, c->fac_min), 0.5);  // solver.cpp:158-162, 201-211
+  } else {
+    err = err_max;
+    if (!isfinite(err)) {
+      h_next = __dmul_rn(__dmul_rn(h, c->fac_min), 0.5);
+    } else {
+      accepted = err <= c->rel_tol;  // solver.cpp:212
+      h_next = d_adjust_step(h, err, c->rel_tol, c->safety, c->fac_min, c->fac_max, c->ctrl_exp);
+    }
+  }
+  c->err = err;
+  c->accepted = accepted;
+  c->h_next = h_next;
+  if (mode == FIN_STEP) return false;  // bs32_step: nf_mask is read back by the host
+  c->attempts += 1;
+  if (c->record_log) {
+    if (log && c->log_count < c->log_capacity) {
+      StepLogRec& r = log[c->log_count];
+      r.t = c->t; r.h = h; r.err = err; r.accepted = accepted;
+    }
+    c->log_count += 1;
+  }
+  c->need_k1 = 0;
+  c->nf_mask = 0;
+  if (accepted) {  // solver.cpp:321-336
+    c->n_acc += 1;
+    c->ix ^= 1;
+    const double tn = __dadd_rn(c->t, h);
+    c->t = c->last ? c->tf : (c->store32 ? rn32(tn) : tn);
+    if (!fixed_k1) c->k1i = S - c->k1i;  // FSAL: k1 <- k_last
+    c->h = h_next;
+    if (c->t >= c->tf) {
+      c->status = MS_COMPLETED;
+      c->done = 1;
+    }
+  } else {  // solver.cpp:337-341
+    c->n_fail += 1;
+    c->h = h_next;
+    c->need_k1 = 1;
+  }
+  if (!c->done) loop_check(c);
+  return !c->done;
+}
+
+struct InitArgs {
+  Bufs B;
+  const double* x0;
+  int64_t dn;
+  double exponent;  // 1/(order+1)
+};
+
+__device__ inline double seq_sum(const double* v, int64_t n) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s = __dadd_rn(s, v[i]);
+  return s;
+}
+
+#ifdef MS_DEFINE_STEP_KERNELS
 __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
   Ctl* c = f.B.ctl;
   const bool dead = c->done != 0;
@@ -677,91 +816,17 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
   const bool any_nf = atomicAdd(&c->any_nonfinite, 0) != 0;
   c->any_nonfinite = 0;
 
-  if (f.mode == FIN_SOLVE && dead) {
-    if (f.has_handle) cudaGraphSetConditional(f.handle, 0);
-    return;
-  }
-  // the need_k1 recompute of this attempt (solver.cpp:298-306)
-  if (f.mode == FIN_SOLVE && c->need_k1) {
-    if (f.k1_elided) c->evals_k1 += 1;
-    else if (c->nf_mask & 1) {
-      c->status = MS_NON_FINITE;
-      c->done = 1;
-      c->nf_mask = 0;
-      if (f.has_handle) cudaGraphSetConditional(f.handle, 0);
-      return;
-    }
-  }
-  double err = nan64(), h_next;
-  bool accepted = false;
-  const double h = c->h_att;
-  if (stage_nf || any_nf) {
-    h_next = __dmul_rn(__dmul_rn(h, c->fac_min), 0.5);  // solver.cpp:158-162, 201-211
-  } else {
-    double e = 0.0;
-    const int nb = gridDim.x;
-    for (int b = 0; b < nb; ++b) e = fmax(e, f.B.part[b]);
-    err = e;
-    if (!isfinite(err)) {
-      h_next = __dmul_rn(__dmul_rn(h, c->fac_min), 0.5);
-    } else {
-      accepted = err <= c->rel_tol;  // solver.cpp:212
-      h_next = d_adjust_step(h, err, c->rel_tol, c->safety, c->fac_min, c->fac_max, c->ctrl_exp);
-    }
-  }
-  c->err = err;
-  c->accepted = accepted;
-  c->h_next = h_next;
-  if (f.mode == FIN_STEP) {
-    return;  // bs32_step: nf_mask is read back by the host
-  }
-  c->attempts += 1;
-  if (c->record_log) {
-    if (c->log_count < c->log_capacity) {
-      StepLogRec& r = f.B.log[c->log_count];
-      r.t = c->t; r.h = h; r.err = err; r.accepted = accepted;
-    }
-    c->log_count += 1;
-  }
-  c->need_k1 = 0;
-  c->nf_mask = 0;
-  if (accepted) {  // solver.cpp:321-336
-    c->n_acc += 1;
-    c->ix ^= 1;
-    const double tn = __dadd_rn(c->t, h);
-    c->t = c->last ? c->tf : (c->store32 ? rn32(tn) : tn);
-    if (!f.fixed_k1) c->k1i = f.S - c->k1i;  // FSAL: k1 <- k_last
-    c->h = h_next;
-    if (c->t >= c->tf) {
-      c->status = MS_COMPLETED;
-      c->done = 1;
-    }
-  } else {  // solver.cpp:337-341
-    c->n_fail += 1;
-    c->h = h_next;
-    c->need_k1 = 1;
-  }
-  if (!c->done) loop_check(c);
-  if (f.has_handle) cudaGraphSetConditional(f.handle, c->done ? 0 : 1);
+  double e = 0.0;
+  if (!(dead || stage_nf || any_nf))
+    for (int b = 0; b < (int)gridDim.x; ++b) e = fmax(e, f.B.part[b]);
+  const bool more = attempt_controller(c, f.S, f.mode, f.k1_elided, f.fixed_k1, dead, stage_nf, any_nf, e, f.B.log);
+  if (f.has_handle && f.mode == FIN_SOLVE) cudaGraphSetConditional(f.handle, more ? 1 : 0);
 }
 
 // ------------------------------------------------------------------------------
 // initial_step (solver.cpp:420-451). The per-element terms are formed in
 // parallel; each of the three sums is then added by one thread in ascending
 // order (the oracle's fixed order).
-struct InitArgs {
-  Bufs B;
-  const double* x0;
-  int64_t dn;
-  double exponent;  // 1/(order+1)
-};
-
-__device__ double seq_sum(const double* v, int64_t n) {
-  double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s = __dadd_rn(s, v[i]);
-  return s;
-}
-
 __global__ void __launch_bounds__(1024) k_init_a(InitArgs a) {
   Ctl* c = a.B.ctl;
   if (c->done) return;

@@ -20,7 +20,8 @@ void go(const RhsLaunch& L, const RhsArgs& a) {
     attr_done = true;
   }
   const int rows = a.row1 - a.row0;
-  const int grid = rows < L.num_sms ? rows : L.num_sms;
+  const int slots = L.num_sms * kFastMinBlocks;
+  const int grid = rows < slots ? rows : slots;
   kern<<<grid, kFastThreads, smem, L.stream>>>(a);
 }
 

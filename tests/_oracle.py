@@ -36,6 +36,8 @@ _SIGS = [
     ("orc_system_destroy", C.c_int, [_VP]),
     ("orc_system_fill_k_uniform", C.c_int, [_VP, C.c_uint64, C.c_uint64, C.c_double, C.c_double]),
     ("orc_system_get_k", C.c_int, [_VP, _DP]),
+    ("orc_system_set_op_round", C.c_int, [_VP, C.c_int]),
+    ("orc_system_set_omega", C.c_int, [_VP, _DP]),
     ("orc_make_lco", C.c_int, [C.c_int, C.c_uint64, C.POINTER(_VP)]),
     ("orc_make_kuramoto", C.c_int, [C.c_int, C.c_double, C.c_double, C.c_uint64, C.POINTER(_VP)]),
     ("orc_make_cc", C.c_int, [C.c_int, C.c_double, C.c_double, C.c_uint64, C.POINTER(_VP)]),
@@ -155,6 +157,13 @@ class OracleSystem:
         out = (C.c_int64 * 4)()
         lib().orc_system_flop_profile(self._h, out)
         return tuple(out)
+
+    def set_op_round(self, ks: int) -> None:
+        check(lib().orc_system_set_op_round(self._h, ks), "set_op_round")
+
+    def set_omega(self, omega) -> None:
+        om = f64(omega)
+        check(lib().orc_system_set_omega(self._h, om.ctypes.data_as(_DP)), "set_omega")
 
     def get_k(self) -> np.ndarray:
         n = self.agents()

@@ -1,0 +1,126 @@
+"""Batched ensembles sharing one K (config C5) against per-trajectory oracle
+systems (same K, own omega_b), through the ms_batch_* C-ABI.
+
+CUDA-core rows sum each (i, b) in ascending j — the oracle's split order — so
+they agree up to the libm ulp of sin/cos. Tensor-core rows (binary32, K in
+f16/bf16) use operands rounded to K's format with exact products and the
+tensor core's fp32 accumulation: the oracle applies the same operand rounding
+(op_round) and the reordering bound TOL = 2 N eps32 mw sum_j |K_ij| is used."""
+import itertools
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from paper_2605_23727_b200 import _abi
+from paper_2605_23727_b200.batch import DeviceBatch
+from paper_2605_23727_b200.configs import TWO_PI, config5_batch, rng_normal, rng_uniform
+from paper_2605_23727_b200.precision import B32, B64, DDD, DDS, SSS, StagePrecision
+from paper_2605_23727_b200.solver import SolveStatus
+from paper_2605_23727_b200.systems import DeviceSystem, SystemSpec
+
+pytestmark = pytest.mark.gpu
+ROWS = [StagePrecision(f, s, g) for f, s, g in itertools.product((B32, B64), repeat=3)]
+OPR = {"bf16": _abi.MS_K_BF16, "f16": _abi.MS_K_F16}
+
+
+def _ensemble(B, n, ks, seed=5):
+    spec = SystemSpec("kuramoto", n, k_storage=ks, omega=np.zeros(n), k_uniform=(seed, 2, 0.0, 2.0))
+    omega = rng_normal(seed, 0, B * n).reshape(B, n)
+    x = rng_uniform(seed, 1, B * n, 0.0, TWO_PI).reshape(B, n)
+    return spec, omega, x
+
+
+def _tol(sp, n, out, kabs_rowsum):
+    eps = lambda f: 2.0 ** -23 if f == B32 else 2.0 ** -52
+    ws = B32 if (sp.f_prec == B32 and sp.sum_prec == B32) else B64
+    return 2.0 * n * eps(sp.sum_prec) * kabs_rowsum / n * 2.0 + 4.0 * eps(B32) * kabs_rowsum / n \
+        + 4.0 * eps(ws) * np.abs(out) + 1e-300
+
+
+@pytest.mark.parametrize("sp", ROWS, ids=str)
+def test_batch_rhs_cuda_core(gpu, sp):
+    spec, omega, x = _ensemble(5, 203, "f32")
+    dev = DeviceSystem(spec)
+    bat = DeviceBatch(dev, omega, tensor_cores=False)
+    got = bat.eval_rhs(x, sp)
+    orc = O.OracleSystem(spec)
+    ks = np.abs(orc.get_k()).sum(axis=1)
+    for b in range(5):
+        orc.set_omega(omega[b])
+        ref = orc.eval_rhs(0.0, x[b], sp)
+        assert np.all(np.abs(got[b] - ref) <= _tol(sp, 203, ref, ks)), b
+
+
+@pytest.mark.parametrize("ks", ["bf16", "f16"])
+@pytest.mark.parametrize("shape", [(160, 300), (64, 128), (7, 1000)])
+def test_batch_rhs_tensor_cores(gpu, ks, shape):
+    B, n = shape
+    spec, omega, x = _ensemble(B, n, ks)
+    dev = DeviceSystem(spec)
+    bat = DeviceBatch(dev, omega, tensor_cores=True)
+    orc = O.OracleSystem(spec)
+    kabs = np.abs(orc.get_k()).sum(axis=1)
+    got = bat.eval_rhs(x, SSS)
+    orc.set_op_round(OPR[ks])
+    picks = sorted({0, 1, B // 2, B - 1})
+    for b in picks:
+        orc.set_omega(omega[b])
+        ref = orc.eval_rhs(0.0, x[b], SSS)
+        err = np.abs(got[b] - ref)
+        tol = _tol(SSS, n, ref, kabs)
+        assert np.all(err <= tol), (b, float(np.max(err / tol)))
+    # binary64 rows of the same ensemble stay exact on CUDA cores
+    got64 = bat.eval_rhs(x, DDD)
+    orc.set_op_round(0)
+    for b in picks[:2]:
+        orc.set_omega(omega[b])
+        ref = orc.eval_rhs(0.0, x[b], DDD)
+        assert np.all(np.abs(got64[b] - ref) <= _tol(DDD, n, ref, kabs))
+
+
+def test_batch_tensor_cores_full_c5_shape(gpu):
+    """The C5 shape (B = 1024, N = 2048): whole GEMM tiles, spot-checked rows."""
+    w = config5_batch()
+    dev = DeviceSystem(w.spec)
+    bat = DeviceBatch(dev, w.omega, tensor_cores=True)
+    got = bat.eval_rhs(w.x0, SSS)
+    assert np.all(np.isfinite(got))
+    orc = O.OracleSystem(w.spec)
+    orc.set_op_round(_abi.MS_K_BF16)
+    kabs = np.abs(orc.get_k()).sum(axis=1)
+    for b in (0, 511, 1023):
+        orc.set_omega(w.omega[b])
+        ref = orc.eval_rhs(0.0, w.x0[b], SSS)
+        assert np.all(np.abs(got[b] - ref) <= _tol(SSS, 2048, ref, kabs)), b
+
+
+@pytest.mark.parametrize("tc", [False, True])
+def test_batch_solve_vs_oracle(gpu, tc):
+    B, n = 6, 128
+    spec, omega, x0 = _ensemble(B, n, "bf16", seed=9)
+    from paper_2605_23727_b200.configs import SSS_D
+    from paper_2605_23727_b200.solver import SolverConfig
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    dev = DeviceSystem(spec)
+    bat = DeviceBatch(dev, omega, tensor_cores=tc)
+    res = bat.solve(x0, 0.0, 4.0, SSS_D, cfg)
+    orc = O.OracleSystem(spec)
+    if tc:
+        orc.set_op_round(_abi.MS_K_BF16)
+    O.set_threads(4)
+    for b in range(B):
+        orc.set_omega(omega[b])
+        o = O.solve(orc, x0[b], 0.0, 4.0, SSS_D, cfg)
+        assert res.status[b] == o.status == SolveStatus.Completed
+        att = o.n_accepted + o.n_failed
+        assert abs(res.n_accepted[b] - o.n_accepted) <= max(1, 0.01 * o.n_accepted), b
+        assert abs(res.n_failed[b] - o.n_failed) <= max(1, 0.01 * att), b
+        assert res.t_reached[b] == o.t_reached
+        scale = np.maximum(np.abs(o.final_state), 1e-3)
+        assert np.all(np.abs(res.final_state[b] - o.final_state) <= 1e-5 * scale), b
+        # evaluation budget of the reference loop: 2 (initial_step) + 1 (cold k1)
+        # + 3 per accepted + 4 per rejected attempt (solver.cpp:255-306)
+        assert res.rhs_evals[b] == 3 + 3 * res.n_accepted[b] + 4 * res.n_failed[b]
+        assert o.flops.rhs_evals == 3 + 3 * o.n_accepted + 4 * o.n_failed
+    assert res.attempts >= int(max(res.n_accepted + res.n_failed))

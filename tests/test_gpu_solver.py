@@ -234,7 +234,9 @@ def test_lco_solve_matches_oracle(gpu, variant):
         t, h, err, acc = b[i - 1]
         h_dev, h_orc = S.adjust_step(h, err, cfg.rel_tol, cfg), O.adjust_step(h, err, cfg.rel_tol, cfg)
         assert h_dev != h_orc and abs(h_dev - h_orc) <= 4 * 2.0 ** -52 * abs(h_orc), (i, h_dev, h_orc)
-    _same_run(r, o, 1e-4 if variant == PolicyVariant.Single else 1e-8, exact_counts=False)
+    # after a split the two runs are two valid solves of the same problem: the
+    # BASELINE gate (1e-5 relative, counts +-1%) applies
+    _same_run(r, o, 1e-4 if variant == PolicyVariant.Single else 1e-5, exact_counts=False)
 
 
 def test_dp54_reference(gpu):  # test_solver.cpp:197-211 + oracle parity
