@@ -308,6 +308,10 @@ int ms_batch_destroy(ms_batch_t b);
 int ms_batch_eval_rhs(ms_batch_t b, const double* x, ms_stage_prec sp, double* out);
 int ms_batch_solve(ms_batch_t b, const double* x0, double t0, double t_final, const ms_policy* policy,
                    const ms_solver_config* cfg, ms_batch_result* res);
+/* measurement hook: mean device ms of the ensemble's contraction kernel and
+ * of its stage-prep kernel over `iters` evaluations at host state x */
+int ms_batch_profile_rhs(ms_batch_t b, const double* x, ms_stage_prec sp, int iters, double* rhs_ms,
+                         double* prep_ms);
 
 /* Measurement hook (no reference counterpart): times `iters` evaluations of
  * the RHS at host state x under row sp with CUDA events on the handle's

@@ -151,18 +151,22 @@ void eval_kuramoto_split(const ModelParams& p, const Vec& x, Vec& out) {
     s[static_cast<std::size_t>(j)] = std::sin(xg);
     c[static_cast<std::size_t>(j)] = std::cos(xg);
   }
-  // tensor-core ensemble semantics (ms_batch_*): the GEMM operands are the
-  // binary32 sin/cos rounded once to K's 16-bit format; the epilogue keeps them
-  std::vector<GS> so = s, co = c;
-  if (p.op_round && sizeof(SS) == 4 && sizeof(GS) == 4) {
-    for (std::size_t j = 0; j < so.size(); ++j) {
-      if (p.op_round == 2) {
-        so[j] = static_cast<GS>(static_cast<_Float16>(static_cast<float>(s[j])));
-        co[j] = static_cast<GS>(static_cast<_Float16>(static_cast<float>(c[j])));
-      } else {
-        so[j] = static_cast<GS>(static_cast<__bf16>(static_cast<float>(s[j])));
-        co[j] = static_cast<GS>(static_cast<__bf16>(static_cast<float>(c[j])));
-      }
+  // tensor-core ensemble semantics (ms_batch_*, csrc/ms_gemm_tc.cuh): each
+  // binary32 sin/cos enters the GEMM as hi + lo in K's 16-bit format
+  // (hi = RN16(v), lo = RN16(v - hi)); the two partial sums are accumulated
+  // separately in binary32 and added once: A = RN32(A_hi + A_lo).
+  const bool tc = p.op_round && sizeof(SS) == 4 && sizeof(GS) == 4;
+  std::vector<GS> sh = s, sl(s.size(), GS(0)), ch = c, cl(c.size(), GS(0));
+  if (tc) {
+    auto r16 = [&](float v) -> float {
+      return p.op_round == 2 ? static_cast<float>(static_cast<_Float16>(v)) : static_cast<float>(static_cast<__bf16>(v));
+    };
+    for (std::size_t j = 0; j < s.size(); ++j) {
+      const float sv = static_cast<float>(s[j]), cv = static_cast<float>(c[j]);
+      sh[j] = static_cast<GS>(r16(sv));
+      sl[j] = static_cast<GS>(r16(sv - static_cast<float>(sh[j])));
+      ch[j] = static_cast<GS>(r16(cv));
+      cl[j] = static_cast<GS>(r16(cv - static_cast<float>(ch[j])));
     }
   }
   const SS mw = static_cast<SS>(p.m[0]);
@@ -172,10 +176,24 @@ void eval_kuramoto_split(const ModelParams& p, const Vec& x, Vec& out) {
   for (int i = 0; i < n; ++i) {
     const FS fval = static_cast<FS>(p.omega[static_cast<std::size_t>(i)]);
     SS A = SS(0), B = SS(0);
-    for (int j = 0; j < n; ++j) {
-      const GS k = kij<GS, HasK>(p, K, i, j);
-      A = A + static_cast<SS>(k * so[static_cast<std::size_t>(j)]);
-      B = B + static_cast<SS>(k * co[static_cast<std::size_t>(j)]);
+    if (tc) {
+      SS Al = SS(0), Bl = SS(0);
+      for (int j = 0; j < n; ++j) {
+        const GS k = kij<GS, HasK>(p, K, i, j);
+        const std::size_t u = static_cast<std::size_t>(j);
+        A = A + static_cast<SS>(k * sh[u]);
+        Al = Al + static_cast<SS>(k * sl[u]);
+        B = B + static_cast<SS>(k * ch[u]);
+        Bl = Bl + static_cast<SS>(k * cl[u]);
+      }
+      A = A + Al;
+      B = B + Bl;
+    } else {
+      for (int j = 0; j < n; ++j) {
+        const GS k = kij<GS, HasK>(p, K, i, j);
+        A = A + static_cast<SS>(k * s[static_cast<std::size_t>(j)]);
+        B = B + static_cast<SS>(k * c[static_cast<std::size_t>(j)]);
+      }
     }
     const SS coup = mw * ((static_cast<SS>(c[static_cast<std::size_t>(i)]) * A) -
                           (static_cast<SS>(s[static_cast<std::size_t>(i)]) * B));

@@ -138,6 +138,7 @@ SIGNATURES = [
     ("ms_batch_eval_rhs", C.c_int, [C.c_void_p, _DP, StagePrec, _DP]),
     ("ms_batch_solve", C.c_int, [C.c_void_p, _DP, C.c_double, C.c_double, C.POINTER(Policy),
                                  C.POINTER(SolverConfigC), C.POINTER(BatchResultC)]),
+    ("ms_batch_profile_rhs", C.c_int, [C.c_void_p, _DP, StagePrec, C.c_int, _DP, _DP]),
     ("ms_profile_rhs", C.c_int, [C.c_void_p, _DP, StagePrec, C.c_int, _DP, _DP]),
     ("ms_dp54_reference", C.c_int, [C.c_void_p, _DP, C.c_double, C.c_double, C.POINTER(SolverConfigC),
                                     C.POINTER(SolveResultC)]),

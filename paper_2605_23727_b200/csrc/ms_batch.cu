@@ -301,7 +301,8 @@ void launch_brhs_cc(ms_batch* m, cudaStream_t st, const BRhsArgs& a) {
   }
 }
 
-void beval(ms_batch* m, cudaStream_t st, const BEval& e, const ms_stage_prec& sp) {
+void beval(ms_batch* m, cudaStream_t st, const BEval& e, const ms_stage_prec& sp, cudaEvent_t mid0 = nullptr,
+           cudaEvent_t mid1 = nullptr) {
   const bool fs32 = is32(sp.f_prec), ss32 = is32(sp.sum_prec), gs32 = is32(sp.g_prec);
   const bool use_tc = m->tc && is_sss(sp);
   BPrepArgs p{};
@@ -332,6 +333,7 @@ void beval(ms_batch* m, cudaStream_t st, const BEval& e, const ms_stage_prec& sp
   a.gate = e.gate;
   a.out_slot = e.out_slot;
   a.ws32 = p.ws32;
+  if (mid0) BCK(cudaEventRecord(mid0, st));
   if (use_tc) {
     launch_tc_gemm(m->gemm, a, st);
   } else if (ss32) {
@@ -342,6 +344,7 @@ void beval(ms_batch* m, cudaStream_t st, const BEval& e, const ms_stage_prec& sp
     else launch_brhs_cc<double, double>(m, st, a);
   }
   BCK(cudaGetLastError());
+  if (mid1) BCK(cudaEventRecord(mid1, st));
 }
 
 BEval bstage(int l) {
@@ -497,7 +500,7 @@ int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t vec = al(sizeof(double) * bn);
     size_t total = vec /*omega*/ + 2 * vec + (kMaxStages + 1) * vec + 3 * vec /*xn, scr0, scr1*/ +
-                   2 * vec /*sc*/ + al(sizeof(uint16_t) * 2 * (size_t)batch * ld) /*op*/ + vec /*fvc*/ +
+                   2 * vec /*sc*/ + al(sizeof(uint16_t) * 4 * (size_t)batch * ld) /*op*/ + vec /*fvc*/ +
                    al(sizeof(Ctl) * batch) + al(sizeof(int));
     char* base = nullptr;
     BCK(cudaMalloc(&base, total));
@@ -523,7 +526,7 @@ int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t
     d.scr0 = reinterpret_cast<double*>(take(sizeof(double) * bn));
     d.scr1 = reinterpret_cast<double*>(take(sizeof(double) * bn));
     d.sc = take(sizeof(double) * 2 * bn);
-    d.op = take(sizeof(uint16_t) * 2 * (size_t)batch * ld);
+    d.op = take(sizeof(uint16_t) * 4 * (size_t)batch * ld);
     d.fvc = reinterpret_cast<double*>(take(sizeof(double) * bn));
     d.ctl = reinterpret_cast<Ctl*>(take(sizeof(Ctl) * batch));
     d.flag = reinterpret_cast<int*>(take(sizeof(int)));
@@ -575,6 +578,43 @@ int ms_batch_eval_rhs(ms_batch_t m, const double* x, ms_stage_prec sp, double* o
     beval(m, m->st, e, sp);
     BCK(cudaMemcpyAsync(out, m->d.kb[0], sizeof(double) * bn, cudaMemcpyDeviceToHost, m->st));
     BCK(cudaStreamSynchronize(m->st));
+  });
+}
+
+int ms_batch_profile_rhs(ms_batch_t m, const double* x, ms_stage_prec sp, int iters, double* rhs_ms,
+                         double* prep_ms) {
+  return bguard([&] {
+    if (!m || !x || iters < 1) throw InvalidArg("batch_profile_rhs: bad arguments");
+    check_prec_b(sp);
+    std::lock_guard<std::mutex> lk(m->mu);
+    BCK(cudaSetDevice(m->sv.dev));
+    const size_t bn = (size_t)m->B * m->d.n;
+    std::memset(m->ctl_host, 0, sizeof(Ctl) * m->B);
+    BCK(cudaMemcpyAsync(m->d.ctl, m->ctl_host, sizeof(Ctl) * m->B, cudaMemcpyHostToDevice, m->st));
+    BCK(cudaMemcpyAsync(m->d.xb[0], x, sizeof(double) * bn, cudaMemcpyHostToDevice, m->st));
+    BEval e;
+    e.l = 0;
+    e.kind = PREP_X;
+    e.out_slot = 0;
+    beval(m, m->st, e, sp);
+    std::vector<cudaEvent_t> ev(3 * (size_t)iters);
+    for (auto& v : ev) BCK(cudaEventCreate(&v));
+    for (int i = 0; i < iters; ++i) {
+      BCK(cudaEventRecord(ev[3 * i], m->st));
+      beval(m, m->st, e, sp, ev[3 * i + 1], ev[3 * i + 2]);
+    }
+    BCK(cudaStreamSynchronize(m->st));
+    double tr = 0, tp = 0;
+    for (int i = 0; i < iters; ++i) {
+      float a = 0, b = 0;
+      BCK(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+      BCK(cudaEventElapsedTime(&b, ev[3 * i + 1], ev[3 * i + 2]));
+      tp += a;
+      tr += b;
+    }
+    for (auto& v : ev) cudaEventDestroy(v);
+    if (rhs_ms) *rhs_ms = tr / iters;
+    if (prep_ms) *prep_ms = tp / iters;
   });
 }
 

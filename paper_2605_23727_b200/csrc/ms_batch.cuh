@@ -26,7 +26,7 @@ struct BatchDev {
   double* scr0;                   // initial_step terms
   double* scr1;
   void* sc;                       // GS-typed s (first B*n) and c (next B*n)
-  void* op;                       // GEMM operand [B][2][ld] in K's 16-bit format (s row, c row)
+  void* op;                       // GEMM operand [B][4][ld] in K's 16-bit format: s_hi, s_lo, c_hi, c_lo
   double* fvc;                    // F (omega in FS) [B][n]
   Ctl* ctl;                       // [B]
   int* flag;                      // [1] any trajectory still running (host loop / conditional)
@@ -110,14 +110,24 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
   GS* sc = reinterpret_cast<GS*>(d.sc);
   sc[e] = sv;
   sc[(int64_t)d.B * d.n + e] = cv;
+  // two-term operands: v = hi + lo with hi = RN16(v), lo = RN16(v - hi) (the
+  // difference is exact in binary32), so K*hi + K*lo carries ~16-22 bits of v
   if (p.op_ks == MS_K_BF16) {
-    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(d.op) + (int64_t)b * 2 * d.ld;
-    op[i] = __float2bfloat16_rn((float)sv);
-    op[d.ld + i] = __float2bfloat16_rn((float)cv);
+    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(d.op) + (int64_t)b * 4 * d.ld;
+    const float s32 = (float)sv, c32 = (float)cv;
+    const __nv_bfloat16 sh = __float2bfloat16_rn(s32), ch = __float2bfloat16_rn(c32);
+    op[i] = sh;
+    op[d.ld + i] = __float2bfloat16_rn(__fsub_rn(s32, __bfloat162float(sh)));
+    op[2 * d.ld + i] = ch;
+    op[3 * d.ld + i] = __float2bfloat16_rn(__fsub_rn(c32, __bfloat162float(ch)));
   } else if (p.op_ks == MS_K_F16) {
-    __half* op = reinterpret_cast<__half*>(d.op) + (int64_t)b * 2 * d.ld;
-    op[i] = __float2half_rn((float)sv);
-    op[d.ld + i] = __float2half_rn((float)cv);
+    __half* op = reinterpret_cast<__half*>(d.op) + (int64_t)b * 4 * d.ld;
+    const float s32 = (float)sv, c32 = (float)cv;
+    const __half sh = __float2half_rn(s32), ch = __float2half_rn(c32);
+    op[i] = sh;
+    op[d.ld + i] = __float2half_rn(__fsub_rn(s32, __half2float(sh)));
+    op[2 * d.ld + i] = ch;
+    op[3 * d.ld + i] = __float2half_rn(__fsub_rn(c32, __half2float(ch)));
   }
 }
 

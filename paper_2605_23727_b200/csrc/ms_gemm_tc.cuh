@@ -1,12 +1,14 @@
 // ms_gemm_tc.cuh — the ensemble's stage contraction on the 5th-generation
 // tensor cores (tcgen05), with the Kuramoto coupling as its fused epilogue.
 //
-//   D[i][2b]   = sum_j K_ij sin(theta_bj)      D[i][2b+1] = sum_j K_ij cos(theta_bj)
-//   k_b[i]     = (double)(omega_bi + (1/N)(c_bi D[i][2b] - s_bi D[i][2b+1]))
+//   A_bi = D[i][4b] + D[i][4b+1] = sum_j K_ij (s_hi + s_lo)(theta_bj)
+//   B_bi = D[i][4b+2] + D[i][4b+3] = sum_j K_ij (c_hi + c_lo)(theta_bj)
+//   k_b[i] = (double)(omega_bi + (1/N)(c_bi A_bi - s_bi B_bi))
 //
 // A = K (N x N, bf16/f16, K-major, row stride ld), B = the operand rows the
-// prep kernel writes ([B][2][ld]: sin row, cos row per trajectory, K-major),
-// M = N, N_gemm = 2B, K_gemm = N. One CTA computes a 128 x 256 tile:
+// prep kernel writes ([B][4][ld]: the two-term split of sin and of cos per
+// trajectory, K-major), M = N, N_gemm = 4B, K_gemm = N. One CTA computes a
+// 128 x 256 tile (64 trajectories):
 //   warp 0        TMA producer: cp.async.bulk.tensor (SWIZZLE_128B) of the A
 //                 and B k-blocks (64 columns) into a 4-stage mbarrier ring
 //   warp 1        TMEM allocator + MMA issuer: one elected thread issues
@@ -15,9 +17,11 @@
 //                 tcgen05.commit releases each smem stage / signals the epilogue
 //   warps 2..5    epilogue: tcgen05.ld 32x32b.x32 (one TMEM lane = one row),
 //                 the coupling formula above in binary32, binary64 stores
-// The sin/cos operands are rounded to K's 16-bit format by the prep kernel;
-// products are exact in fp32; accumulation order/precision is the tensor
-// core's, so parity with the oracle is by the reordering tolerance.
+// Each binary32 sin/cos value enters as hi + lo, both in K's 16-bit format
+// (hi = RN16(v), lo = RN16(v - hi)); K is exact in its storage format, so every
+// product is exact in fp32 and the operand keeps ~16 (bf16) / 22 (f16) bits.
+// Accumulation order/precision is the tensor core's: parity with the oracle
+// (same split) is by the reordering tolerance.
 #pragma once
 
 #include <cuda.h>
@@ -46,7 +50,7 @@ struct TcGemm {
 
 struct TcArgs {
   BRhsArgs a;
-  int n, nb2;  // rows of K, GEMM columns (2B)
+  int n, ncol;  // rows of K, GEMM columns (4B: s_hi, s_lo, c_hi, c_lo per trajectory)
   uint32_t idesc;
 };
 
@@ -96,6 +100,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* tmem_full = empty + kTcStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
+  __shared__ int tc_skip[kTcBN / 4];
+  __shared__ double* tc_out[kTcBN / 4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * kTcBM, n0 = blockIdx.y * kTcBN;
   const int nkb = (t.n + kTcBK - 1) / kTcBK;
@@ -167,11 +173,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    : "memory");
     }
   } else {  // epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +32
+    const int q4 = warp & 3;
+    const int et = threadIdx.x - 64;  // 0..127
+    const int tb0 = n0 >> 2;          // first trajectory of this tile
+    const BatchDev& d = t.a.d;
+    // per-trajectory decisions of this tile, read once (not per element)
+    if (et < kTcBN / 4) {
+      const int b = tb0 + et;
+      int skip = 1;
+      double* outp = nullptr;
+      if (b < d.B) {
+        const Ctl* c = d.ctl + b;
+        skip = stage_skip(c, t.a.l, t.a.gate) ? 1 : 0;
+        outp = bslot(d, t.a.S, t.a.out_slot, c) + (int64_t)b * d.n;
+      }
+      tc_skip[et] = skip;
+      tc_out[et] = outp;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
     tc_wait(tmem_full, 0);
     tc_fence_after();
-    const int q4 = warp & 3;
     const int i = m0 + q4 * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
+    const float mw = (float)d.mw;
+    const float* scf = reinterpret_cast<const float*>(d.sc);
+    const int64_t bn = (int64_t)d.B * d.n;
 #pragma unroll 1
     for (int c0 = 0; c0 < kTcBN; c0 += 32) {
       uint32_t r[32];
@@ -184,13 +210,33 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
           : "r"(lane_addr + (uint32_t)c0));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (i < t.n) {
+      if (i >= t.n) continue;
+      // 8 trajectories per 32 columns: issue all their loads, then compute
+      float sv[8], cv[8];
+      double fv[8];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int col = n0 + c0 + 2 * q;
-          if (col < t.nb2)
-            b_epilogue<float, float>(t.a, i, col >> 1, __uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+      for (int q = 0; q < 8; ++q) {
+        const int tq = (c0 >> 2) + q;
+        const int b = tb0 + tq;
+        sv[q] = cv[q] = 0.f;
+        fv[q] = 0.0;
+        if (!tc_skip[tq]) {
+          const int64_t e = (int64_t)b * d.n + i;
+          sv[q] = scf[e];
+          cv[q] = scf[bn + e];
+          fv[q] = d.fvc[e];
         }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int tq = (c0 >> 2) + q;
+        if (tc_skip[tq]) continue;
+        const float A = __fadd_rn(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]));
+        const float Bv = __fadd_rn(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(cv[q], A), __fmul_rn(sv[q], Bv)));
+        const double o = ws_add(fv[q], (double)coup, t.a.ws32);
+        tc_out[tq][i] = o;
+        if (!isfinite(o)) atomicOr(&d.ctl[tb0 + tq].nf_mask, 1 << t.a.l);
       }
     }
   }
@@ -224,7 +270,7 @@ inline void tc_gemm_setup(TcGemm& g, const BatchDev& d, int sms) {
     if (r != CUDA_SUCCESS) throw std::runtime_error("tensor map (K) encode failed");
   }
   {
-    const cuuint64_t dims[2] = {(cuuint64_t)d.n, (cuuint64_t)(2 * d.B)};
+    const cuuint64_t dims[2] = {(cuuint64_t)d.n, (cuuint64_t)(4 * d.B)};
     const cuuint64_t strides[1] = {(cuuint64_t)d.ld * 2};
     const cuuint32_t box[2] = {kTcBK, kTcBN};
     const cuuint32_t es[2] = {1, 1};
@@ -234,7 +280,7 @@ inline void tc_gemm_setup(TcGemm& g, const BatchDev& d, int sms) {
     if (r != CUDA_SUCCESS) throw std::runtime_error("tensor map (operand) encode failed");
   }
   g.grid_m = (d.n + kTcBM - 1) / kTcBM;
-  g.grid_n = (2 * d.B + kTcBN - 1) / kTcBN;
+  g.grid_n = (4 * d.B + kTcBN - 1) / kTcBN;
   cudaError_t e = cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
   if (e != cudaSuccess) throw std::runtime_error(std::string("tc gemm smem attribute: ") + cudaGetErrorString(e));
   g.ready = true;
@@ -254,7 +300,7 @@ inline void launch_tc_gemm(const TcGemm& g, const BRhsArgs& a, cudaStream_t st) 
   TcArgs t{};
   t.a = a;
   t.n = a.d.n;
-  t.nb2 = 2 * a.d.B;
+  t.ncol = 4 * a.d.B;
   t.idesc = tc_idesc(a.d.ks);
   dim3 grid(g.grid_m, g.grid_n);
   k_tc_gemm<<<grid, kTcThreads, kTcSmem, st>>>(g.tmA, g.tmB, t);

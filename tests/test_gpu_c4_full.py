@@ -1,0 +1,74 @@
+"""Config C4 at BASELINE.json's full size (Kuramoto N = 32768, K f32 4 GiB):
+the device against the oracle on the same seeded inputs, through properties
+that do not need a full CPU solve (tens of minutes): one RHS evaluation per
+precision row, the first attempts of the adaptive loop, and rows of the
+device-generated K against an independent vectorised SplitMix64."""
+import os
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from paper_2605_23727_b200 import solver as S
+from paper_2605_23727_b200.configs import config4_kuramoto
+from paper_2605_23727_b200.precision import B32, DDD, DDS, SSS
+from paper_2605_23727_b200.systems import DeviceSystem
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def c4(gpu):
+    w = config4_kuramoto()
+    O.set_threads(os.cpu_count() or 1)
+    return w, DeviceSystem(w.spec), O.OracleSystem(w.spec)
+
+
+def test_c4_rhs_every_row(c4):
+    w, dev, orc = c4
+    n = w.spec.n_agents
+    gsum = 2.0 * 2.0 * n  # |K| <= 2, |s|,|c| <= 1, both sums
+    for sp in (SSS, DDS, DDD):
+        a, b = dev.eval_rhs(0.0, w.x0, sp), orc.eval_rhs(0.0, w.x0, sp)
+        eps = 2.0 ** -23 if sp.sum_prec == B32 else 2.0 ** -52
+        tol = 2.0 * n * eps * gsum / n + 4.0 * eps * np.abs(b) + (4 * 2.0 ** -23 * gsum / n if sp.g_prec == B32 else 0)
+        assert np.all(np.abs(a - b) <= tol), (sp, float(np.max(np.abs(a - b) / tol)))
+        # the typical deviation is far below the worst-case bound
+        assert np.median(np.abs(a - b)) <= (1e-5 if sp.sum_prec == B32 else 1e-12)
+
+
+def test_c4_first_attempts(c4):
+    w, dev, orc = c4
+    cfg = S.SolverConfig(rel_tol=w.cfg.rel_tol, abs_tol=w.cfg.abs_tol, time_limits_enabled=False, max_iterations=4)
+    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, cfg)
+    o = O.solve(orc, w.x0, w.t0, w.tf, w.policy, cfg)
+    assert r.status == o.status == S.SolveStatus.MaxIterations
+    assert (r.n_accepted, r.n_failed) == (o.n_accepted, o.n_failed)
+    assert r.t_reached == pytest.approx(o.t_reached, rel=1e-12)
+    for a, b in zip(r.step_log, o.step_log):
+        assert a.accepted == b.accepted and a.h == pytest.approx(b.h, rel=1e-9)
+    scale = np.maximum(np.abs(o.final_state), 1e-3)
+    assert np.max(np.abs(r.final_state - o.final_state) / scale) <= 1e-6
+
+
+def _splitmix_uniform(seed, stream, idx):
+    M = np.uint64(0xFFFFFFFFFFFFFFFF)
+    with np.errstate(over="ignore"):
+        s0 = np.uint64(seed) + np.uint64(stream) * np.uint64(0xD1342543DE82EF95)
+        z = s0 + (idx.astype(np.uint64) + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def test_c4_device_k_rows_match_generator(gpu):
+    w = config4_kuramoto()
+    n = w.spec.n_agents
+    for r0 in (0, 16380, n - 8):
+        w.spec.row_begin, w.spec.row_end = r0, r0 + 8
+        part = DeviceSystem(w.spec)
+        idx = np.arange(r0 * n, (r0 + 8) * n, dtype=np.int64)
+        ref = (0.0 + 2.0 * _splitmix_uniform(3, 2, idx)).astype(np.float32).astype(np.float64).reshape(8, n)
+        assert np.array_equal(part.get_k(), ref)
+        part.close()

@@ -1,0 +1,52 @@
+"""C5: batched Kuramoto ensemble (B=1024 x N=2048, shared bf16 K) on the B200.
+Prints one JSON line: trajectory-steps/s of the full lock-step solve, and the
+tensor-core roofline of the tcgen05 contraction (FLOPs / CUDA-event time)."""
+import argparse
+import ctypes as C
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+from paper_2605_23727_b200 import _abi  # noqa: E402
+from paper_2605_23727_b200.batch import DeviceBatch  # noqa: E402
+from paper_2605_23727_b200.configs import config5_batch  # noqa: E402
+from paper_2605_23727_b200.precision import SSS  # noqa: E402
+from paper_2605_23727_b200.systems import DeviceSystem  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--batch", type=int, default=1024)
+ap.add_argument("--n", type=int, default=2048)
+ap.add_argument("--tf", type=float, default=20.0)
+ap.add_argument("--tc", type=int, default=1)
+ap.add_argument("--steps", type=int, default=2)
+a = ap.parse_args()
+w = config5_batch(batch=a.batch, n=a.n, tf=a.tf)
+dev = DeviceSystem(w.spec)
+bat = DeviceBatch(dev, w.omega, tensor_cores=bool(a.tc))
+rhs, prep = C.c_double(), C.c_double()
+x = np.ascontiguousarray(w.x0)
+_abi.check(_abi.lib().ms_batch_profile_rhs(bat._h, _abi.dptr(x), SSS.c(), 20, C.byref(rhs), C.byref(prep)), "prof")
+flops = 2.0 * a.n * a.n * 2 * a.batch
+peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+peak = peaks.get("bf16_tflops", 1590.0)
+bat.solve(w.x0, w.t0, w.tf, w.policy, w.cfg)  # warm-up (graph instantiation)
+res = [bat.solve(w.x0, w.t0, w.tf, w.policy, w.cfg) for _ in range(a.steps)]
+ms = sum(r.device_ms for r in res)
+acc = sum(int(r.n_accepted.sum()) for r in res)
+r0 = res[0]
+line = {
+    "workload": f"C5 batched Kuramoto B={a.batch} N={a.n} K bf16, t in [0,{a.tf}], rtol 1e-6 atol 1e-9",
+    "tensor_cores": bool(a.tc),
+    "value": acc / (ms / 1e3), "unit": "trajectory_accepted_steps/s",
+    "ms_per_solve": ms / a.steps, "lockstep_attempts": r0.attempts,
+    "accepted_per_traj_mean": float(r0.n_accepted.mean()), "rejected_per_traj_mean": float(r0.n_failed.mean()),
+    "completed": int((r0.status == 0).sum()),
+    "contraction": {"kernel": "k_tc_gemm (tcgen05 kind::f16 M128 N256)" if a.tc else "kb_rhs_cc",
+                    "ms": rhs.value, "prep_ms": prep.value, "TFLOPs": flops / (rhs.value * 1e-3) / 1e12,
+                    "peak_bf16_TFLOPs": peak, "frac": flops / (rhs.value * 1e-3) / 1e12 / peak},
+}
+print(json.dumps(line), flush=True)
