@@ -583,6 +583,196 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
 }
 
 // ------------------------------------------------------------------------------
+// rhs_tma: the split-Kuramoto K sweep with K itself streamed by cp.async.bulk.
+// The register-fed sweep above keeps ~64 KB of K in flight per SM, the
+// register file's limit, and tops out near 6.5 TB/s; a plain read probe needs
+// ~4x that in flight to reach ~7.3 TB/s (tools/bw_probe.cu). Here the bytes
+// in flight live in shared memory: one producer warp streams, per stage, the
+// row segments [TC columns] of a 32-row group plus the matching s/c columns
+// into a 3-deep ring (~216 KB); 16 consumer warps own 2 rows each of the
+// group and sum them from shared memory. Lane l handles columns 4l + 128m
+// (8l + 256m for 16-bit K) in ascending order, exactly like k_rhs_fast, so
+// both sweeps produce bit-identical rows.
+#ifndef MS_TMA_LANES
+#define MS_TMA_LANES 1     // 1: the whole producer warp issues the row copies
+#endif
+// per (GS, K storage): rows per consumer warp and K bytes per stage, chosen by
+// tools/tune_rhs.py (profiles/r1_tune_tma.txt); macros override for tuning
+#ifndef MS_TMA_RPW_F32
+#define MS_TMA_RPW_F32 1
+#endif
+#ifndef MS_TMA_KB_F32
+#define MS_TMA_KB_F32 65536
+#endif
+#ifndef MS_TMA_RPW_F64
+#define MS_TMA_RPW_F64 2
+#endif
+#ifndef MS_TMA_KB_F64
+#define MS_TMA_KB_F64 65536
+#endif
+#ifndef MS_TMA_KB_K16
+#define MS_TMA_KB_K16 32768
+#endif
+constexpr int kTmaConsumers = 16;
+constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
+constexpr int kTmaStages = 4;
+
+template <class GS, int KS>
+struct TmaGeom {
+  using KT = typename KElem<KS>::T;
+  static constexpr int RPW = sizeof(GS) == 8 ? MS_TMA_RPW_F64 : MS_TMA_RPW_F32;
+  static constexpr int RG = kTmaConsumers * RPW;  // rows per group
+  static constexpr int KBYTES = sizeof(KT) == 2 ? MS_TMA_KB_K16 : (sizeof(GS) == 8 ? MS_TMA_KB_F64 : MS_TMA_KB_F32);
+  static constexpr int TC = KBYTES / (RG * (int)sizeof(KT));   // columns per tile
+  static constexpr int SC_BYTES = 2 * TC * (int)sizeof(GS);
+  static constexpr int STAGE_BYTES = KBYTES + SC_BYTES;
+  static constexpr int NS = (232448 - 512) / STAGE_BYTES < kTmaStages ? (232448 - 512) / STAGE_BYTES : kTmaStages;
+  static constexpr size_t SMEM = (size_t)NS * STAGE_BYTES + 2 * kTmaStages * sizeof(uint64_t) + 128;
+  static_assert(TC % (32 * KVec<KS>::N) == 0, "tile width must be a whole number of warp steps");
+};
+
+template <class SS, class GS, int KS>
+__global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(RhsArgs a) {
+  if (stage_skip(a.ctl, a.l, a.gate)) return;
+  using G = TmaGeom<GS, KS>;
+  using KT = typename G::KT;
+  constexpr int VEC = KVec<KS>::N;
+  constexpr int COLS_IT = 32 * VEC;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)G::NS * G::STAGE_BYTES);
+  uint64_t* empty = full + G::NS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = a.row1 - a.row0;
+  const int rb = a.row0 + (int)(total * blockIdx.x / gridDim.x);
+  const int re = a.row0 + (int)(total * (blockIdx.x + 1) / gridDim.x);
+  const int ngroups = (re - rb + G::RG - 1) / G::RG;
+  const int ld = (int)a.ld;
+  const int ntiles = (ld + G::TC - 1) / G::TC;
+  const int Q = ngroups * ntiles;
+  const GS* gin = reinterpret_cast<const GS*>(a.gin);
+  const KT* Kbase = reinterpret_cast<const KT*>(a.K);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < G::NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kTmaConsumers) {  // producer warp
+    for (int q = 0; q < Q; ++q) {
+      const int st = q % G::NS;
+      if (q >= G::NS) {
+        if (lane == 0) mbar_wait(&empty[st], ((q / G::NS) & 1) ^ 1);
+        __syncwarp();
+      }
+      const int g = q / ntiles, t = q % ntiles;
+      const int r0 = rb + g * G::RG;
+      const int nr = min(G::RG, re - r0);
+      const int c0 = t * G::TC;
+      const int cc = min(G::TC, ld - c0);
+      const uint32_t kbytes = (uint32_t)(cc * sizeof(KT));
+      const uint32_t sbytes = (uint32_t)(cc * sizeof(GS));
+      unsigned char* sk = smem + (size_t)st * G::STAGE_BYTES;
+      GS* ss = reinterpret_cast<GS*>(sk + G::KBYTES);
+      if (lane == 0) {
+        mbar_expect_tx(&full[st], kbytes * nr + 2 * sbytes);
+        bulk_g2s(ss, gin + c0, sbytes, &full[st]);
+        bulk_g2s(ss + G::TC, gin + (size_t)ld + c0, sbytes, &full[st]);
+      }
+      if (MS_TMA_LANES) {
+        for (int r = lane; r < nr; r += 32)
+          bulk_g2s(sk + (size_t)r * G::TC * sizeof(KT), Kbase + (size_t)(r0 + r - a.row0) * ld + c0, kbytes,
+                   &full[st]);
+      } else if (lane == 0) {
+        for (int r = 0; r < nr; ++r)
+          bulk_g2s(sk + (size_t)r * G::TC * sizeof(KT), Kbase + (size_t)(r0 + r - a.row0) * ld + c0, kbytes,
+                   &full[st]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // consumers: warp w owns rows w and w + 16 of every group
+  const SS mw = cvt<SS>(a.mw);
+  double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
+  bool nonfinite = false;
+  int q = 0;
+  for (int g = 0; g < ngroups; ++g) {
+    const int r0 = rb + g * G::RG;
+    int rows[G::RPW];
+    int nr = 0;
+#pragma unroll
+    for (int k = 0; k < G::RPW; ++k) {
+      const int rl = warp + kTmaConsumers * k;  // local row in the group
+      rows[k] = (r0 + rl < re) ? rl : -1;
+      if (r0 + rl < re) nr = k + 1;
+    }
+    SS A[G::RPW], B[G::RPW];
+#pragma unroll
+    for (int k = 0; k < G::RPW; ++k) { A[k] = SS(0); B[k] = SS(0); }
+    for (int t = 0; t < ntiles; ++t, ++q) {
+      const int st = q % G::NS;
+      const int cc = min(G::TC, ld - t * G::TC);
+      mbar_wait(&full[st], (q / G::NS) & 1);
+      const unsigned char* sk = smem + (size_t)st * G::STAGE_BYTES;
+      const GS* sv = reinterpret_cast<const GS*>(sk + G::KBYTES);
+      const GS* cv = sv + G::TC;
+      if (nr > 0) {
+        for (int col = lane * VEC; col < cc; col += COLS_IT) {
+          GS s_loc[VEC], c_loc[VEC];
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            s_loc[v] = sv[col + v];
+            c_loc[v] = cv[col + v];
+          }
+#pragma unroll
+          for (int k = 0; k < G::RPW; ++k) {
+            if (k < nr) {
+              const uint4 kv = *reinterpret_cast<const uint4*>(sk + ((size_t)rows[k] * G::TC + col) * sizeof(KT));
+              float kf[VEC];
+              KVec<KS>::unpack(kv, kf);
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) {
+                const GS kg = (GS)kf[v];
+                A[k] = add<SS>(A[k], (SS)mul<GS>(kg, s_loc[v]));
+                B[k] = add<SS>(B[k], (SS)mul<GS>(kg, c_loc[v]));
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int k = 0; k < G::RPW; ++k) {
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) {
+        A[k] = add<SS>(A[k], shfl_xor(A[k], m));
+        B[k] = add<SS>(B[k], shfl_xor(B[k], m));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < G::RPW; ++k) {
+      if (lane == k && k < nr) {
+        const int r = r0 + rows[k];
+        const SS si = (SS)gin[r], ci = (SS)gin[ld + r];
+        const SS coup = mul<SS>(mw, sub<SS>(mul<SS>(ci, A[k]), mul<SS>(si, B[k])));
+        const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
+        out[(int64_t)r * a.d + a.cs] = o;
+        nonfinite |= !isfinite(o);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
+}
+
+// ------------------------------------------------------------------------------
 // rhs_faithful: eval_core's exact order (systems.cpp:50-57): per row, ascending
 // j including j = i, acc = acc + mw * (SS)G_ij, G in GS with RN_GS(K_ij).
 template <int MODEL, class SS, class GS, int KS>

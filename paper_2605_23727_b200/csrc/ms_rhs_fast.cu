@@ -1,5 +1,7 @@
 // ms_rhs_fast.cu — instantiation and launch of k_rhs_fast for every
 // (model, SS, GS, K storage) combination a policy row can ask for.
+#include <cstdlib>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
@@ -9,8 +11,39 @@ namespace msb {
 
 namespace {
 
+// K sweep selection for the split Kuramoto: MS_SWEEP=ldg keeps the
+// register-fed sweep, anything else (default) the TMA-fed one
+bool use_tma_sweep() {
+  const char* v = std::getenv("MS_SWEEP");
+  return !(v && std::strcmp(v, "ldg") == 0);
+}
+
+template <class SS, class GS, int KS>
+void go_tma(const RhsLaunch& L, const RhsArgs& a) {
+  auto kern = k_rhs_tma<SS, GS, KS>;
+  constexpr size_t smem = TmaGeom<GS, KS>::SMEM;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tma attribute: ") + cudaGetErrorString(e));
+    attr_done = true;
+  }
+  const int rows = a.row1 - a.row0;
+  const int grid = rows < L.num_sms ? rows : L.num_sms;
+  kern<<<grid, kTmaThreads, smem, L.stream>>>(a);
+}
+
 template <int MODEL, bool SPLIT, class SS, class GS, int KS>
 void go(const RhsLaunch& L, const RhsArgs& a) {
+  // the TMA-fed sweep wins for f32 K (7.2 vs 6.5 TB/s); with 16-bit K its
+  // row copies get small and the s/c traffic per K byte doubles, and the
+  // register-fed sweep stays ahead (profiles/r1_tune_tma.txt)
+  if constexpr (MODEL == MD_KUR && SPLIT && KS == MS_K_F32) {
+    if (use_tma_sweep()) {
+      go_tma<SS, GS, KS>(L, a);
+      return;
+    }
+  }
   auto kern = k_rhs_fast<MODEL, SPLIT, SS, GS, KS>;
   constexpr size_t smem = fast_smem_bytes<GS, SPLIT>();
   static bool attr_done = false;

@@ -151,3 +151,25 @@ def test_row_sharded_rhs_is_bitwise_the_unsharded_rows(gpu):
         part = DeviceSystem(spec)
         got = part.eval_rhs(0.0, x, StagePrecision(B32, B32, B32))
         assert np.array_equal(got[r0:r1], ref[r0:r1])
+
+
+@pytest.mark.parametrize("k_storage", ["f32", "f16", "bf16"])
+@pytest.mark.parametrize("n", [1000, 4096, 8200])
+@pytest.mark.parametrize("sp", [StagePrecision(B32, B32, B32), StagePrecision(B64, B64, B32),
+                                StagePrecision(B64, B64, B64)], ids=str)
+def test_tma_sweep_bitwise_equals_register_sweep(gpu, k_storage, n, sp, monkeypatch):
+    """The TMA-fed K sweep (k_rhs_tma) and the register-fed one (k_rhs_fast)
+    assign columns to lanes identically: rows must agree bit for bit."""
+    spec = kur_spec(n, k_storage, "fast", coupling_k=1.0)
+    dev = DeviceSystem(spec)
+    x = rng_uniform(6, 1, n, 0.0, 50.0)
+    monkeypatch.setenv("MS_SWEEP", "ldg")
+    a = dev.eval_rhs(0.0, x, sp)
+    monkeypatch.setenv("MS_SWEEP", "tma")
+    b = dev.eval_rhs(0.0, x, sp)
+    assert np.array_equal(a, b)
+    # and sharded row ranges of the TMA sweep reproduce the full rows
+    spec.row_begin, spec.row_end = 3, n - 5
+    part = DeviceSystem(spec)
+    c = part.eval_rhs(0.0, x, sp)
+    assert np.array_equal(c[3:n - 5], b[3:n - 5])

@@ -11,16 +11,11 @@ sys.path.insert(0, str(ROOT))
 from paper_2605_23727_b200 import build as B  # noqa: E402
 
 VARIANTS = {
-    "base": {},
-    "r4": {"MS_FAST_R": 4},
-    "t256x2": {"MS_FAST_THREADS": 256, "MS_FAST_MINB": 2},
-    "t1024r4": {"MS_FAST_THREADS": 1024, "MS_FAST_R": 4},
-    "c2048": {"MS_CHUNK": 2048},
-    "c1024": {"MS_CHUNK": 1024},
-    "c4096ns3": {"MS_CHUNK": 4096, "MS_NS": 3},
-    "pfr4": {"MS_PREFETCH": 1, "MS_FAST_R": 4},
-    "pfr6": {"MS_PREFETCH": 1, "MS_FAST_R": 6},
-    "pfr4t256x2": {"MS_PREFETCH": 1, "MS_FAST_R": 4, "MS_FAST_THREADS": 256, "MS_FAST_MINB": 2},
+    "g1": {},
+    "g2": {"MS_TMA_KB_F64": 65536, "MS_TMA_RPW_F64": 2, "MS_TMA_KB_K16": 49152},
+    "g3": {"MS_TMA_KB_F64": 32768, "MS_TMA_KB_K16": 24576},
+    "g4": {"MS_TMA_KB_F32": 49152, "MS_TMA_KB_K16": 65536},
+    "g5": {"MS_TMA_KB_F32": 81920, "MS_TMA_KB_K16": 16384},
 }
 
 
@@ -37,9 +32,9 @@ def main(names=None):
         dflags = [f"-D{k}={v}" for k, v in defs.items()]
         subprocess.run([nvcc, *B._host_cxx(), *B.NVCC_FLAGS, *dflags, "-I", str(ROOT / "include"), "-c",
                         str(B.CSRC / "ms_rhs_fast.cu"), "-o", str(obj)], check=True)
+        others = [str(B.BUILD / (src + ".o")) for src in B.SOURCES if src != "ms_rhs_fast.cu"]
         subprocess.run([nvcc, *B._host_cxx(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(lib),
-                        str(B.BUILD / "ms_api.cu.o"), str(obj), str(B.BUILD / "ms_rhs_faithful.cu.o"), "-lcudadevrt"],
-                       check=True)
+                        *others, str(obj), "-lcudadevrt"], check=True)
         return name
 
     items = [(k, v) for k, v in VARIANTS.items() if not names or k in names]

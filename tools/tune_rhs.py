@@ -17,6 +17,7 @@ from paper_2605_23727_b200.configs import config4_kuramoto
 from paper_2605_23727_b200.precision import SSS, DDS, DDD
 from paper_2605_23727_b200.systems import DeviceSystem
 res = {}
+import os
 for ks in ("f32", "f16"):
     w = config4_kuramoto(n=32768, k_storage=ks)
     dev = DeviceSystem(w.spec)
@@ -38,7 +39,7 @@ def main():
     out = {}
     for lib in sorted(VAR.glob("lib_*.so")):
         name = lib.stem[4:]
-        env = dict(os.environ, MS_LIB_PATH=str(lib))
+        env = dict(os.environ, MS_LIB_PATH=str(lib), MS_SWEEP=os.environ.get("MS_SWEEP", "tma"))
         r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
         line = [l for l in r.stdout.splitlines() if l.startswith("JSON")]
         out[name] = json.loads(line[0][4:]) if line else {"error": r.stderr[-800:]}
