@@ -104,6 +104,26 @@ def bytes_per_eval(n, rows, ks_bytes):
     return rows * n * ks_bytes + n * 2 * 4 + 2 * n * 8 + n * 8
 
 
+def ncu_traffic(kernel_prefix):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel from the committed `ncu --set full` capture (profiles/), or None."""
+    import csv
+    p = ROOT / "profiles" / "r1_k_rhs_tma_f32_raw.csv"
+    if not p.exists():
+        return None
+    rows = list(csv.reader(p.open()))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        if kernel_prefix in r[hdr.index("Kernel Name")]:
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tot = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                i = hdr.index(k)
+                tot += float(r[i].replace(",", "")) * scale.get(units[i], 1)
+            return tot
+    return None
+
+
 def cpu_sample(n, seed, threads, attempts=2, ks="f32"):
     """The oracle on a bounded sample of C4: `attempts` BS3(2) attempts from
     theta0 at the initial step (3 RHS evaluations each), OpenMP over rows."""
@@ -282,8 +302,15 @@ def run_ours(args):
         "accepted_steps_per_solve": results[0].n_accepted, "rejected_per_solve": results[0].n_failed,
         "rhs_evals_per_solve": results[0].flops.rhs_evals,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": f"k_rhs_fast<Kuramoto split, f32, f32, K {args.kdtype}>",
+                     "frac": achieved / peak,
+                     "traffic": (ncu_traffic("k_rhs_tma<float, float, 1>")
+                                 if args.kdtype == "f32" and rows == n and os.environ.get("MS_SWEEP", "tma") != "ldg"
+                                 else None),
+                     "traffic_source": "profiles/r1_k_rhs_tma_f32_raw.csv (ncu --set full, one launch)",
+                     "peak_kind": peak_kind,
+                     "kernel": ("k_rhs_tma<f32, f32, K f32> (cp.async.bulk-fed K sweep)" if args.kdtype == "f32"
+                                and os.environ.get("MS_SWEEP", "tma") != "ldg"
+                                else f"k_rhs_fast<Kuramoto split, f32, f32, K {args.kdtype}>"),
                      "bytes_per_launch": bpe, "launch_ms": rhs_ms.value, "prep_ms": prep_ms.value,
                      "solve_effective_GBps": solve_gbs},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,
