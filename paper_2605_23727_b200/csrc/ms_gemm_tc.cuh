@@ -34,11 +34,21 @@
 
 namespace msb {
 
-constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 64, kTcStages = 4;
+#ifndef MS_TC_STAGES
+#define MS_TC_STAGES 2   // 2 x 48 KB: two CTAs per SM, one's epilogue overlaps the other's MMA
+#endif
+#ifndef MS_TC_EPI_WARPS
+#define MS_TC_EPI_WARPS 8  // 4 or 8 (two warps per TMEM lane quarter, half the columns each)
+#endif
+#ifndef MS_TC_MINB
+#define MS_TC_MINB 2
+#endif
+constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 64, kTcStages = MS_TC_STAGES;
+constexpr int kTcEpiWarps = MS_TC_EPI_WARPS;
 constexpr int kTcABytes = kTcBM * kTcBK * 2;  // 16 KB
 constexpr int kTcBBytes = kTcBN * kTcBK * 2;  // 32 KB
 constexpr int kTcStageBytes = kTcABytes + kTcBBytes;
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr size_t kTcSmem = 1024 /*align slack*/ + (size_t)kTcStages * kTcStageBytes + 256;
 
 struct TcGemm {
@@ -89,7 +99,7 @@ __device__ __forceinline__ uint64_t umma_smem_desc(uint32_t smem_addr) {
   return d;
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreads, MS_TC_MINB)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs t) {
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   // 1024-byte alignment for SWIZZLE_128B tiles
@@ -174,7 +184,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else {  // epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +32
     const int q4 = warp & 3;
-    const int et = threadIdx.x - 64;  // 0..127
+    const int half = (warp - 2) >> 2;  // column half (8 epilogue warps) or 0
+    const int et = threadIdx.x - 64;   // 0 .. 32*kTcEpiWarps-1
     const int tb0 = n0 >> 2;          // first trajectory of this tile
     const BatchDev& d = t.a.d;
     // per-trajectory decisions of this tile, read once (not per element)
@@ -190,7 +201,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_skip[et] = skip;
       tc_out[et] = outp;
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpiWarps) : "memory");
     tc_wait(tmem_full, 0);
     tc_fence_after();
     const int i = m0 + q4 * 32 + lane;
@@ -198,8 +209,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const float mw = (float)d.mw;
     const float* scf = reinterpret_cast<const float*>(d.sc);
     const int64_t bn = (int64_t)d.B * d.n;
+    constexpr int kCols = kTcBN * 4 / kTcEpiWarps;  // columns per epilogue warp
 #pragma unroll 1
-    for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+    for (int c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 32) {
       uint32_t r[32];
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"

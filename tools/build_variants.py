@@ -10,12 +10,13 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 from paper_2605_23727_b200 import build as B  # noqa: E402
 
+# name -> (translation unit to rebuild, -D overrides)
 VARIANTS = {
-    "g1": {},
-    "g2": {"MS_TMA_KB_F64": 65536, "MS_TMA_RPW_F64": 2, "MS_TMA_KB_K16": 49152},
-    "g3": {"MS_TMA_KB_F64": 32768, "MS_TMA_KB_K16": 24576},
-    "g4": {"MS_TMA_KB_F32": 49152, "MS_TMA_KB_K16": 65536},
-    "g5": {"MS_TMA_KB_F32": 81920, "MS_TMA_KB_K16": 16384},
+    "tc_base": ("ms_batch.cu", {}),
+    "tc_s2x2": ("ms_batch.cu", {"MS_TC_STAGES": 2, "MS_TC_MINB": 2}),
+    "tc_e8": ("ms_batch.cu", {"MS_TC_EPI_WARPS": 8}),
+    "tc_s2x2_e8": ("ms_batch.cu", {"MS_TC_STAGES": 2, "MS_TC_MINB": 2, "MS_TC_EPI_WARPS": 8}),
+    "tc_s3_e8": ("ms_batch.cu", {"MS_TC_STAGES": 3, "MS_TC_EPI_WARPS": 8}),
 }
 
 
@@ -26,13 +27,13 @@ def main(names=None):
     nvcc = B._nvcc()
 
     def one(item):
-        name, defs = item
-        obj = out / f"rhs_fast_{name}.o"
+        name, (tu, defs) = item
+        obj = out / f"{tu}_{name}.o"
         lib = out / f"lib_{name}.so"
         dflags = [f"-D{k}={v}" for k, v in defs.items()]
         subprocess.run([nvcc, *B._host_cxx(), *B.NVCC_FLAGS, *dflags, "-I", str(ROOT / "include"), "-c",
-                        str(B.CSRC / "ms_rhs_fast.cu"), "-o", str(obj)], check=True)
-        others = [str(B.BUILD / (src + ".o")) for src in B.SOURCES if src != "ms_rhs_fast.cu"]
+                        str(B.CSRC / tu), "-o", str(obj)], check=True)
+        others = [str(B.BUILD / (src + ".o")) for src in B.SOURCES if src != tu]
         subprocess.run([nvcc, *B._host_cxx(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(lib),
                         *others, str(obj), "-lcudadevrt"], check=True)
         return name
