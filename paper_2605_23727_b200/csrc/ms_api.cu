@@ -320,7 +320,8 @@ void ensure_workspace(ms_system* s, int64_t log_cap) {
       if (kv.second.g) cudaGraphDestroy(kv.second.g);
     }
     s->graphs.clear();
-    cudaFree(s->ws_mem);
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaFree(s->ws_mem));
     s->ws_ready = false;
   }
   const int64_t dn = s->dn();
@@ -340,7 +341,9 @@ void ensure_workspace(ms_system* s, int64_t log_cap) {
   total += al(sizeof(Ctl));
   char* base = nullptr;
   CK(cudaMalloc(&base, total));
-  CK(cudaMemset(base, 0, total));
+  // zero on the system's own (non-blocking) stream: a legacy-stream memset
+  // is not ordered before kernels on s->stream and can land after them
+  CK(cudaMemsetAsync(base, 0, total, s->stream));
   s->ws_mem = base;
   char* p = base;
   auto take = [&](size_t b) {

@@ -333,6 +333,7 @@ void beval(ms_batch* m, cudaStream_t st, const BEval& e, const ms_stage_prec& sp
   a.gate = e.gate;
   a.out_slot = e.out_slot;
   a.ws32 = p.ws32;
+  a.fs32 = p.fs32;
   if (mid0) BCK(cudaEventRecord(mid0, st));
   if (use_tc) {
     launch_tc_gemm(m->gemm, a, st);
@@ -538,6 +539,9 @@ int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t
     BCK(cudaMallocHost(&m->ctl_host, sizeof(Ctl) * batch));
     BCK(cudaMallocHost(&m->flag_host, sizeof(int)));
     if (m->tc) tc_gemm_setup(m->gemm, d, v.sms);
+    // the zeroing and omega upload ran on the legacy stream; m->st is
+    // non-blocking, so finish them before any kernel of the batch can start
+    BCK(cudaDeviceSynchronize());
     *out = m.release();
   });
 }

@@ -104,7 +104,6 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
       d.xb[ix ^ 1][e] = v;
     }
   }
-  d.fvc[e] = (double)cvt<FS>(d.omega[e]);
   const GS xg = cvt<GS>(v);
   const GS sv = dsin<GS>(xg), cv = dcos<GS>(xg);
   GS* sc = reinterpret_cast<GS*>(d.sc);
@@ -133,8 +132,14 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
 
 struct BRhsArgs {
   BatchDev d;
-  int S, l, gate, out_slot, ws32;
+  int S, l, gate, out_slot, ws32, fs32;
 };
+
+// F of the Kuramoto agent in FS (systems.cpp:136-139): RN_FS(omega), exact in binary64
+__device__ __forceinline__ double b_fval(const BatchDev& d, int64_t e, int fs32) {
+  const double w = d.omega[e];
+  return fs32 ? (double)__double2float_rn(w) : w;
+}
 
 // coupling epilogue of one (row i, trajectory b): k = (double)(RN_WS(omega) +
 // RN_WS(mw (c_i A - s_i B))), SS arithmetic
@@ -147,7 +152,7 @@ __device__ __forceinline__ void b_epilogue(const BRhsArgs& a, int i, int b, SS A
   const GS* sc = reinterpret_cast<const GS*>(d.sc);
   const SS si = (SS)sc[e], ci = (SS)sc[(int64_t)d.B * d.n + e];
   const SS coup = mul<SS>(cvt<SS>(d.mw), sub<SS>(mul<SS>(ci, A), mul<SS>(si, Bv)));
-  const double o = ws_add(d.fvc[e], (double)coup, a.ws32);
+  const double o = ws_add(b_fval(d, e, a.fs32), (double)coup, a.ws32);
   bslot(d, a.S, a.out_slot, c)[i + (int64_t)b * d.n] = o;
   if (!isfinite(o)) atomicOr(&c->nf_mask, 1 << a.l);
 }

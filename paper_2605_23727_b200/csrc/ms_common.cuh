@@ -38,6 +38,11 @@ template <> __device__ __forceinline__ double dsin<double>(double x) { return si
 template <class S> __device__ __forceinline__ S dcos(S x);
 template <> __device__ __forceinline__ float dcos<float>(float x) { return cr_cosf(x); }
 template <> __device__ __forceinline__ double dcos<double>(double x) { return cos(x); }
+// fast-path arctangent: CUDA's own atanf (<= 2 ulp) in binary32 — the fast
+// sweep is held to tolerance parity, only the faithful sweep needs cr_atanf
+template <class S> __device__ __forceinline__ S fatan(S x);
+template <> __device__ __forceinline__ float fatan<float>(float x) { return atanf(x); }
+template <> __device__ __forceinline__ double fatan<double>(double x) { return atan(x); }
 template <class S> __device__ __forceinline__ S datan(S x);
 template <> __device__ __forceinline__ float datan<float>(float x) { return cr_atanf(x); }
 template <> __device__ __forceinline__ double datan<double>(double x) { return atan(x); }

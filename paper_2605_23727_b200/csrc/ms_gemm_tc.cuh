@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kTcThreads, MS_TC_MINB)
           const int64_t e = (int64_t)b * d.n + i;
           sv[q] = scf[e];
           cv[q] = scf[bn + e];
-          fv[q] = d.fvc[e];
+          fv[q] = b_fval(d, e, t.a.fs32);
         }
       }
 #pragma unroll

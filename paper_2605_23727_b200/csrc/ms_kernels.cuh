@@ -381,7 +381,7 @@ __device__ __forceinline__ void sweep_step(const uint4 (&kv)[R], int nr, const G
         } else {
           GS g;
           if (MODEL == MD_LCO) g = mul<GS>(kg, sub<GS>(s_loc[v], xi[k]));
-          else g = mul<GS>(pref[k], mul<GS>(kg, datan<GS>(sub<GS>(s_loc[v], xi[k]))));
+          else g = mul<GS>(pref[k], mul<GS>(kg, fatan<GS>(sub<GS>(s_loc[v], xi[k]))));
           A[k] = add<SS>(A[k], (SS)g);
         }
       }
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
                 } else if (c0 + col + v < a.n) {
                   GS g;
                   if (MODEL == MD_LCO) g = mul<GS>(kscal, sub<GS>(s_loc[v], xi[k]));
-                  else g = mul<GS>(pref[k], mul<GS>(kscal, datan<GS>(sub<GS>(s_loc[v], xi[k]))));
+                  else g = mul<GS>(pref[k], mul<GS>(kscal, fatan<GS>(sub<GS>(s_loc[v], xi[k]))));
                   A[k] = add<SS>(A[k], (SS)g);
                 }
               }

