@@ -303,6 +303,7 @@ def run_ours(args):
         "rhs_evals_per_solve": results[0].flops.rhs_evals,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
+                     "frac_nominal_8TBps": achieved / 8000.0,  # both denominators
                      "traffic": (ncu_traffic("k_rhs_tma<float, float, 1>")
                                  if args.kdtype == "f32" and rows == n and os.environ.get("MS_SWEEP", "tma") != "ldg"
                                  else None),

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define MS_ABI_VERSION 1
+#define MS_ABI_VERSION 2
 
 /* ---- return codes ---------------------------------------------------- */
 #define MS_OK 0
@@ -125,7 +125,7 @@ typedef struct {
   double fac_min;
   double fac_max;
   double controller_exponent;
-  int32_t record_snapshots; /* not supported on the device: must be 0 */
+  int32_t record_snapshots; /* StepSnapshot per accepted step (solver.cpp:324-327), see ms_solve_result */
   int32_t _pad;
 } ms_solver_config;
 
@@ -182,6 +182,15 @@ typedef struct {
   int64_t step_log_capacity; /* in */
   int64_t step_log_count;    /* out: records produced (may exceed capacity) */
   double device_ms;          /* out: device time of the adaptive loop (CUDA events) */
+  /* StepSnapshot (solver.hpp:96-100) when cfg->record_snapshots: host buffer of
+   * (snapshot_capacity + 1) x dN doubles. Row 0 is the loop's starting state
+   * (x0, rounded to binary32 under binary32 storage, solver.cpp:263); row k+1
+   * is the state after accepted step k, so snapshot k = (row k, row k+1,
+   * snapshot_h[k]). NULL = not recorded. */
+  double* snapshots;
+  double* snapshot_h;          /* [snapshot_capacity] step sizes */
+  int64_t snapshot_capacity;   /* in */
+  int64_t snapshot_count;      /* out: accepted steps (may exceed capacity) */
 } ms_solve_result;
 
 /* StepOutcome, solver.hpp:75-86 (vectors are caller buffers of length dN) */

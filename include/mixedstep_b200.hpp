@@ -11,6 +11,8 @@
 // std::runtime_error (MS_ECUDA); numerical failure is SolveResult::status.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -110,12 +112,14 @@ struct SolverConfig {  // solver.hpp:39-61
 
 struct StepRecord { double t, h, err; bool accepted; };
 struct FlopTally { std::int64_t low = 0, high = 0, rhs_evals = 0; };
+struct StepSnapshot { Vector x_before, x_after; double h; };  // solver.hpp:96-100
 struct SolveResult {
   SolveStatus status = SolveStatus::Completed;
   Vector final_state;
   double t_reached = 0.0;
   std::int64_t n_accepted = 0, n_failed = 0;
   std::vector<StepRecord> step_log;
+  std::vector<StepSnapshot> snapshots;
   FlopTally flops;
   double device_ms = 0.0;
   std::int64_t total_steps() const { return n_accepted + n_failed; }
@@ -213,6 +217,18 @@ SolveResult run(F&& call, std::size_t dn, const SolverConfig& cfg) {
   r.final_state = out.final_state.data();
   r.step_log = log.empty() ? nullptr : log.data();
   r.step_log_capacity = static_cast<int64_t>(log.size());
+  // snapshots: as many accepted steps as 256 MiB of rows hold
+  std::int64_t scap = 0;
+  if (cfg.record_snapshots) {
+    const std::int64_t fit = static_cast<std::int64_t>((std::size_t(256) << 20) / (8 * (dn ? dn : 1))) - 1;
+    scap = std::max<std::int64_t>(1, std::min<std::int64_t>(cfg.max_iterations, fit));
+  }
+  std::vector<double> rows(scap ? static_cast<std::size_t>(scap + 1) * dn : 0), hs(static_cast<std::size_t>(scap));
+  if (scap) {
+    r.snapshots = rows.data();
+    r.snapshot_h = hs.data();
+    r.snapshot_capacity = scap;
+  }
   call(r);
   out.status = static_cast<SolveStatus>(r.status);
   out.t_reached = r.t_reached;
@@ -223,6 +239,11 @@ SolveResult run(F&& call, std::size_t dn, const SolverConfig& cfg) {
   const int64_t m = r.step_log_count < r.step_log_capacity ? r.step_log_count : r.step_log_capacity;
   for (int64_t i = 0; i < m; ++i)
     out.step_log.push_back({log[i].t, log[i].h, log[i].err, log[i].accepted != 0});
+  const int64_t ns = std::min<int64_t>(scap, r.snapshot_count);
+  for (int64_t k = 0; k < ns; ++k) {
+    const double* b = rows.data() + static_cast<std::size_t>(k) * dn;
+    out.snapshots.push_back({Vector(b, b + dn), Vector(b + dn, b + 2 * dn), hs[static_cast<std::size_t>(k)]});
+  }
   return out;
 }
 }  // namespace detail
@@ -242,6 +263,82 @@ inline SolveResult dp54_reference(const System& sys, const Vector& x0, double t0
   return detail::run([&](ms_solve_result& r) {
     check(ms_dp54_reference(sys.handle(), x0.data(), t0, t_final, &c, &r), "dp54_reference");
   }, x0.size(), cfg);
+}
+
+// ---- host metrics over device results (metrics.hpp / metrics.cpp) ------------
+
+// Analytic propagator of the reference LCO at time t (systems.cpp:270-306):
+// the agent mean rotates, deviations decay through exp(tA), A = [[-1,1],[-1,0]].
+inline Vector lco_analytic(const Vector& x0, double t) {
+  if (x0.size() % 2 != 0) throw std::invalid_argument("lco_analytic: state length must be 2N");
+  const std::size_t n = x0.size() / 2;
+  double xm0 = 0.0, vm0 = 0.0;
+  for (std::size_t i = 0; i < n; ++i) {
+    xm0 += x0[2 * i];
+    vm0 += x0[2 * i + 1];
+  }
+  xm0 /= static_cast<double>(n);
+  vm0 /= static_cast<double>(n);
+  const double ct = std::cos(t), st = std::sin(t);
+  const double xm = xm0 * ct + vm0 * st, vm = -xm0 * st + vm0 * ct;
+  const double w = std::sqrt(3.0) / 2.0, decay = std::exp(-0.5 * t);
+  const double cw = std::cos(w * t), sw = std::sin(w * t) / w;
+  const double p00 = decay * (cw - 0.5 * sw), p01 = decay * sw, p10 = decay * -sw, p11 = decay * (cw + 0.5 * sw);
+  Vector out(x0.size());
+  for (std::size_t i = 0; i < n; ++i) {
+    const double du = x0[2 * i] - xm0, dv = x0[2 * i + 1] - vm0;
+    out[2 * i] = xm + p00 * du + p01 * dv;
+    out[2 * i + 1] = vm + p10 * du + p11 * dv;
+  }
+  return out;
+}
+
+// ||x_ref - x||_2 / sqrt(N) (metrics.cpp:10-17), squares summed in index order
+inline double normalized_final_error(const Vector& x_ref, const Vector& x, std::int64_t n_agents) {
+  if (x_ref.size() != x.size()) throw std::invalid_argument("normalized_final_error: length mismatch");
+  if (n_agents < 1) throw std::invalid_argument("normalized_final_error: N must be >= 1");
+  double s = 0.0;
+  for (std::size_t k = 0; k < x.size(); ++k) s += (x_ref[k] - x[k]) * (x_ref[k] - x[k]);
+  return std::sqrt(s) / std::sqrt(static_cast<double>(n_agents));
+}
+
+// one-step error against the analytic LCO propagator re-anchored at x_n (metrics.cpp:42-52)
+inline double real_local_error(const Vector& x_n, const Vector& x_next, double h_n, double ab, double rel) {
+  const Vector x_ex = lco_analytic(x_n, h_n);
+  const double delta = ab / rel;
+  double err = 0.0;
+  for (std::size_t k = 0; k < x_next.size(); ++k)
+    err = std::max(err, std::abs(x_next[k] - x_ex[k]) / std::max(std::abs(x_ex[k]), delta));
+  return err;
+}
+
+struct ErrorReport {  // metrics.hpp:31-35
+  double normalized_final_error = 0.0;
+  double mean_e_bs = 0.0;
+  bool has_mean_e_analytic = false;
+  double mean_e_analytic = 0.0;
+};
+
+// metrics.cpp:19-40
+inline ErrorReport error_report(const SolveResult& run, const Vector& x_ref_final, std::int64_t n_agents, double ab,
+                                double rel) {
+  ErrorReport er;
+  er.normalized_final_error = normalized_final_error(x_ref_final, run.final_state, n_agents);
+  double sum = 0.0;
+  std::int64_t n = 0;
+  for (const StepRecord& r : run.step_log)
+    if (r.accepted) {
+      sum += r.err;
+      ++n;
+    }
+  er.mean_e_bs = n > 0 ? sum / static_cast<double>(n) : 0.0;
+  if (!run.snapshots.empty()) {
+    double a = 0.0;
+    for (const StepSnapshot& q : run.snapshots) a += real_local_error(q.x_before, q.x_after, q.h, ab, rel);
+    er.has_mean_e_analytic = true;
+    er.mean_e_analytic = a / static_cast<double>(run.snapshots.size());
+  }
+  return er;
 }
 
 }  // namespace mixedstep_b200

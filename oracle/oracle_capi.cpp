@@ -116,6 +116,19 @@ void fill_result(const SolveResult& r, int dn, ms_solve_result* out) {
     }
   }
   out->device_ms = 0.0;
+  // StepSnapshots in the C-ABI layout: row 0 = x_before of the first, row k+1
+  // = x_after of snapshot k (consecutive snapshots chain, solver.cpp:324-327)
+  out->snapshot_count = static_cast<int64_t>(r.snapshots.size());
+  if (out->snapshots && out->snapshot_h && !r.snapshots.empty()) {
+    const int64_t m = std::min<int64_t>(out->snapshot_capacity, out->snapshot_count);
+    const size_t row = static_cast<size_t>(dn);
+    std::memcpy(out->snapshots, r.snapshots[0].x_before.data(), sizeof(double) * row);
+    for (int64_t k = 0; k < m; ++k) {
+      const StepSnapshot& q = r.snapshots[static_cast<size_t>(k)];
+      std::memcpy(out->snapshots + (size_t)(k + 1) * row, q.x_after.data(), sizeof(double) * row);
+      out->snapshot_h[k] = q.h;
+    }
+  }
 }
 
 }  // namespace

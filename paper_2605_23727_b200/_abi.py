@@ -75,6 +75,7 @@ class SolveResultC(C.Structure):
         ("flops_low", C.c_int64), ("flops_high", C.c_int64),
         ("final_state", _DP), ("step_log", C.POINTER(StepRecordC)),
         ("step_log_capacity", C.c_int64), ("step_log_count", C.c_int64), ("device_ms", C.c_double),
+        ("snapshots", _DP), ("snapshot_h", _DP), ("snapshot_capacity", C.c_int64), ("snapshot_count", C.c_int64),
     ]
 
 
@@ -156,6 +157,9 @@ class CudaError(MixedstepError):
 _lib = None
 
 
+ABI_VERSION = 2  # MS_ABI_VERSION of include/mixedstep_b200.h
+
+
 def lib() -> C.CDLL:
     """Load the in-tree sm_100a library; raises if it has not been built."""
     global _lib
@@ -169,6 +173,8 @@ def lib() -> C.CDLL:
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if L.ms_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH}: ABI version {L.ms_abi_version()} != {ABI_VERSION}: rebuild it")
         _lib = L
     return _lib
 

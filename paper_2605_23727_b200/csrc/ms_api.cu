@@ -289,6 +289,10 @@ struct ms_system {
   };
   std::map<std::string, GraphEntry> graphs;
   std::mutex mu;
+  // StepSnapshot buffer: (snap_cap + 1) rows of dN, then snap_cap step sizes
+  double* snap = nullptr;
+  double* snap_h = nullptr;
+  int64_t snap_cap = -1;
   // host-driven (sharded) loop
   bool loop_active = false;
   SolvePlanStore* loop_plan = nullptr;
@@ -491,7 +495,31 @@ struct SolvePlan {
   int storage;
   int lowest;
   bool k1_elided;
+  bool snaps;  // record StepSnapshots (k_snapshot after each finalize)
 };
+
+int snap_grid(const ms_system* s) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((s->dn() + 255) / 256, 2 * s->sms));
+}
+
+// snapshot rows for `cap` accepted steps; the loop graphs capture the buffer
+// address, so growing it drops them
+void ensure_snapshots(ms_system* s, int64_t cap) {
+  if (cap <= s->snap_cap) return;
+  CK(cudaStreamSynchronize(s->stream));
+  for (auto& kv : s->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.g) cudaGraphDestroy(kv.second.g);
+  }
+  s->graphs.clear();
+  if (s->snap) CK(cudaFree(s->snap));
+  s->snap = nullptr;
+  s->snap_cap = -1;
+  const size_t bytes = sizeof(double) * ((size_t)(cap + 1) * (size_t)s->dn() + (size_t)cap);
+  CK(cudaMalloc(&s->snap, bytes));
+  s->snap_h = s->snap + (size_t)(cap + 1) * (size_t)s->dn();
+  s->snap_cap = cap;
+}
 
 // one attempt: [k1 recompute] -> stages -> finalize
 void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_handle,
@@ -513,6 +541,10 @@ void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_
   f.handle = h;
   k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
   CK(cudaGetLastError());
+  if (P.snaps) {
+    k_snapshot<<<snap_grid(s), 256, 0, st>>>(s->B, s->snap, s->snap_h, s->snap_cap, s->dn(), 0);
+    CK(cudaGetLastError());
+  }
 }
 
 // initial_step + cold k1 + loop head (solver.cpp:247-269)
@@ -558,7 +590,6 @@ void validate_cfg(const ms_solver_config& c, double t0, double tf) {  // solver.
     throw InvalidArg("solver: need 0 < abs_tol <= rel_tol < 1");
   if (!(c.fac_min < 1.0 && c.fac_max > 1.0)) throw InvalidArg("solver: need fac_min < 1 < fac_max");
   if (!(tf > t0)) throw InvalidArg("solver: need t_final > t0");
-  if (c.record_snapshots) throw InvalidArg("solver: record_snapshots is not supported on the device");
 }
 
 void init_ctl(ms_system* s, Ctl& c, const ms_solver_config& cfg, double t0, double tf, const SolvePlan& P,
@@ -583,13 +614,15 @@ void init_ctl(ms_system* s, Ctl& c, const ms_solver_config& cfg, double t0, doub
   c.store32 = P.storage == MS_BINARY32 ? 1 : 0;
   c.time_limits = cfg.time_limits_enabled ? 1 : 0;
   c.record_log = cfg.record_step_log ? 1 : 0;
+  c.snap_on = P.snaps ? 1 : 0;
   c.status = MS_COMPLETED;
   (void)s;
 }
 
 std::string plan_key(const SolvePlan& P) {
   char buf[160];
-  int o = std::snprintf(buf, sizeof(buf), "S%d:st%d:el%d:k1%d%d%d", P.T->S, P.storage, (int)P.k1_elided,
+  int o = std::snprintf(buf, sizeof(buf), "S%d:st%d:el%d:sn%d:k1%d%d%d", P.T->S, P.storage, (int)P.k1_elided,
+                        (int)P.snaps,
                         P.k1_row.f_prec, P.k1_row.sum_prec, P.k1_row.g_prec);
   for (int l = 0; l < P.T->S - 1; ++l)
     o += std::snprintf(buf + o, sizeof(buf) - o, ":%d%d%d", P.rows[l].f_prec, P.rows[l].sum_prec, P.rows[l].g_prec);
@@ -651,13 +684,16 @@ void tally(ms_system* s, const Ctl& c, const SolvePlan& P, int64_t out[3]) {
   out[2] = high;
 }
 
-void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf, const SolvePlan& P,
+void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf, const SolvePlan& P0,
                const ms_solver_config& cfg, ms_solve_result* res, cudaStream_t user_stream, bool out_dev) {
   validate_cfg(cfg, t0, tf);
   std::lock_guard<std::mutex> lk(s->mu);
   set_device(s);
   const int64_t cap = (cfg.record_step_log && res->step_log) ? std::max<int64_t>(res->step_log_capacity, 1) : 1;
   ensure_workspace(s, cap);
+  SolvePlan P = P0;
+  P.snaps = cfg.record_snapshots && res->snapshots && res->snapshot_h && res->snapshot_capacity >= 0;
+  if (P.snaps) ensure_snapshots(s, std::max<int64_t>(res->snapshot_capacity, 1));
   cudaStream_t st = s->stream;
   if (user_stream && user_stream != st) {
     // order the solve after the caller's prior work on its stream
@@ -677,6 +713,10 @@ void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf
   cudaGraphExec_t exec = host_loop ? nullptr : get_loop_graph(s, P);
   CK(cudaEventRecord(s->ev0, st));
   launch_init(s, st, P, true);
+  if (P.snaps) {
+    k_snapshot<<<snap_grid(s), 256, 0, st>>>(s->B, s->snap, s->snap_h, s->snap_cap, dn, 1);
+    CK(cudaGetLastError());
+  }
   if (host_loop) {
     for (;;) {
       launch_attempt(s, st, P, false, 0);
@@ -710,6 +750,15 @@ void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf
         res->step_log[i].accepted = tmp[(size_t)i].accepted;
       }
     }
+  }
+  res->snapshot_count = P.snaps ? c.n_acc : 0;
+  if (P.snaps) {
+    const int64_t m = std::min<int64_t>(res->snapshot_capacity, c.n_acc);
+    CK(cudaMemcpyAsync(res->snapshots, s->snap, sizeof(double) * (size_t)(m + 1) * (size_t)dn,
+                       out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (m > 0)
+      CK(cudaMemcpyAsync(res->snapshot_h, s->snap_h, sizeof(double) * (size_t)m,
+                         out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   }
   CK(cudaStreamSynchronize(st));
   if (user_stream && user_stream != st) {
@@ -1123,6 +1172,7 @@ int ms_system_destroy(ms_system_t s) {
     for (void* p : s->dev_arrays) cudaFree(p);
     if (s->K) cudaFree(s->K);
     if (s->ws_mem) cudaFree(s->ws_mem);
+    if (s->snap) cudaFree(s->snap);
     if (s->ctl_host) cudaFreeHost(s->ctl_host);
     delete s->loop_plan;
     if (s->ev0) cudaEventDestroy(s->ev0);

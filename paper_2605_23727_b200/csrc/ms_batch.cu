@@ -65,8 +65,11 @@ struct BFinArgs {
   int bslot_[kMaxStages];
 };
 
-// x_tilde, weighted max-norm and the controller of one trajectory per CTA
-__global__ void __launch_bounds__(256) kb_finalize(BFinArgs f) {
+// x_tilde, weighted max-norm and the controller of one trajectory per CTA;
+// the last CTA to finish (ticket) also evaluates the loop condition, so an
+// attempt ends without a separate condition kernel
+constexpr int kBFinThreads = 256;
+__global__ void __launch_bounds__(kBFinThreads) kb_finalize(BFinArgs f, int has_handle, cudaGraphConditionalHandle h) {
   const int b = blockIdx.x;
   const BatchDev& d = f.d;
   Ctl* c = d.ctl + b;
@@ -77,50 +80,62 @@ __global__ void __launch_bounds__(256) kb_finalize(BFinArgs f) {
   if (!dead && !stage_nf) {
     const int ix = c->ix;
     const int64_t o = (int64_t)b * d.n;
-    const double* x = d.xb[ix] + o;
-    const double* xst = d.xb[ix ^ 1] + o;
-    const double* xnx = c->store32 ? d.xn + o : xst;
+    const double* __restrict__ x = d.xb[ix] + o;
+    const double* __restrict__ xst = d.xb[ix ^ 1] + o;
+    const double* __restrict__ xnx = c->store32 ? d.xn + o : xst;
+    // the four BS3(2) error weights b~ (all nonzero, bplan checks nbt == 4)
+    const double* __restrict__ k0 = bslot(d, f.S, f.bslot_[0], c) + o;
+    const double* __restrict__ k1 = bslot(d, f.S, f.bslot_[1], c) + o;
+    const double* __restrict__ k2 = bslot(d, f.S, f.bslot_[2], c) + o;
+    const double* __restrict__ k3 = bslot(d, f.S, f.bslot_[3], c) + o;
+    const double b0 = f.bt[0], b1 = f.bt[1], b2 = f.bt[2], b3 = f.bt[3];
     const double h = c->h_att;
     const double floor_w = __ddiv_rn(c->abs_tol, c->rel_tol);
-    for (int i = threadIdx.x; i < d.n; i += blockDim.x) {
-      double comb = __dmul_rn(f.bt[0], bslot(d, f.S, f.bslot_[0], c)[o + i]);
-      for (int t = 1; t < f.nbt; ++t) comb = __dadd_rn(comb, __dmul_rn(f.bt[t], bslot(d, f.S, f.bslot_[t], c)[o + i]));
-      const double xt = __dadd_rn(x[i], __dmul_rn(h, comb));
+#pragma unroll 4
+    for (int i = threadIdx.x; i < d.n; i += kBFinThreads) {
+      double comb = __dmul_rn(b0, k0[i]);
+      comb = __dadd_rn(comb, __dmul_rn(b1, k1[i]));
+      comb = __dadd_rn(comb, __dmul_rn(b2, k2[i]));
+      comb = __dadd_rn(comb, __dmul_rn(b3, k3[i]));
+      const double xi = x[i];
+      const double xt = __dadd_rn(xi, __dmul_rn(h, comb));
       const double xn = xnx[i];
       nf |= !isfinite(xn) || !isfinite(xt) || !isfinite(xst[i]);
-      const double w = fmax(fmax(fabs(x[i]), fabs(xn)), floor_w);
+      const double w = fmax(fmax(fabs(xi), fabs(xn)), floor_w);
       m = fmax(m, __ddiv_rn(fabs(__dsub_rn(xn, xt)), w));
     }
   }
-  __shared__ double red[8];
-  __shared__ int rnf[8];
-  for (int s = 16; s >= 1; s >>= 1) {
-    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
-  }
+  __shared__ double red[kBFinThreads / 32];
+  __shared__ int rnf[kBFinThreads / 32];
+  __shared__ int last;
+  for (int s = 16; s >= 1; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
   nf = __any_sync(0xffffffffu, nf);
   if ((threadIdx.x & 31) == 0) {
     red[threadIdx.x >> 5] = m;
     rnf[threadIdx.x >> 5] = nf;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  double e = 0.0;
-  int anynf = 0;
-  for (int w = 0; w < 8; ++w) {
-    e = fmax(e, red[w]);
-    anynf |= rnf[w];
+  if (threadIdx.x == 0) {
+    double e = 0.0;
+    int anynf = 0;
+    for (int w = 0; w < kBFinThreads / 32; ++w) {
+      e = fmax(e, red[w]);
+      anynf |= rnf[w];
+    }
+    attempt_controller(c, f.S, FIN_SOLVE, f.k1_elided, 0, dead, stage_nf, anynf != 0, e, nullptr);
+    __threadfence();
+    last = atomicAdd(d.ticket, 1u) == gridDim.x - 1;
   }
-  attempt_controller(c, f.S, FIN_SOLVE, f.k1_elided, 0, dead, stage_nf, anynf != 0, e, nullptr);
-}
-
-// loop condition: does any trajectory still run?
-__global__ void __launch_bounds__(1024) kb_cond(const Ctl* ctl, int B, int* flag, int has_handle,
-                                                cudaGraphConditionalHandle h) {
+  __syncthreads();
+  if (!last) return;
+  // loop condition: does any trajectory still run?
+  __threadfence();
   int any = 0;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) any |= ctl[b].done == 0;
+  for (int q = threadIdx.x; q < d.B; q += kBFinThreads) any |= reinterpret_cast<volatile const Ctl*>(d.ctl + q)->done == 0;
   any = __syncthreads_or(any);
   if (threadIdx.x == 0) {
-    *flag = any;
+    *d.flag = any;
+    *d.ticket = 0u;
     if (has_handle) cudaGraphSetConditional(h, any ? 1 : 0);
   }
 }
@@ -404,9 +419,8 @@ void battempt(ms_batch* m, cudaStream_t st, const BPlan& P, bool has_handle, cud
     f.bslot_[f.nbt] = mm == 0 ? SLOT_K1 : (mm == 3 ? SLOT_KLAST : mm);
     ++f.nbt;
   }
-  kb_finalize<<<m->B, 256, 0, st>>>(f);
-  BCK(cudaGetLastError());
-  kb_cond<<<1, 1024, 0, st>>>(m->d.ctl, m->B, m->d.flag, has_handle ? 1 : 0, h);
+  if (f.nbt != 4) throw InvalidArg("batch: finalize expects the four BS3(2) error weights");
+  kb_finalize<<<m->B, kBFinThreads, 0, st>>>(f, has_handle ? 1 : 0, h);
   BCK(cudaGetLastError());
 }
 
@@ -530,7 +544,8 @@ int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t
     d.op = take(sizeof(uint16_t) * 4 * (size_t)batch * ld);
     d.fvc = reinterpret_cast<double*>(take(sizeof(double) * bn));
     d.ctl = reinterpret_cast<Ctl*>(take(sizeof(Ctl) * batch));
-    d.flag = reinterpret_cast<int*>(take(sizeof(int)));
+    d.flag = reinterpret_cast<int*>(take(2 * sizeof(int)));
+    d.ticket = reinterpret_cast<unsigned*>(d.flag + 1);
     d.mw = 1.0 / n;
     BCK(cudaMemcpy(m->omega, omega, sizeof(double) * bn, cudaMemcpyHostToDevice));
     BCK(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
@@ -632,6 +647,7 @@ int ms_batch_solve(ms_batch_t m, const double* x0, double t0, double tf, const m
       throw InvalidArg("solver: need 0 < abs_tol <= rel_tol < 1");
     if (!(cfg->fac_min < 1.0 && cfg->fac_max > 1.0)) throw InvalidArg("solver: need fac_min < 1 < fac_max");
     if (!(tf > t0)) throw InvalidArg("solver: need t_final > t0");
+    if (cfg->record_snapshots) throw InvalidArg("batch_solve: snapshots are recorded by ms_solve only");
     std::lock_guard<std::mutex> lk(m->mu);
     BCK(cudaSetDevice(m->sv.dev));
     const BPlan P = bplan(*pol);

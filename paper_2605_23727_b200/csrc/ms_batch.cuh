@@ -30,6 +30,7 @@ struct BatchDev {
   double* fvc;                    // F (omega in FS) [B][n]
   Ctl* ctl;                       // [B]
   int* flag;                      // [1] any trajectory still running (host loop / conditional)
+  unsigned* ticket;               // [1] finalize last-block counter (reset by the last block)
   double mw;                      // 1/N
 };
 
@@ -105,7 +106,8 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
     }
   }
   const GS xg = cvt<GS>(v);
-  const GS sv = dsin<GS>(xg), cv = dcos<GS>(xg);
+  GS sv, cv;
+  dsincos(xg, &sv, &cv);
   GS* sc = reinterpret_cast<GS*>(d.sc);
   sc[e] = sv;
   sc[(int64_t)d.B * d.n + e] = cv;

@@ -38,6 +38,15 @@ template <> __device__ __forceinline__ double dsin<double>(double x) { return si
 template <class S> __device__ __forceinline__ S dcos(S x);
 template <> __device__ __forceinline__ float dcos<float>(float x) { return cr_cosf(x); }
 template <> __device__ __forceinline__ double dcos<double>(double x) { return cos(x); }
+// sin and cos of one argument with a shared argument reduction (CUDA's
+// sincos evaluates the same kernels as sin and cos)
+__device__ __forceinline__ void dsincos(float x, float* s, float* c) {
+  double sd, cd;
+  sincos((double)x, &sd, &cd);
+  *s = __double2float_rn(sd);
+  *c = __double2float_rn(cd);
+}
+__device__ __forceinline__ void dsincos(double x, double* s, double* c) { sincos(x, s, c); }
 // fast-path arctangent: CUDA's own atanf (<= 2 ulp) in binary32 — the fast
 // sweep is held to tolerance parity, only the faithful sweep needs cr_atanf
 template <class S> __device__ __forceinline__ S fatan(S x);
@@ -105,7 +114,10 @@ struct Ctl {
   int32_t store32, time_limits, record_log, init_skip2;
   int32_t any_nonfinite;  // finalize scratch
   uint32_t ticket;        // last-block-done counter (finalize / init)
+  int32_t snap_on;        // record StepSnapshots (solver.cpp:324-327)
+  int32_t snap_pending;   // this attempt was accepted: k_snapshot copies x
   int32_t _pad;
+  double snap_hv;         // h of the accepted attempt (h_att before loop_check moves on)
 };
 
 struct StepLogRec {

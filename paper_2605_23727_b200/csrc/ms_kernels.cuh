@@ -239,8 +239,10 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs p) {
     // slot it is added to (systems.cpp:123-126, 141-143, 183-184)
     const GS xg = cvt<GS>(a[0]);
     if (p.split) {
-      gin[i] = dsin<GS>(xg);
-      gin[p.ld + i] = dcos<GS>(xg);
+      GS sv, cv;
+      dsincos(xg, &sv, &cv);
+      gin[i] = sv;
+      gin[p.ld + i] = cv;
     } else {
       gin[i] = xg;
     }
@@ -918,6 +920,8 @@ __device__ inline bool attempt_controller(Ctl* c, int S, int mode, int k1_elided
   }
   c->need_k1 = 0;
   c->nf_mask = 0;
+  c->snap_pending = (accepted && c->snap_on) ? 1 : 0;
+  if (accepted) c->snap_hv = h;
   if (accepted) {  // solver.cpp:321-336
     c->n_acc += 1;
     c->ix ^= 1;
@@ -1011,6 +1015,22 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
     for (int b = 0; b < (int)gridDim.x; ++b) e = fmax(e, f.B.part[b]);
   const bool more = attempt_controller(c, f.S, f.mode, f.k1_elided, f.fixed_k1, dead, stage_nf, any_nf, e, f.B.log);
   if (f.has_handle && f.mode == FIN_SOLVE) cudaGraphSetConditional(f.handle, more ? 1 : 0);
+}
+
+// StepSnapshot capture (solver.cpp:324-327): after an accepted attempt copy the
+// new loop state into row n_acc of the snapshot buffer (row 0 = the starting
+// state, written once after initialisation with row0 = 1).
+__global__ void __launch_bounds__(256) k_snapshot(Bufs B, double* snap, double* snap_h, int64_t cap, int64_t dn,
+                                                  int row0) {
+  const Ctl* c = B.ctl;
+  if (!row0 && !c->snap_pending) return;
+  const int64_t row = row0 ? 0 : c->n_acc;
+  if (row > cap) return;
+  const double* x = B.xb[c->ix];
+  double* dst = snap + row * dn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dn; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = x[e];
+  if (!row0 && blockIdx.x == 0 && threadIdx.x == 0) snap_h[row - 1] = c->snap_hv;
 }
 
 // ------------------------------------------------------------------------------

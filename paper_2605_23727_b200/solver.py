@@ -70,6 +70,13 @@ class StepRecord:  # solver.hpp:88-93
 
 
 @dataclass
+class StepSnapshot:  # solver.hpp:96-100: the state pair of one accepted step
+    x_before: np.ndarray
+    x_after: np.ndarray
+    h: float
+
+
+@dataclass
 class FlopTally:  # solver.hpp:104-113
     low: int = 0
     high: int = 0
@@ -91,6 +98,8 @@ class SolveResult:  # solver.hpp:115-126
     flops: FlopTally
     device_ms: float = 0.0
     step_log_count: int = 0
+    snapshots: list = field(default_factory=list)
+    snapshot_count: int = 0
 
     def total_steps(self) -> int:
         return self.n_accepted + self.n_failed
@@ -161,13 +170,30 @@ def bs32_step(sys: DeviceSystem, t: float, x_n, h: float, k1, policy: PrecisionP
                        FlopTally(o.flops_low, o.flops_high, o.rhs_evals))
 
 
-def _result(r: _abi.SolveResultC, final: np.ndarray, log: np.ndarray | None) -> SolveResult:
+def _result(r: _abi.SolveResultC, final: np.ndarray, log: np.ndarray | None, snaps=None) -> SolveResult:
     steps = []
     if log is not None:
         m = min(len(log), r.step_log_count)
         steps = [StepRecord(float(e.t), float(e.h), float(e.err), bool(e.accepted)) for e in log[:m]]
+    shots = []
+    if snaps is not None:
+        rows, hs = snaps
+        m = min(len(hs), r.snapshot_count)
+        shots = [StepSnapshot(rows[k], rows[k + 1], float(hs[k])) for k in range(m)]
     return SolveResult(SolveStatus(r.status), final, r.t_reached, r.n_accepted, r.n_failed, steps,
-                       FlopTally(r.flops_low, r.flops_high, r.rhs_evals), r.device_ms, r.step_log_count)
+                       FlopTally(r.flops_low, r.flops_high, r.rhs_evals), r.device_ms, r.step_log_count,
+                       shots, r.snapshot_count if snaps is not None else 0)
+
+
+def _snapshot_buffers(cfg: SolverConfig, dn: int, capacity: int | None):
+    """Host rows for StepSnapshots: by default as many accepted steps as fit
+    in 256 MiB (the count reported says whether the run had more)."""
+    if not cfg.record_snapshots:
+        return None
+    if capacity is None:
+        capacity = min(cfg.max_iterations, max(1, (256 << 20) // (8 * max(dn, 1)) - 1))
+    cap = max(int(capacity), 1)
+    return np.empty((cap + 1, dn)), np.empty(cap)
 
 
 def _log_buffer(cfg: SolverConfig, capacity: int | None):
@@ -179,20 +205,26 @@ def _log_buffer(cfg: SolverConfig, capacity: int | None):
 
 
 def solve(sys: DeviceSystem, x0, t0: float, t_final: float, policy: PrecisionPolicy, cfg: SolverConfig,
-          log_capacity: int | None = None) -> SolveResult:
-    """Adaptive BS3(2) solve (solver.cpp:462-470); the step loop runs on the device."""
+          log_capacity: int | None = None, snapshot_capacity: int | None = None) -> SolveResult:
+    """Adaptive BS3(2) solve (solver.cpp:462-470); the step loop runs on the device.
+    With ``cfg.record_snapshots`` the device copies the state after every
+    accepted step (solver.cpp:324-327) into ``result.snapshots``."""
     x0 = _f64(x0)
     final = np.empty_like(x0)
     log, cap = _log_buffer(cfg, log_capacity)
+    snaps = _snapshot_buffers(cfg, x0.size, snapshot_capacity)
     r = _abi.SolveResultC()
     r.final_state = _abi.dptr(final)
     if log is not None:
         r.step_log = C.cast(log, C.POINTER(_abi.StepRecordC))
         r.step_log_capacity = cap
+    if snaps is not None:
+        r.snapshots, r.snapshot_h = _abi.dptr(snaps[0]), _abi.dptr(snaps[1])
+        r.snapshot_capacity = len(snaps[1])
     pol, cc = policy.c(), cfg.c()
     _abi.check(_abi.lib().ms_solve(sys.handle, _abi.dptr(x0), t0, t_final, C.byref(pol), C.byref(cc),
                                    C.byref(r)), "ms_solve")
-    return _result(r, final, log)
+    return _result(r, final, log, snaps)
 
 
 def solve_device(sys: DeviceSystem, x0_dev_ptr: int, final_dev_ptr: int, t0: float, t_final: float,
