@@ -50,6 +50,19 @@ template <> struct K16<MS_K_BF16> {
   __device__ static T from(float v) { return __float2bfloat16_rn(v); }
 };
 
+// F of the Kuramoto agent in FS (systems.cpp:136-139): RN_FS(omega), exact in binary64
+__device__ __forceinline__ double b_fval(const BatchDev& d, int64_t e, int fs32) {
+  const double w = d.omega[e];
+  return fs32 ? (double)__double2float_rn(w) : w;
+}
+
+// Per-element inputs of the tensor-core coupling epilogue, written by the prep
+// kernel into the `sc` buffer on that path: one 16-byte load per (b, i).
+struct __align__(16) TcRec {
+  float s, c;  // sin, cos of theta_bi in binary32 (the row side, exact GS values)
+  double f;    // F = RN_FS(omega_bi)
+};
+
 struct BPrepArgs {
   BatchDev d;
   int S, l, kind, gate, count, out_slot, nterms;
@@ -108,9 +121,17 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
   const GS xg = cvt<GS>(v);
   GS sv, cv;
   dsincos(xg, &sv, &cv);
-  GS* sc = reinterpret_cast<GS*>(d.sc);
-  sc[e] = sv;
-  sc[(int64_t)d.B * d.n + e] = cv;
+  if (p.op_ks) {  // tensor-core path: the epilogue's record
+    TcRec r;
+    r.s = (float)sv;
+    r.c = (float)cv;
+    r.f = b_fval(d, e, p.fs32);
+    reinterpret_cast<TcRec*>(d.sc)[e] = r;
+  } else {
+    GS* sc = reinterpret_cast<GS*>(d.sc);
+    sc[e] = sv;
+    sc[(int64_t)d.B * d.n + e] = cv;
+  }
   // two-term operands: v = hi + lo with hi = RN16(v), lo = RN16(v - hi) (the
   // difference is exact in binary32), so K*hi + K*lo carries ~16-22 bits of v
   if (p.op_ks == MS_K_BF16) {
@@ -136,12 +157,6 @@ struct BRhsArgs {
   BatchDev d;
   int S, l, gate, out_slot, ws32, fs32;
 };
-
-// F of the Kuramoto agent in FS (systems.cpp:136-139): RN_FS(omega), exact in binary64
-__device__ __forceinline__ double b_fval(const BatchDev& d, int64_t e, int fs32) {
-  const double w = d.omega[e];
-  return fs32 ? (double)__double2float_rn(w) : w;
-}
 
 // coupling epilogue of one (row i, trajectory b): k = (double)(RN_WS(omega) +
 // RN_WS(mw (c_i A - s_i B))), SS arithmetic

@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -53,8 +54,10 @@ constexpr size_t kTcSmem = 1024 /*align slack*/ + (size_t)kTcStages * kTcStageBy
 
 struct TcGemm {
   CUtensorMap tmA;
-  CUtensorMap tmB;
+  CUtensorMap tmB;   // 256-row operand boxes (single-CTA kernel)
+  CUtensorMap tmB2;  // 128-row operand boxes (CTA-pair kernel)
   int grid_m = 0, grid_n = 0;
+  bool pair = true;  // CTA-pair kernel (MS_TC=1cta selects the single-CTA one)
   bool ready = false;
 };
 
@@ -97,6 +100,60 @@ __device__ __forceinline__ uint64_t umma_smem_desc(uint32_t smem_addr) {
   d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
   d |= (uint64_t)2 << 61;                    // layout: SWIZZLE_128B
   return d;
+}
+
+__device__ __forceinline__ void tc_ld32(uint32_t addr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Coupling epilogue of one warp: TMEM lane = row i, columns [c_beg, c_end) of
+// the tile (4 per trajectory: s_hi, s_lo, c_hi, c_lo sums). The record loads
+// of the next 8 trajectories are issued before the current 8 are finished.
+__device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr, int i, int tb0, int c_beg, int c_end,
+                                            const int* skip, double* const* outp) {
+  const BatchDev& d = t.a.d;
+  const float mw = (float)d.mw;
+  const TcRec* rec = reinterpret_cast<const TcRec*>(d.sc);
+  const bool row_ok = i < t.n;
+  TcRec cur[8];
+  auto load = [&](int c0, TcRec (&v)[8]) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int tq = (c0 >> 2) + q;
+      if (row_ok && !skip[tq]) v[q] = rec[(int64_t)(tb0 + tq) * d.n + i];
+    }
+  };
+  load(c_beg, cur);
+#pragma unroll 1
+  for (int c0 = c_beg; c0 < c_end; c0 += 32) {
+    uint32_t r[32];
+    tc_ld32(lane_addr + (uint32_t)c0, r);
+    TcRec nxt[8];
+    if (c0 + 32 < c_end) load(c0 + 32, nxt);
+    if (row_ok) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int tq = (c0 >> 2) + q;
+        if (skip[tq]) continue;
+        const float A = __fadd_rn(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]));
+        const float Bv = __fadd_rn(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(cur[q].c, A), __fmul_rn(cur[q].s, Bv)));
+        const double o = ws_add(cur[q].f, (double)coup, t.a.ws32);
+        outp[tq][i] = o;
+        if (!isfinite(o)) atomicOr(&d.ctl[tb0 + tq].nf_mask, 1 << t.a.l);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+  }
 }
 
 __global__ void __launch_bounds__(kTcThreads, MS_TC_MINB)
@@ -206,57 +263,197 @@ __global__ void __launch_bounds__(kTcThreads, MS_TC_MINB)
     tc_fence_after();
     const int i = m0 + q4 * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
-    const float mw = (float)d.mw;
-    const float* scf = reinterpret_cast<const float*>(d.sc);
-    const int64_t bn = (int64_t)d.B * d.n;
     constexpr int kCols = kTcBN * 4 / kTcEpiWarps;  // columns per epilogue warp
-#pragma unroll 1
-    for (int c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 32) {
-      uint32_t r[32];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-          : "r"(lane_addr + (uint32_t)c0));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (i >= t.n) continue;
-      // 8 trajectories per 32 columns: issue all their loads, then compute
-      float sv[8], cv[8];
-      double fv[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int tq = (c0 >> 2) + q;
-        const int b = tb0 + tq;
-        sv[q] = cv[q] = 0.f;
-        fv[q] = 0.0;
-        if (!tc_skip[tq]) {
-          const int64_t e = (int64_t)b * d.n + i;
-          sv[q] = scf[e];
-          cv[q] = scf[bn + e];
-          fv[q] = b_fval(d, e, t.a.fs32);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int tq = (c0 >> 2) + q;
-        if (tc_skip[tq]) continue;
-        const float A = __fadd_rn(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]));
-        const float Bv = __fadd_rn(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-        const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(cv[q], A), __fmul_rn(sv[q], Bv)));
-        const double o = ws_add(fv[q], (double)coup, t.a.ws32);
-        tc_out[tq][i] = o;
-        if (!isfinite(o)) atomicOr(&d.ctl[tb0 + tq].nf_mask, 1 << t.a.l);
-      }
-    }
+    tc_epilogue(t, lane_addr, i, tb0, half * kCols, (half + 1) * kCols, tc_skip, tc_out);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+// ------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x 512 tile (128 trajectories). Each CTA stages its 128 rows of K and its
+// two 128-column halves of the operand tile, so one k-block moves 96 KB for
+// 16.8 MFLOP (5.7 B/kFLOP, against 11.4 for the single-CTA 128 x 256 tile):
+// the stage contraction is bound by the L2->SM operand stream (~6.3 KB/cycle
+// chip-wide), not by the tensor pipe, so halving the bytes per flop is the
+// lever. The leader CTA (rank 0) issues tcgen05.mma.cta_group::2 M256 N256
+// twice per k-step (columns 0-255 and 256-511 of the tile into TMEM columns
+// 0-255 / 256-511 of both CTAs); both CTAs' TMA copies complete on the
+// leader's full barrier, and the leader's commits arrive on both CTAs' empty
+// barriers (multicast), so each producer refills only stages the pair's MMAs
+// have drained. Each CTA's epilogue owns its 128 rows x 128 trajectories.
+#ifndef MS_T2_BN
+#define MS_T2_BN 512     // GEMM columns per pair tile: 512 (two N256 MMAs, all of TMEM) or 256
+#endif
+#ifndef MS_T2_STAGES
+#define MS_T2_STAGES 4
+#endif
+#ifndef MS_T2_MINB
+#define MS_T2_MINB 1
+#endif
+constexpr int kT2BM = 128;           // rows per CTA (256 per pair)
+constexpr int kT2BN = MS_T2_BN;      // GEMM columns per pair tile
+constexpr int kT2NMma = kT2BN / 256; // N256 MMAs per k-step
+constexpr int kT2Half = 128;         // operand rows (columns of D) staged per CTA per MMA
+constexpr int kT2Stages = MS_T2_STAGES;
+#ifndef MS_T2_EPI
+#define MS_T2_EPI 8      // epilogue warps: 4 TMEM lane quarters x (MS_T2_EPI / 4) column parts
+#endif
+constexpr int kT2EpiWarps = MS_T2_EPI;
+constexpr int kT2ABytes = kT2BM * kTcBK * 2;               // 16 KB
+constexpr int kT2BBytes = kT2NMma * kT2Half * kTcBK * 2;   // 16 KB per N256 MMA
+constexpr int kT2StageBytes = kT2ABytes + kT2BBytes;
+constexpr int kT2Threads = 64 + 32 * kT2EpiWarps;
+constexpr size_t kT2Smem = 1024 + (size_t)kT2Stages * kT2StageBytes + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma2_load(uint32_t dst, const CUtensorMap* tm, uint32_t bar_cluster, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MINB)
+    k_tc_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs t) {
+  extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kT2Stages * kT2StageBytes);
+  uint64_t* empty = full + kT2Stages;
+  uint64_t* tmem_full = empty + kT2Stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  __shared__ int tc_skip[kT2BN / 4];
+  __shared__ double* tc_out[kT2BN / 4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int m0 = (blockIdx.x >> 1) * (2 * kT2BM) + (int)rank * kT2BM;  // this CTA's rows
+  const int n0 = blockIdx.y * kT2BN;                                    // the pair's columns
+  const int nkb = (t.n + kTcBK - 1) / kTcBK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < kT2Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {  // same warp in both CTAs (cta_group::2 allocation is collective over the pair)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(kT2BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // the peer's barriers exist before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs): own smem, completion on the leader's barrier
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % kT2Stages;
+        if (kb >= kT2Stages) tc_wait(&empty[st], ((kb / kT2Stages) & 1) ^ 1);
+        const uint32_t sa = smem_u32(smem + (size_t)st * kT2StageBytes);
+        const uint32_t sb = sa + kT2ABytes;
+        if (rank == 0) mbar_expect_tx(&full[st], 2 * kT2StageBytes);
+        const uint32_t bar = map_to_rank(smem_u32(&full[st]), 0);
+        tma2_load(sa, &tmA, bar, kb * kTcBK, m0);
+#pragma unroll
+        for (int hf = 0; hf < kT2NMma; ++hf)
+          tma2_load(sb + hf * (kT2Half * kTcBK * 2), &tmB, bar, kb * kTcBK, n0 + hf * 2 * kT2Half + (int)rank * kT2Half);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // MMA issuer: the leader only
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % kT2Stages;
+        tc_wait(&full[st], (kb / kT2Stages) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + (size_t)st * kT2StageBytes);
+        const uint32_t sb = sa + kT2ABytes;
+#pragma unroll
+        for (int k = 0; k < kTcBK / 16; ++k) {
+          const uint64_t adesc = umma_smem_desc(sa + k * 32);
+          const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+#pragma unroll
+          for (int hf = 0; hf < kT2NMma; ++hf) {
+            const uint64_t bdesc = umma_smem_desc(sb + hf * (kT2Half * kTcBK * 2) + k * 32);
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(hf * 256)),
+                "l"(adesc), "l"(bdesc), "r"(t.idesc), "r"(acc));
+          }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(&empty[st])),
+            "h"((uint16_t)3)
+            : "memory");
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              smem_u32(tmem_full)),
+          "h"((uint16_t)3)
+          : "memory");
+    }
+  } else {  // epilogue: TMEM lane quarter warp%4, column part (warp-2)/4
+    const int q4 = warp & 3;
+    const int part = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64;
+    const int tb0 = n0 >> 2;  // first trajectory of the pair tile (both CTAs: same columns)
+    const BatchDev& d = t.a.d;
+    if (et < kT2BN / 4) {
+      const int b = tb0 + et;
+      int skip = 1;
+      double* outp = nullptr;
+      if (b < d.B) {
+        const Ctl* c = d.ctl + b;
+        skip = stage_skip(c, t.a.l, t.a.gate) ? 1 : 0;
+        outp = bslot(d, t.a.S, t.a.out_slot, c) + (int64_t)b * d.n;
+      }
+      tc_skip[et] = skip;
+      tc_out[et] = outp;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kT2EpiWarps) : "memory");
+    tc_wait(tmem_full, 0);
+    tc_fence_after();
+    const int i = m0 + q4 * 32 + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
+    constexpr int kCols = kT2BN / (kT2EpiWarps / 4);  // columns per epilogue warp
+#ifndef MS_T2_NOEPI
+    tc_epilogue(t, lane_addr, i, tb0, part * kCols, (part + 1) * kCols, tc_skip, tc_out);
+#else
+    (void)lane_addr; (void)i; (void)kCols;
+#endif
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kT2BN));
   }
 }
 
@@ -290,21 +487,34 @@ inline void tc_gemm_setup(TcGemm& g, const BatchDev& d, int sms) {
                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("tensor map (operand) encode failed");
+    const cuuint32_t box2[2] = {kTcBK, kT2Half};
+    r = encode(&g.tmB2, dt, 2, d.op, dims, strides, box2, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("tensor map (operand, pair) encode failed");
   }
-  g.grid_m = (d.n + kTcBM - 1) / kTcBM;
-  g.grid_n = (4 * d.B + kTcBN - 1) / kTcBN;
-  cudaError_t e = cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-  if (e != cudaSuccess) throw std::runtime_error(std::string("tc gemm smem attribute: ") + cudaGetErrorString(e));
+  const char* v = std::getenv("MS_TC");
+  g.pair = !(v && std::string(v) == "1cta");
+  if (g.pair) {
+    g.grid_m = 2 * ((d.n + 2 * kT2BM - 1) / (2 * kT2BM));
+    g.grid_n = (4 * d.B + kT2BN - 1) / kT2BN;
+    cudaError_t e = cudaFuncSetAttribute(k_tc_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT2Smem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("tc gemm2 smem attribute: ") + cudaGetErrorString(e));
+  } else {
+    g.grid_m = (d.n + kTcBM - 1) / kTcBM;
+    g.grid_n = (4 * d.B + kTcBN - 1) / kTcBN;
+    cudaError_t e = cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("tc gemm smem attribute: ") + cudaGetErrorString(e));
+  }
   g.ready = true;
 }
 
 inline void tc_gemm_teardown(TcGemm& g) { g.ready = false; }
 
 // instruction descriptor of tcgen05.mma kind::f16: D f32, A/B bf16 (1) or
-// f16 (0), both K-major, N = 256, M = 128
-inline uint32_t tc_idesc(int ks) {
+// f16 (0), both K-major, N = 256, M = 128 (single CTA) or 256 (CTA pair)
+inline uint32_t tc_idesc(int ks, int m) {
   const uint32_t ab = ks == MS_K_F16 ? 0u : 1u;
-  return (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(kTcBN >> 3) << 17) | ((uint32_t)(kTcBM >> 4) << 24);
+  return (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 inline void launch_tc_gemm(const TcGemm& g, const BRhsArgs& a, cudaStream_t st) {
@@ -313,9 +523,14 @@ inline void launch_tc_gemm(const TcGemm& g, const BRhsArgs& a, cudaStream_t st) 
   t.a = a;
   t.n = a.d.n;
   t.ncol = 4 * a.d.B;
-  t.idesc = tc_idesc(a.d.ks);
   dim3 grid(g.grid_m, g.grid_n);
-  k_tc_gemm<<<grid, kTcThreads, kTcSmem, st>>>(g.tmA, g.tmB, t);
+  if (g.pair) {
+    t.idesc = tc_idesc(a.d.ks, 2 * kT2BM);
+    k_tc_gemm2<<<grid, kT2Threads, kT2Smem, st>>>(g.tmA, g.tmB2, t);
+  } else {
+    t.idesc = tc_idesc(a.d.ks, kTcBM);
+    k_tc_gemm<<<grid, kTcThreads, kTcSmem, st>>>(g.tmA, g.tmB, t);
+  }
 }
 
 }  // namespace msb

@@ -17,6 +17,17 @@ VARIANTS = {
     "tc_e8": ("ms_batch.cu", {"MS_TC_EPI_WARPS": 8}),
     "tc_s2x2_e8": ("ms_batch.cu", {"MS_TC_STAGES": 2, "MS_TC_MINB": 2, "MS_TC_EPI_WARPS": 8}),
     "tc_s3_e8": ("ms_batch.cu", {"MS_TC_STAGES": 3, "MS_TC_EPI_WARPS": 8}),
+    # CTA-pair kernel: tile width, ring depth, CTAs per SM, epilogue off (mainloop time)
+    "tc2_n512_s4": ("ms_batch.cu", {}),
+    "tc2_n512_s4_noepi": ("ms_batch.cu", {"MS_T2_NOEPI": 1}),
+    "tc2_n512_s3": ("ms_batch.cu", {"MS_T2_STAGES": 3}),
+    "tc2_n256_s4": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 4}),
+    "tc2_n256_s3x2": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2}),
+    "tc2_n256_s2x2": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 2, "MS_T2_MINB": 2}),
+    "tc2_n512_s4_e16": ("ms_batch.cu", {"MS_T2_EPI": 16}),
+    "tc2_n512_s3_e16": ("ms_batch.cu", {"MS_T2_EPI": 16, "MS_T2_STAGES": 3}),
+    "tc2_n256_s3x2_e16": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_EPI": 16}),
+    "tc2_n256_s3x2_noepi": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_NOEPI": 1}),
 }
 
 

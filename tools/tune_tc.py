@@ -26,7 +26,7 @@ out = bat.eval_rhs(x, SSS)
 print("JSON" + json.dumps({"gemm_ms": rhs.value, "prep_ms": prep.value, "digest": float(np.sum(out[:, :64]))}))
 ''' % ROOT
 res = {}
-for lib in sorted(VAR.glob("lib_tc_*.so")):
+for lib in sorted(VAR.glob(sys.argv[1] if len(sys.argv) > 1 else "lib_tc*.so")):
     name = lib.stem[4:]
     r = subprocess.run([sys.executable, "-c", CHILD], env=dict(os.environ, MS_LIB_PATH=str(lib)),
                        capture_output=True, text=True, timeout=600)
