@@ -291,6 +291,19 @@ int ms_loop_run_segment(ms_system_t sys, int list, int index, void* stream, ms_e
 int ms_loop_done(ms_system_t sys, void* stream, int* done);
 int ms_loop_end(ms_system_t sys, ms_solve_result* res, int final_on_device, void* stream);
 
+/* ---- concurrent policy variants ------------------------
+ * Up to four solves of one system from the same x0, one policy each (the
+ * harness's Single/Mixed1/Mixed2/Double, harness.cpp:113-121), advanced in
+ * lock-step attempts on the device. For the split Kuramoto over a stored K
+ * each stage is ONE K sweep for all variants. Every variant's result (state,
+ * counts, step log) is bit-identical to its own ms_solve; device_ms is the
+ * shared loop time. Snapshots are not recorded here. */
+typedef struct ms_variants* ms_variants_t;
+int ms_variants_create(ms_system_t sys, int32_t count, ms_variants_t* out);
+int ms_variants_destroy(ms_variants_t v);
+int ms_variants_solve(ms_variants_t v, const double* x0, double t0, double t_final, const ms_policy* policies,
+                      const ms_solver_config* cfg, ms_solve_result* results);
+
 /* ---- batched ensembles sharing one K (BASELINE.json configs[4]) ---------
  * B Kuramoto trajectories (own omega_b, theta0_b, own adaptive controller)
  * over the K of a Kuramoto system handle. Each trajectory follows the

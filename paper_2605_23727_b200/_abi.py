@@ -134,6 +134,10 @@ SIGNATURES = [
     ("ms_loop_run_segment", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(ExchangeC)]),
     ("ms_loop_done", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]),
     ("ms_loop_end", C.c_int, [C.c_void_p, C.POINTER(SolveResultC), C.c_int, C.c_void_p]),
+    ("ms_variants_create", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("ms_variants_destroy", C.c_int, [C.c_void_p]),
+    ("ms_variants_solve", C.c_int, [C.c_void_p, _DP, C.c_double, C.c_double, C.POINTER(Policy),
+                                    C.POINTER(SolverConfigC), C.POINTER(SolveResultC)]),
     ("ms_batch_create", C.c_int, [C.c_void_p, C.c_int32, _DP, C.c_int32, C.POINTER(C.c_void_p)]),
     ("ms_batch_destroy", C.c_int, [C.c_void_p]),
     ("ms_batch_eval_rhs", C.c_int, [C.c_void_p, _DP, StagePrec, _DP]),

@@ -22,6 +22,7 @@
 
 #define MS_DEFINE_STEP_KERNELS 1
 #include "ms_dispatch.h"
+#include "ms_multi.cuh"
 #include "ms_internal.h"
 
 using namespace msb;
@@ -315,6 +316,48 @@ double* upload_array(ms_system* s, const double* host, int n) {
 
 size_t kelem_bytes(int ks) { return ks == MS_K_F32 ? 4 : 2; }
 
+size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// bytes of one solve workspace (Bufs) with a step log of log_cap records
+size_t bufs_bytes(const ms_system* s, int64_t log_cap) {
+  const int64_t dn = s->dn();
+  const int fin_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((dn + kFinThreads - 1) / kFinThreads, 2 * s->sms));
+  const size_t vec = al256(sizeof(double) * dn);
+  size_t total = 0;
+  total += 2 * vec;                                      // xb
+  total += (kMaxStages + 1) * vec;                       // kb
+  total += 3 * vec;                                      // xn, xt, scratch
+  total += al256(sizeof(double) * 2 * s->ld);            // gin
+  total += al256(sizeof(double) * s->ld);                // rowc
+  total += al256(sizeof(double) * s->n);                 // fvc
+  total += al256(sizeof(double) * fin_blocks);           // part
+  total += al256(sizeof(StepLogRec) * std::max<int64_t>(log_cap, 1));
+  total += al256(sizeof(Ctl));
+  return total;
+}
+
+void carve_bufs(const ms_system* s, char* base, int64_t log_cap, Bufs& B) {
+  const int64_t dn = s->dn();
+  const int fin_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((dn + kFinThreads - 1) / kFinThreads, 2 * s->sms));
+  char* p = base;
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += al256(b);
+    return r;
+  };
+  for (int i = 0; i < 2; ++i) B.xb[i] = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  for (int i = 0; i < kMaxStages + 1; ++i) B.kb[i] = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  B.xn = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  B.xt = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  B.scratch = reinterpret_cast<double*>(take(sizeof(double) * dn));
+  B.gin = take(sizeof(double) * 2 * s->ld);
+  B.rowc = take(sizeof(double) * s->ld);
+  B.fvc = reinterpret_cast<double*>(take(sizeof(double) * s->n));
+  B.part = reinterpret_cast<double*>(take(sizeof(double) * fin_blocks));
+  B.log = reinterpret_cast<StepLogRec*>(take(sizeof(StepLogRec) * std::max<int64_t>(log_cap, 1)));
+  B.ctl = reinterpret_cast<Ctl*>(take(sizeof(Ctl)));
+}
+
 void ensure_workspace(ms_system* s, int64_t log_cap) {
   if (s->ws_ready && log_cap <= s->log_cap) return;
   if (s->ws_ready) {
@@ -328,45 +371,16 @@ void ensure_workspace(ms_system* s, int64_t log_cap) {
     CK(cudaFree(s->ws_mem));
     s->ws_ready = false;
   }
-  const int64_t dn = s->dn();
-  s->fin_blocks = (int)std::min<int64_t>((dn + kFinThreads - 1) / kFinThreads, 2 * s->sms);
+  s->fin_blocks = (int)std::min<int64_t>((s->dn() + kFinThreads - 1) / kFinThreads, 2 * s->sms);
   if (s->fin_blocks < 1) s->fin_blocks = 1;
-  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t vec = al(sizeof(double) * dn);
-  size_t total = 0;
-  total += 2 * vec;                                  // xb
-  total += (kMaxStages + 1) * vec;                   // kb
-  total += 3 * vec;                                  // xn, xt, scratch
-  total += al(sizeof(double) * 2 * s->ld);           // gin
-  total += al(sizeof(double) * s->ld);               // rowc
-  total += al(sizeof(double) * s->n);                // fvc
-  total += al(sizeof(double) * s->fin_blocks);       // part
-  total += al(sizeof(StepLogRec) * std::max<int64_t>(log_cap, 1));
-  total += al(sizeof(Ctl));
+  const size_t total = bufs_bytes(s, log_cap);
   char* base = nullptr;
   CK(cudaMalloc(&base, total));
   // zero on the system's own (non-blocking) stream: a legacy-stream memset
   // is not ordered before kernels on s->stream and can land after them
   CK(cudaMemsetAsync(base, 0, total, s->stream));
   s->ws_mem = base;
-  char* p = base;
-  auto take = [&](size_t b) {
-    char* r = p;
-    p += al(b);
-    return r;
-  };
-  Bufs& B = s->B;
-  for (int i = 0; i < 2; ++i) B.xb[i] = reinterpret_cast<double*>(take(sizeof(double) * dn));
-  for (int i = 0; i < kMaxStages + 1; ++i) B.kb[i] = reinterpret_cast<double*>(take(sizeof(double) * dn));
-  B.xn = reinterpret_cast<double*>(take(sizeof(double) * dn));
-  B.xt = reinterpret_cast<double*>(take(sizeof(double) * dn));
-  B.scratch = reinterpret_cast<double*>(take(sizeof(double) * dn));
-  B.gin = take(sizeof(double) * 2 * s->ld);
-  B.rowc = take(sizeof(double) * s->ld);
-  B.fvc = reinterpret_cast<double*>(take(sizeof(double) * s->n));
-  B.part = reinterpret_cast<double*>(take(sizeof(double) * s->fin_blocks));
-  B.log = reinterpret_cast<StepLogRec*>(take(sizeof(StepLogRec) * std::max<int64_t>(log_cap, 1)));
-  B.ctl = reinterpret_cast<Ctl*>(take(sizeof(Ctl)));
+  carve_bufs(s, base, log_cap, s->B);
   s->log_cap = std::max<int64_t>(log_cap, 1);
   if (!s->ctl_host) CK(cudaMallocHost(&s->ctl_host, sizeof(Ctl)));
   s->ws_ready = true;
@@ -388,12 +402,13 @@ struct EvalSpec {
   const double* xsrc = nullptr;
 };
 
-void launch_eval(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp,
-                 cudaEvent_t mid0 = nullptr, cudaEvent_t mid1 = nullptr) {
+// prep of one evaluation into workspace B; false when the model has no
+// coupling sweep (the reference's scalar test fixtures)
+bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp) {
   const bool fs32 = is32(sp.f_prec), ss32 = is32(sp.sum_prec), gs32 = is32(sp.g_prec);
   PrepArgs p{};
   p.md = s->md;
-  p.B = s->B;
+  p.B = B;
   p.S = e.S;
   p.l = e.l;
   p.kind = e.kind;
@@ -416,7 +431,7 @@ void launch_eval(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_stag
   if (s->fixture) {
     launch_prep_model<-1>(fs32, gs32, pgrid, st, p);
     CK(cudaGetLastError());
-    return;
+    return false;
   }
   switch (s->mkind) {
     case MD_LCO: launch_prep_model<MD_LCO>(fs32, gs32, pgrid, st, p); break;
@@ -424,9 +439,14 @@ void launch_eval(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_stag
     default: launch_prep_model<MD_CC>(fs32, gs32, pgrid, st, p); break;
   }
   CK(cudaGetLastError());
+  (void)ss32;
+  return true;
+}
+
+RhsArgs rhs_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_prec& sp) {
   RhsArgs a{};
-  a.ctl = s->B.ctl;
-  a.nf_mask = &s->B.ctl->nf_mask;
+  a.ctl = B.ctl;
+  a.nf_mask = &B.ctl->nf_mask;
   a.l = e.l;
   a.gate = e.gate;
   a.S = e.S;
@@ -436,21 +456,38 @@ void launch_eval(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_stag
   a.n = s->n;
   a.row0 = s->row0;
   a.row1 = s->row1;
-  a.gin = s->B.gin;
-  a.rowc = s->B.rowc;
-  a.fvc = s->B.fvc;
-  for (int i = 0; i < kMaxStages + 1; ++i) a.kb[i] = s->B.kb[i];
+  a.gin = B.gin;
+  a.rowc = B.rowc;
+  a.fvc = B.fvc;
+  for (int i = 0; i < kMaxStages + 1; ++i) a.kb[i] = B.kb[i];
   a.d = s->d;
   a.cs = s->cs;
   a.mw = s->md.m[s->cs];
   a.coupling_k = s->md.coupling_k;
-  a.ws32 = p.ws32;
-  RhsLaunch L{s->mkind, p.split != 0, ss32, gs32, s->ks, s->sms, st};
-  if (mid0) CK(cudaEventRecord(mid0, st));
+  a.ws32 = (is32(sp.f_prec) && is32(sp.sum_prec)) ? 1 : 0;
+  return a;
+}
+
+void launch_sweep(ms_system* s, cudaStream_t st, const RhsArgs& a, const ms_stage_prec& sp) {
+  const bool split = s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST;
+  RhsLaunch L{s->mkind, split, is32(sp.sum_prec), is32(sp.g_prec), s->ks, s->sms, st};
   if (s->rhs_mode == MS_RHS_FAST) launch_rhs_fast(L, a);
   else launch_rhs_faithful(L, a);
   CK(cudaGetLastError());
+}
+
+void launch_eval(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp,
+                 cudaEvent_t mid0 = nullptr, cudaEvent_t mid1 = nullptr) {
+  if (!launch_prep(s, B, st, e, sp)) return;
+  const RhsArgs a = rhs_args(s, B, e, sp);
+  if (mid0) CK(cudaEventRecord(mid0, st));
+  launch_sweep(s, st, a, sp);
   if (mid1) CK(cudaEventRecord(mid1, st));
+}
+
+void launch_eval(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp,
+                 cudaEvent_t mid0 = nullptr, cudaEvent_t mid1 = nullptr) {
+  launch_eval(s, s->B, st, e, sp, mid0, mid1);
 }
 
 // stage l of an attempt (rk_step, solver.cpp:130-154)
@@ -471,9 +508,9 @@ EvalSpec stage_spec(const Tableau& T, int l) {
   return e;
 }
 
-FinArgs fin_args(ms_system* s, const Tableau& T, int mode, int k1_elided) {
+FinArgs fin_args(ms_system* s, const Bufs& B, const Tableau& T, int mode, int k1_elided) {
   FinArgs f{};
-  f.B = s->B;
+  f.B = B;
   f.S = T.S;
   for (int m = 0; m < T.S; ++m) {
     if (T.b_tilde[m] == 0.0) continue;
@@ -536,7 +573,7 @@ void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_
     launch_eval(s, st, e, P.k1_row);
   }
   for (int l = 1; l < T.S; ++l) launch_eval(s, st, stage_spec(T, l), P.rows[l - 1]);
-  FinArgs f = fin_args(s, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
+  FinArgs f = fin_args(s, s->B, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
   f.has_handle = has_handle ? 1 : 0;
   f.handle = h;
   k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
@@ -929,7 +966,7 @@ void loop_run(ms_system* s, const SolvePlan& P, int list, int index, cudaStream_
   }
   if (l != S) throw InvalidArg("loop: bad attempt segment");
   launch_scan(s, st, out_of(S - 1), S - 1);
-  FinArgs f = fin_args(s, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
+  FinArgs f = fin_args(s, s->B, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
   f.fixed_k1 = 1;
   k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
   CK(cudaGetLastError());
@@ -946,6 +983,331 @@ void check_policy(const ms_policy& p) {
   for (int l = 0; l < 3; ++l) check_prec(p.per_stage[l]);
   check_prec(p.first_step_k1);
   if (p.storage > 1) throw InvalidArg("policy: bad storage format");
+}
+
+}  // namespace
+
+
+// =====================================================================================
+// Concurrent policy variants: up to four solves of one system
+// (the harness's Single/Mixed1/Mixed2/Double, harness.cpp:113-121) advanced in
+// lock-step attempts, each lane with its own workspace and controller. Every
+// stage is the lanes' preps followed by ONE K sweep (k_rhs_multi) when the
+// model is the split Kuramoto over a stored K; otherwise by the lanes' own
+// sweeps back to back. A lane that finishes stops launching work of its own.
+
+namespace {
+
+bool use_multi_sweep(const ms_system* s) {
+  const char* v = std::getenv("MS_MULTI");
+  if (v && std::strcmp(v, "off") == 0) return false;
+  return !s->fixture && s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST && s->ks != MS_K_SCALAR;
+}
+
+struct LaneCtls {
+  Ctl* c[kMaxLanes];
+};
+
+// loop condition over the lanes (the WHILE node of the variants graph)
+__global__ void k_lanes_cond(LaneCtls L, int nl, int* flag, int has_handle, cudaGraphConditionalHandle h) {
+  int any = 0;
+  for (int v = 0; v < nl; ++v) any |= L.c[v]->done == 0;
+  *flag = any;
+  if (has_handle) cudaGraphSetConditional(h, any ? 1 : 0);
+}
+
+}  // namespace
+
+struct ms_variants {
+  ms_system* s = nullptr;
+  int nl = 0;
+  char* mem = nullptr;
+  int64_t log_cap = 0;
+  Bufs B[kMaxLanes];
+  Ctl* ctl_host = nullptr;  // pinned [kMaxLanes]
+  int* flag = nullptr;      // device: any lane still running
+  int* flag_host = nullptr;
+  std::map<std::string, ms_system::GraphEntry> graphs;
+  std::mutex mu;
+};
+
+namespace {
+
+void drop_graphs(ms_variants* v) {
+  for (auto& kv : v->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.g) cudaGraphDestroy(kv.second.g);
+  }
+  v->graphs.clear();
+}
+
+void variants_workspace(ms_variants* v, int64_t log_cap) {
+  ms_system* s = v->s;
+  if (v->mem && log_cap <= v->log_cap) return;
+  CK(cudaStreamSynchronize(s->stream));
+  drop_graphs(v);
+  if (v->mem) CK(cudaFree(v->mem));
+  v->mem = nullptr;
+  const size_t one = bufs_bytes(s, log_cap);
+  CK(cudaMalloc(&v->mem, one * v->nl + 256));
+  CK(cudaMemsetAsync(v->mem, 0, one * v->nl + 256, s->stream));
+  for (int l = 0; l < v->nl; ++l) carve_bufs(s, v->mem + one * l, log_cap, v->B[l]);
+  v->flag = reinterpret_cast<int*>(v->mem + one * v->nl);
+  v->log_cap = log_cap;
+}
+
+// one evaluation of every participating lane: preps, then the shared sweep
+void mlaunch_eval(ms_variants* v, cudaStream_t st, const EvalSpec* e, const ms_stage_prec* sp, const bool* on) {
+  ms_system* s = v->s;
+  bool sweep = false;
+  for (int l = 0; l < v->nl; ++l)
+    if (on[l]) sweep |= launch_prep(s, v->B[l], st, e[l], sp[l]);
+  if (!sweep) return;
+  // participating lanes sorted by (SS, GS): (f32,f32) | (f64,f32) | (f64,f64)
+  int order[kMaxLanes], cnt[3] = {0, 0, 0}, np = 0;
+  bool fusable = use_multi_sweep(s);
+  for (int pass = 0; pass < 3; ++pass)
+    for (int l = 0; l < v->nl; ++l) {
+      if (!on[l]) continue;
+      const bool ss64 = !is32(sp[l].sum_prec), gs64 = !is32(sp[l].g_prec);
+      const int ty = !ss64 ? (gs64 ? -1 : 0) : (gs64 ? 2 : 1);
+      if (ty < 0) fusable = false;  // (f32 sum, f64 G): no fused kernel
+      if (ty == pass) {
+        order[np++] = l;
+        ++cnt[pass];
+      }
+    }
+  if (fusable && np >= 2) {
+    MultiArgs m{};
+    m.nl = np;
+    m.l = e[order[0]].l;
+    m.gate = e[order[0]].gate;
+    m.S = e[order[0]].S;
+    m.out_slot = e[order[0]].out_slot;
+    m.ld = s->ld;
+    m.n = s->n;
+    m.row0 = s->row0;
+    m.row1 = s->row1;
+    m.mw = s->md.m[s->cs];
+    for (int i = 0; i < np; ++i) {
+      const int l = order[i];
+      LaneArgs& L = m.lane[i];
+      L.ctl = v->B[l].ctl;
+      L.nf_mask = &v->B[l].ctl->nf_mask;
+      L.gin = v->B[l].gin;
+      L.fvc = v->B[l].fvc;
+      for (int j = 0; j < kMaxStages + 1; ++j) L.kb[j] = v->B[l].kb[j];
+      L.ws32 = (is32(sp[l].f_prec) && is32(sp[l].sum_prec)) ? 1 : 0;
+    }
+    launch_rhs_multi(m, cnt[0], cnt[1], cnt[2], s->ks, s->K, s->sms, st);
+    CK(cudaGetLastError());
+  } else {
+    for (int l = 0; l < v->nl; ++l)
+      if (on[l]) launch_sweep(s, st, rhs_args(s, v->B[l], e[l], sp[l]), sp[l]);
+  }
+}
+
+// initial_step + cold k1 of every lane (launch_init, lane-parallel)
+void mlaunch_init(ms_variants* v, cudaStream_t st, const SolvePlan* P) {
+  ms_system* s = v->s;
+  const Tableau& T = *P[0].T;
+  const int nl = v->nl;
+  bool on[kMaxLanes] = {};
+  EvalSpec e[kMaxLanes];
+  ms_stage_prec sp[kMaxLanes];
+  for (int l = 0; l < nl; ++l) {
+    on[l] = true;
+    k_stamp_start<<<1, 1, 0, st>>>(v->B[l].ctl);
+    e[l].S = T.S;
+    e[l].l = 7;
+    e[l].kind = PREP_X;
+    e[l].count = CNT_DDD;
+    e[l].out_slot = 1;
+    sp[l] = kDDD;
+  }
+  mlaunch_eval(v, st, e, sp, on);
+  InitArgs ia[kMaxLanes];
+  for (int l = 0; l < nl; ++l) {
+    ia[l] = InitArgs{};
+    ia[l].B = v->B[l];
+    ia[l].x0 = v->B[l].xb[0];
+    ia[l].dn = s->dn();
+    ia[l].exponent = 1.0 / static_cast<double>(T.order_high + 1);
+    k_init_a<<<1, 1024, 0, st>>>(ia[l]);
+    CK(cudaGetLastError());
+    e[l].kind = PREP_INIT_X1;
+    e[l].gate = GATE_INIT2;
+    e[l].out_slot = 2;
+  }
+  mlaunch_eval(v, st, e, sp, on);
+  for (int l = 0; l < nl; ++l) {
+    k_init_b<<<1, 1024, 0, st>>>(ia[l]);
+    CK(cudaGetLastError());
+    e[l] = EvalSpec{};
+    e[l].S = T.S;
+    e[l].l = 0;
+    e[l].kind = PREP_X;
+    e[l].count = CNT_K1;
+    e[l].out_slot = SLOT_K1;
+    e[l].round_x = P[l].storage == MS_BINARY32 ? 1 : 0;
+    sp[l] = P[l].k1_row;
+  }
+  mlaunch_eval(v, st, e, sp, on);
+  for (int l = 0; l < nl; ++l) k_loop_head<<<1, 1, 0, st>>>(v->B[l].ctl);
+  CK(cudaGetLastError());
+}
+
+// one lock-step attempt of every lane (launch_attempt, lane-parallel)
+void mlaunch_attempt(ms_variants* v, cudaStream_t st, const SolvePlan* P, bool has_handle,
+                     cudaGraphConditionalHandle h) {
+  ms_system* s = v->s;
+  const Tableau& T = *P[0].T;
+  const int nl = v->nl;
+  bool on[kMaxLanes] = {};
+  EvalSpec e[kMaxLanes];
+  ms_stage_prec sp[kMaxLanes];
+  bool any_k1 = false;
+  for (int l = 0; l < nl; ++l) {
+    on[l] = !P[l].k1_elided;
+    any_k1 |= on[l];
+    e[l].S = T.S;
+    e[l].l = 0;
+    e[l].kind = PREP_X;
+    e[l].gate = GATE_NEED_K1;
+    e[l].count = CNT_K1;
+    e[l].out_slot = SLOT_K1;
+    sp[l] = P[l].k1_row;
+  }
+  if (any_k1) mlaunch_eval(v, st, e, sp, on);
+  for (int st_l = 1; st_l < T.S; ++st_l) {
+    for (int l = 0; l < nl; ++l) {
+      on[l] = true;
+      e[l] = stage_spec(T, st_l);
+      sp[l] = P[l].rows[st_l - 1];
+    }
+    mlaunch_eval(v, st, e, sp, on);
+  }
+  LaneCtls lc{};
+  for (int l = 0; l < nl; ++l) {
+    FinArgs f = fin_args(s, v->B[l], T, FIN_SOLVE, P[l].k1_elided ? 1 : 0);
+    f.has_handle = 0;
+    k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
+    CK(cudaGetLastError());
+    lc.c[l] = v->B[l].ctl;
+  }
+  k_lanes_cond<<<1, 1, 0, st>>>(lc, nl, v->flag, has_handle ? 1 : 0, h);
+  CK(cudaGetLastError());
+}
+
+cudaGraphExec_t variants_graph(ms_variants* v, const SolvePlan* P) {
+  std::string key;
+  for (int l = 0; l < v->nl; ++l) key += plan_key(P[l]) + "|";
+  auto it = v->graphs.find(key);
+  if (it != v->graphs.end()) return it->second.exec;
+  ms_system* s = v->s;
+  ms_system::GraphEntry ge;
+  CK(cudaGraphCreate(&ge.g, 0));
+  cudaGraphConditionalHandle handle;
+  CK(cudaGraphConditionalHandleCreate(&handle, ge.g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, ge.g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(s->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  try {
+    mlaunch_attempt(v, s->stream, P, true, handle);
+  } catch (...) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(s->stream, &dummy);
+    throw;
+  }
+  CK(cudaStreamEndCapture(s->stream, &body));
+  CK(cudaGraphInstantiate(&ge.exec, ge.g, 0));
+  v->graphs[key] = ge;
+  return ge.exec;
+}
+
+void run_variants(ms_variants* v, const double* x0, double t0, double tf, const ms_policy* pols,
+                  const ms_solver_config& cfg, ms_solve_result* res) {
+  validate_cfg(cfg, t0, tf);
+  if (cfg.record_snapshots) throw InvalidArg("variants: snapshots are recorded by ms_solve only");
+  ms_system* s = v->s;
+  std::lock_guard<std::mutex> lk(s->mu);
+  std::lock_guard<std::mutex> lk2(v->mu);
+  set_device(s);
+  ensure_workspace(s, 1);  // sets fin_blocks; the lanes carry their own buffers
+  SolvePlan P[kMaxLanes];
+  int64_t cap = 1;
+  for (int l = 0; l < v->nl; ++l) {
+    check_policy(pols[l]);
+    P[l] = plan_bs32(pols[l]);
+    if (cfg.record_step_log && res[l].step_log) cap = std::max<int64_t>(cap, res[l].step_log_capacity);
+  }
+  variants_workspace(v, cap);
+  cudaStream_t st = s->stream;
+  const int64_t dn = s->dn();
+  for (int l = 0; l < v->nl; ++l) {
+    init_ctl(s, v->ctl_host[l], cfg, t0, tf, P[l], v->log_cap);
+    CK(cudaMemcpyAsync(v->B[l].ctl, &v->ctl_host[l], sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(v->B[l].xb[0], x0, sizeof(double) * dn, cudaMemcpyHostToDevice, st));
+  }
+  const bool host_loop = use_host_loop();
+  cudaGraphExec_t exec = host_loop ? nullptr : variants_graph(v, P);
+  CK(cudaEventRecord(s->ev0, st));
+  mlaunch_init(v, st, P);
+  if (host_loop) {
+    for (;;) {
+      mlaunch_attempt(v, st, P, false, 0);
+      CK(cudaMemcpyAsync(v->flag_host, v->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (!*v->flag_host) break;
+    }
+  } else {
+    CK(cudaGraphLaunch(exec, st));
+  }
+  CK(cudaEventRecord(s->ev1, st));
+  for (int l = 0; l < v->nl; ++l)
+    CK(cudaMemcpyAsync(&v->ctl_host[l], v->B[l].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  for (int l = 0; l < v->nl; ++l) {
+    const Ctl& c = v->ctl_host[l];
+    ms_solve_result* r = &res[l];
+    if (r->final_state)
+      CK(cudaMemcpyAsync(r->final_state, v->B[l].xb[c.ix], sizeof(double) * dn, cudaMemcpyDeviceToHost, st));
+    r->step_log_count = c.record_log ? c.log_count : 0;
+    if (r->step_log && c.record_log) {
+      const int64_t m = std::min<int64_t>(std::min<int64_t>(r->step_log_capacity, c.log_count), v->log_cap);
+      if (m > 0) {
+        std::vector<StepLogRec> tmp((size_t)m);
+        CK(cudaMemcpyAsync(tmp.data(), v->B[l].log, sizeof(StepLogRec) * m, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int64_t i = 0; i < m; ++i) {
+          r->step_log[i].t = tmp[(size_t)i].t;
+          r->step_log[i].h = tmp[(size_t)i].h;
+          r->step_log[i].err = tmp[(size_t)i].err;
+          r->step_log[i].accepted = tmp[(size_t)i].accepted;
+        }
+      }
+    }
+    r->snapshot_count = 0;
+    r->status = c.status;
+    r->t_reached = c.t;
+    r->n_accepted = c.n_acc;
+    r->n_failed = c.n_fail;
+    int64_t tl[3];
+    tally(s, c, P[l], tl);
+    r->rhs_evals = tl[0];
+    r->flops_low = tl[1];
+    r->flops_high = tl[2];
+    r->device_ms = ms;
+  }
+  CK(cudaStreamSynchronize(st));
 }
 
 }  // namespace
@@ -1374,7 +1736,7 @@ int ms_bs32_step(ms_system_t s, double t, const double* x_n, double h, const dou
     CK(cudaMemcpyAsync(s->B.xb[0], x_n, sizeof(double) * dn, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(s->B.kb[0], k1, sizeof(double) * dn, cudaMemcpyHostToDevice, st));
     for (int l = 1; l < T.S; ++l) launch_eval(s, st, stage_spec(T, l), P.rows[l - 1]);
-    FinArgs f = fin_args(s, T, FIN_STEP, 0);
+    FinArgs f = fin_args(s, s->B, T, FIN_STEP, 0);
     k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&c, s->B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -1552,6 +1914,41 @@ int ms_dp54_reference(ms_system_t s, const double* x0, double t0, double t_final
     rc.controller_exponent = 1.0 / 5.0;
     rc.record_snapshots = 0;
     run_solve(s, x0, false, t0, t_final, plan_dp54(), rc, res, nullptr, false);
+  });
+}
+
+int ms_variants_create(ms_system_t s, int count, ms_variants_t* out) {
+  return guard([&] {
+    if (!s || !out) throw InvalidArg("variants_create: null argument");
+    if (count < 1 || count > kMaxLanes) throw InvalidArg("variants_create: count must be 1..4");
+    set_device(s);
+    auto v = std::make_unique<ms_variants>();
+    v->s = s;
+    v->nl = count;
+    CK(cudaMallocHost(&v->ctl_host, sizeof(Ctl) * kMaxLanes));
+    CK(cudaMallocHost(&v->flag_host, sizeof(int)));
+    *out = v.release();
+  });
+}
+
+int ms_variants_destroy(ms_variants_t v) {
+  if (!v) return MS_OK;
+  return guard([&] {
+    cudaSetDevice(v->s->dev);
+    cudaStreamSynchronize(v->s->stream);
+    drop_graphs(v);
+    if (v->mem) cudaFree(v->mem);
+    if (v->ctl_host) cudaFreeHost(v->ctl_host);
+    if (v->flag_host) cudaFreeHost(v->flag_host);
+    delete v;
+  });
+}
+
+int ms_variants_solve(ms_variants_t v, const double* x0, double t0, double t_final, const ms_policy* policies,
+                      const ms_solver_config* cfg, ms_solve_result* results) {
+  return guard([&] {
+    if (!v || !x0 || !policies || !cfg || !results) throw InvalidArg("variants_solve: null argument");
+    run_variants(v, x0, t0, t_final, policies, *cfg, results);
   });
 }
 

@@ -106,6 +106,9 @@ class RunOptions:  # harness.hpp:52-60 (jobs: one device, cases run in order)
     output_dir: str = ""
     step_log_csv: bool = False
     rhs_mode: str = "fast"
+    # run the variants of a case concurrently (DeviceVariants: one K sweep per
+    # stage for all of them; results bit-identical to one solve each)
+    concurrent_variants: bool = True
 
 
 @dataclass
@@ -144,6 +147,9 @@ class DeviceEngine:
 
     def dp54_reference(self, sys, x0, tf, cfg):
         return S.dp54_reference(sys, x0, 0.0, tf, cfg)
+
+    def solve_variants(self, sys, x0, tf, policies, cfg):
+        return S.solve_variants(sys, x0, 0.0, tf, policies, cfg)
 
     def release(self, sys):
         sys.close()
@@ -199,11 +205,15 @@ def run_one(tc: TestCase, spec: CampaignSpec | None = None, opt: RunOptions | No
                             wall_clock_limit=opt.wall_clock_limit, slow_solver_elapsed=opt.slow_solver_elapsed,
                             slow_solver_progress=opt.slow_solver_progress)
         ref = engine.dp54_reference(sys, x0, tc.t_final, base)
-        runs, double_steps = [], None
-        for v in spec.variants:
-            cfg = SolverConfig(**{**base.__dict__, "record_snapshots": spec.snapshots and tc.benchmark == "lco"})
-            r = engine.solve(sys, x0, tc.t_final, policy_for(v), cfg)
-            runs.append(r)
+        snaps = spec.snapshots and tc.benchmark == "lco"
+        cfg = SolverConfig(**{**base.__dict__, "record_snapshots": snaps})
+        if (opt.concurrent_variants and not snaps and hasattr(engine, "solve_variants")
+                and 1 <= len(spec.variants) <= 4):
+            runs = engine.solve_variants(sys, x0, tc.t_final, [policy_for(v) for v in spec.variants], cfg)
+        else:
+            runs = [engine.solve(sys, x0, tc.t_final, policy_for(v), cfg) for v in spec.variants]
+        double_steps = None
+        for v, r in zip(spec.variants, runs):
             if v == PolicyVariant.Double and r.total_steps() > 0:
                 double_steps = r.total_steps()
     finally:

@@ -227,6 +227,59 @@ def solve(sys: DeviceSystem, x0, t0: float, t_final: float, policy: PrecisionPol
     return _result(r, final, log, snaps)
 
 
+class DeviceVariants:
+    """Concurrent solves of one system under up to four policies (the
+    harness's variant set, harness.cpp:113-121) in lock-step on the device:
+    each stage of all variants is one K sweep when the model allows it, and
+    each variant's result is bit-identical to its own ``solve``."""
+
+    def __init__(self, sys: DeviceSystem, count: int):
+        self.sys, self.count = sys, int(count)
+        h = C.c_void_p()
+        _abi.check(_abi.lib().ms_variants_create(sys.handle, self.count, C.byref(h)), "ms_variants_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            _abi.lib().ms_variants_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def solve(self, x0, t0: float, t_final: float, policies, cfg: SolverConfig,
+              log_capacity: int | None = None) -> list:
+        if len(policies) != self.count:
+            raise ValueError(f"expected {self.count} policies")
+        x0 = _f64(x0)
+        finals = [np.empty_like(x0) for _ in policies]
+        logs = [_log_buffer(cfg, log_capacity) for _ in policies]
+        res = (_abi.SolveResultC * self.count)()
+        for r, fin, (log, cap) in zip(res, finals, logs):
+            r.final_state = _abi.dptr(fin)
+            if log is not None:
+                r.step_log = C.cast(log, C.POINTER(_abi.StepRecordC))
+                r.step_log_capacity = cap
+        pols = (_abi.Policy * self.count)(*[p.c() for p in policies])
+        cc = cfg.c()
+        _abi.check(_abi.lib().ms_variants_solve(self._h, _abi.dptr(x0), t0, t_final, pols, C.byref(cc), res),
+                   "ms_variants_solve")
+        return [_result(r, fin, log) for r, fin, (log, _) in zip(res, finals, logs)]
+
+
+def solve_variants(sys: DeviceSystem, x0, t0: float, t_final: float, policies, cfg: SolverConfig,
+                   log_capacity: int | None = None) -> list:
+    """One-shot DeviceVariants.solve."""
+    v = DeviceVariants(sys, len(policies))
+    try:
+        return v.solve(x0, t0, t_final, policies, cfg, log_capacity)
+    finally:
+        v.close()
+
+
 def solve_device(sys: DeviceSystem, x0_dev_ptr: int, final_dev_ptr: int, t0: float, t_final: float,
                  policy: PrecisionPolicy, cfg: SolverConfig, stream: int = 0,
                  log_capacity: int | None = 0) -> SolveResult:

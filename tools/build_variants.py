@@ -27,6 +27,15 @@ VARIANTS = {
     "tc2_n512_s4_e16": ("ms_batch.cu", {"MS_T2_EPI": 16}),
     "tc2_n512_s3_e16": ("ms_batch.cu", {"MS_T2_EPI": 16, "MS_T2_STAGES": 3}),
     "tc2_n256_s3x2_e16": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_EPI": 16}),
+    # concurrent-variant sweep (ms_multi.cuh): consumer warps x rows per warp
+    "multi_w8r4": ("ms_multi.cu", {}),
+    "multi_w16r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 16, "MS_MULTI_R": 2}),
+    "multi_w12r4": ("ms_multi.cu", {"MS_MULTI_WARPS": 12, "MS_MULTI_R": 4}),
+    "multi_w8r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 8, "MS_MULTI_R": 2}),
+    "multi_w16r2_i": ("ms_multi.cu", {"MS_MULTI_WARPS": 16, "MS_MULTI_R": 2, "MS_MULTI_INTCVT": 1}),
+    "multi_w12r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 12, "MS_MULTI_R": 2}),
+    "multi_w16r3": ("ms_multi.cu", {"MS_MULTI_WARPS": 16, "MS_MULTI_R": 3}),
+    "multi_w20r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 20, "MS_MULTI_R": 2}),
     "tc2_n256_s3x2_noepi": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_NOEPI": 1}),
 }
 
