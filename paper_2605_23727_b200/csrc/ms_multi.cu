@@ -1,5 +1,6 @@
 // ms_multi.cu — instantiations and launch of k_rhs_multi (ms_multi.cuh): one
-// kernel per (K storage, lane-type counts) with 2..4 lanes.
+// kernel per (K storage, lane-type counts) with 1..4 lanes (one lane: the
+// 2D-TMA-tiled single-system split sweep, MS_SWEEP=tile).
 #include <cudaTypedefs.h>
 
 #include <map>
@@ -57,19 +58,20 @@ void go(const CUtensorMap& tm, const MultiArgs& m, int grid, cudaStream_t st) {
   auto kern = k_rhs_multi<KS, NS, NDS, NDD>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MultiGeom<KS>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)MultiGeom<KS, NS + NDS + NDD>::SMEM);
     if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_multi attribute: ") + cudaGetErrorString(e));
     attr_done = true;
   }
-  kern<<<grid, kMultiThreads, MultiGeom<KS>::SMEM, st>>>(tm, m);
+  kern<<<grid, kMultiThreads, MultiGeom<KS, NS + NDS + NDD>::SMEM, st>>>(tm, m);
 }
 
 template <int KS, int NS, int NDS>
 void by_dd(int ndd, const CUtensorMap& tm, const MultiArgs& m, int grid, cudaStream_t st) {
   constexpr int left = kMaxLanes - NS - NDS;
   switch (ndd) {
-    case 0: if constexpr (NS + NDS >= 2) { go<KS, NS, NDS, 0>(tm, m, grid, st); return; } break;
-    case 1: if constexpr (left >= 1 && NS + NDS >= 1) { go<KS, NS, NDS, 1>(tm, m, grid, st); return; } break;
+    case 0: if constexpr (NS + NDS >= 1) { go<KS, NS, NDS, 0>(tm, m, grid, st); return; } break;
+    case 1: if constexpr (left >= 1) { go<KS, NS, NDS, 1>(tm, m, grid, st); return; } break;
     case 2: if constexpr (left >= 2) { go<KS, NS, NDS, 2>(tm, m, grid, st); return; } break;
     case 3: if constexpr (left >= 3) { go<KS, NS, NDS, 3>(tm, m, grid, st); return; } break;
     case 4: if constexpr (left >= 4) { go<KS, NS, NDS, 4>(tm, m, grid, st); return; } break;
@@ -106,7 +108,7 @@ void by_s(int ns, int nds, int ndd, const CUtensorMap& tm, const MultiArgs& m, i
 }  // namespace
 
 void launch_rhs_multi(const MultiArgs& m, int ns, int nds, int ndd, int ks, const void* K, int sms, cudaStream_t st) {
-  if (ns + nds + ndd != m.nl || m.nl < 2 || m.nl > kMaxLanes) throw std::invalid_argument("rhs_multi: lane count");
+  if (ns + nds + ndd != m.nl || m.nl < 1 || m.nl > kMaxLanes) throw std::invalid_argument("rhs_multi: lane count");
   const int rows = m.row1 - m.row0;
   const CUtensorMap& tm = k_map(K, m.ld, rows, ks);
   const int groups = (rows + kMultiTR - 1) / kMultiTR;

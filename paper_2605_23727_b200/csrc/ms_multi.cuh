@@ -62,14 +62,14 @@ constexpr int kMultiR = MS_MULTI_R;              // rows per consumer warp
 constexpr int kMultiTR = kMultiWarps * kMultiR;  // rows per group / K tile
 constexpr int kMultiThreads = (kMultiWarps + 1) * 32;
 
-template <int KS>
+template <int KS, int NL = kMaxLanes>
 struct MultiGeom {
   using KT = typename KElem<KS>::T;
   static constexpr int VEC = KVec<KS>::N;
   static constexpr int TC = 32 * VEC;                          // tile columns = one warp step
   static constexpr int KTILE = kMultiTR * TC * (int)sizeof(KT);  // 16 KB
   static constexpr int LANEB = 2 * TC * 8;                     // s + c at the widest GS
-  static constexpr int STAGE = KTILE + kMaxLanes * LANEB;
+  static constexpr int STAGE = KTILE + NL * LANEB;
   // ring depth: the largest power of two (cheap modulo) that fits
   static constexpr int NS = (8 * STAGE <= 200 * 1024) ? 8 : (4 * STAGE <= 200 * 1024 ? 4 : 2);
   static constexpr size_t SMEM = (size_t)NS * STAGE + 2 * NS * sizeof(uint64_t) + 128;
@@ -111,7 +111,7 @@ __device__ __forceinline__ void multi_tile(const unsigned char* sk, int warp, in
                                            const bool (&act)[NS + NDS + NDD],
                                            float (&AS)[NS > 0 ? NS : 1][kMultiR][2],
                                            double (&AD)[NDS + NDD > 0 ? NDS + NDD : 1][kMultiR][2]) {
-  using G = MultiGeom<KS>;
+  using G = MultiGeom<KS, NS + NDS + NDD>;
   constexpr int VEC = G::VEC, TC = G::TC, R = kMultiR;
   // this lane's K vectors of the warp's rows, then one lane type at a time
   float kf[R][VEC];
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
     k_rhs_multi(const __grid_constant__ CUtensorMap tmK, MultiArgs a) {
   constexpr int NL = NS + NDS + NDD;
   static_assert(NL >= 1 && NL <= kMaxLanes, "lane count");
-  using G = MultiGeom<KS>;
+  using G = MultiGeom<KS, NL>;
   constexpr int VEC = G::VEC, TC = G::TC, R = kMultiR;
   bool act[NL];
   bool any = false;

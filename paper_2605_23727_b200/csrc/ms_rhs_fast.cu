@@ -6,16 +6,47 @@
 #include <string>
 
 #include "ms_dispatch.h"
+#include "ms_multi.cuh"
 
 namespace msb {
 
 namespace {
 
 // K sweep selection for the split Kuramoto: MS_SWEEP=ldg keeps the
-// register-fed sweep, anything else (default) the TMA-fed one
+// register-fed sweep, MS_SWEEP=tile the 2D-tensor-tiled one-lane k_rhs_multi,
+// anything else (default) the row-copy TMA sweep for f32 K
 bool use_tma_sweep() {
   const char* v = std::getenv("MS_SWEEP");
   return !(v && std::strcmp(v, "ldg") == 0);
+}
+bool use_tile_sweep(int ks) {
+  const char* v = std::getenv("MS_SWEEP");
+  (void)ks;
+  return v && std::strcmp(v, "tile") == 0;
+}
+
+template <class SS, class GS, int KS>
+void go_tile(const RhsLaunch& L, const RhsArgs& a) {
+  MultiArgs m{};
+  m.nl = 1;
+  m.l = a.l;
+  m.gate = a.gate;
+  m.S = a.S;
+  m.out_slot = a.out_slot;
+  m.ld = a.ld;
+  m.n = a.n;
+  m.row0 = a.row0;
+  m.row1 = a.row1;
+  m.mw = a.mw;
+  LaneArgs& ln = m.lane[0];
+  ln.ctl = a.ctl;
+  ln.nf_mask = a.nf_mask;
+  ln.gin = a.gin;
+  ln.fvc = a.fvc;
+  for (int i = 0; i < kMaxStages + 1; ++i) ln.kb[i] = a.kb[i];
+  ln.ws32 = a.ws32;
+  const bool ss64 = sizeof(SS) == 8, gs64 = sizeof(GS) == 8;
+  launch_rhs_multi(m, !ss64 ? 1 : 0, ss64 && !gs64 ? 1 : 0, ss64 && gs64 ? 1 : 0, KS, a.K, L.num_sms, L.stream);
 }
 
 template <class SS, class GS, int KS>
@@ -38,6 +69,12 @@ void go(const RhsLaunch& L, const RhsArgs& a) {
   // the TMA-fed sweep wins for f32 K (7.2 vs 6.5 TB/s); with 16-bit K its
   // row copies get small and the s/c traffic per K byte doubles, and the
   // register-fed sweep stays ahead (profiles/r1_tune_tma.txt)
+  if constexpr (MODEL == MD_KUR && SPLIT && KS != MS_K_SCALAR && !(sizeof(SS) == 4 && sizeof(GS) == 8)) {
+    if (use_tile_sweep(KS)) {
+      go_tile<SS, GS, KS>(L, a);
+      return;
+    }
+  }
   if constexpr (MODEL == MD_KUR && SPLIT && KS == MS_K_F32) {
     if (use_tma_sweep()) {
       go_tma<SS, GS, KS>(L, a);

@@ -173,3 +173,25 @@ def test_tma_sweep_bitwise_equals_register_sweep(gpu, k_storage, n, sp, monkeypa
     part = DeviceSystem(spec)
     c = part.eval_rhs(0.0, x, sp)
     assert np.array_equal(c[3:n - 5], b[3:n - 5])
+
+
+@pytest.mark.parametrize("k_storage", ["f32", "f16", "bf16"])
+@pytest.mark.parametrize("n", [1000, 4096])
+@pytest.mark.parametrize("sp", [StagePrecision(B32, B32, B32), StagePrecision(B64, B64, B32),
+                                StagePrecision(B64, B64, B64)], ids=str)
+def test_tile_sweep_bitwise_equals_register_sweep(gpu, k_storage, n, sp, monkeypatch):
+    """The 2D-tensor-tiled sweep (one-lane k_rhs_multi, MS_SWEEP=tile) keeps the
+    lanes' column order: rows agree bit for bit with the register sweep, also
+    on a row-sharded handle."""
+    spec = kur_spec(n, k_storage, "fast", coupling_k=1.0)
+    dev = DeviceSystem(spec)
+    x = rng_uniform(7, 1, n, 0.0, 50.0)
+    monkeypatch.setenv("MS_SWEEP", "ldg")
+    a = dev.eval_rhs(0.0, x, sp)
+    monkeypatch.setenv("MS_SWEEP", "tile")
+    b = dev.eval_rhs(0.0, x, sp)
+    assert np.array_equal(a, b)
+    spec.row_begin, spec.row_end = 5, n - 3
+    part = DeviceSystem(spec)
+    c = part.eval_rhs(0.0, x, sp)
+    assert np.array_equal(c[5:n - 3], b[5:n - 3])

@@ -36,6 +36,8 @@ VARIANTS = {
     "multi_w12r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 12, "MS_MULTI_R": 2}),
     "multi_w16r3": ("ms_multi.cu", {"MS_MULTI_WARPS": 16, "MS_MULTI_R": 3}),
     "multi_w20r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 20, "MS_MULTI_R": 2}),
+    "multi_w16r4": ("ms_multi.cu", {"MS_MULTI_WARPS": 16, "MS_MULTI_R": 4}),
+    "multi_w24r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 24, "MS_MULTI_R": 2}),
     "tc2_n256_s3x2_noepi": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_NOEPI": 1}),
 }
 

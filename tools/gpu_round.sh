@@ -1,5 +1,6 @@
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_variants.py tests/test_gpu_harness.py -q -x --timeout 800 -p no:cacheprovider > gpurun_out/pytest_var.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_var.log
-timeout 900 python tools/bench_variants.py --c4-tf 5.0 > gpurun_out/bench_variants.log 2>&1
-echo done >> gpurun_out/bench_variants.log
+timeout 2400 python -m pytest tests -m gpu -q --timeout 1200 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo rc=$? >> gpurun_out/bench.log
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo rc=$? >> gpurun_out/bench_ref.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo rc=$? >> gpurun_out/smoke.log
