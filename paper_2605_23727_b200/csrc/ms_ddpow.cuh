@@ -95,13 +95,51 @@ MS_HD inline dd dd_log(double x) {
   t = dd_add(t, dd{-1.0, 0.0});       // - 1
   return dd_add(dd{y0, 0.0}, t);      // one Newton step
 }
-MS_HD inline double pow_cr(double x, double y) {
+// general path: exp(y log x) in double-double (two dd_exp: ~1200 dependent ops)
+MS_HD inline double pow_cr_general(double x, double y) {
   if (!(x > 0.0) || !isfinite(x) || !isfinite(y)) return pow(x, y);
   if (y == 0.0 || x == 1.0) return 1.0;
   const dd l = dd_log(x);
   const dd r = dd_exp(dd_mul_d(l, y));
   const double v = msb_add(r.hi, r.lo);
   return isfinite(v) ? v : pow(x, y);
+}
+
+// y = RN(1/q), the controller's exponents (1/3 step control, 1/4 initial_step,
+// 1/5 and 1/6 for DP5(4)): x^(1/q) in double-double by one Newton step from
+// the libm estimate (error ~q*eps^2), times x^(y - 1/q) = 1 + (y - 1/q) ln x
+// (|y - 1/q| < 2^-54, so that factor needs ln x to a few bits only), rounded
+// once. ~60 operations instead of ~1200; tests/test_ddpow_host.py checks it
+// against the general path and against exact decimal arithmetic.
+MS_HD inline bool pow_root(double x, double y, double* out) {
+  int q = 0;
+  for (int k = 2; k <= 8; ++k)
+    if (y == msb_div(1.0, (double)k)) q = k;
+  if (q == 0 || !(x > 1e-290 && x < 1e290)) return false;
+  const double r0 = pow(x, y);
+  if (!(r0 > 0.0) || !isfinite(r0)) return false;
+  dd p{r0, 0.0};
+  for (int i = 1; i < q; ++i) p = dd_mul_d(p, r0);  // r0^q
+  const dd diff = dd_add(p, dd{-x, 0.0});            // r0^q - x
+  double der = (double)q;
+  for (int i = 1; i < q; ++i) der = msb_mul(der, r0);  // q r0^(q-1)
+  const double corr = msb_div(msb_add(diff.hi, diff.lo), der);
+  dd r = dd_two_sum(r0, -corr);                         // x^(1/q) to ~100 bits
+  // y - 1/q = -(residual of RN(1/q)): 1/q = yq + res exactly to 2^-106
+  const double res = msb_div(fma(-y, (double)q, 1.0), (double)q);
+  const double t = msb_mul(msb_mul(r.hi, -res), log(x));  // r * (y - 1/q) ln x
+  const double v = msb_add(r.hi, msb_add(r.lo, t));
+  if (!isfinite(v)) return false;
+  *out = v;
+  return true;
+}
+
+MS_HD inline double pow_cr(double x, double y) {
+  if (!(x > 0.0) || !isfinite(x) || !isfinite(y)) return pow(x, y);
+  if (y == 0.0 || x == 1.0) return 1.0;
+  double v;
+  if (pow_root(x, y, &v)) return v;
+  return pow_cr_general(x, y);
 }
 
 }  // namespace msb
