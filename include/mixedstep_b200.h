@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define MS_ABI_VERSION 2
+#define MS_ABI_VERSION 3
 
 /* ---- return codes ---------------------------------------------------- */
 #define MS_OK 0
@@ -191,6 +191,15 @@ typedef struct {
   double* snapshot_h;          /* [snapshot_capacity] step sizes */
   int64_t snapshot_capacity;   /* in */
   int64_t snapshot_count;      /* out: accepted steps (may exceed capacity) */
+  /* Dense output (D6 extension; the reference has none): the cubic
+   * Hermite interpolant of each accepted step from (x_n, k1) to (x_{n+1}, k_last)
+   * at the sorted output times t_eval[n_eval] in [t0, t_final]; y_eval is a host
+   * buffer of n_eval x dN doubles. Times <= t0 get the starting state. NULL =
+   * none. n_eval_done: rows written (< n_eval if the solve stopped early). */
+  const double* t_eval;
+  int64_t n_eval;
+  double* y_eval;
+  int64_t n_eval_done;
 } ms_solve_result;
 
 /* StepOutcome, solver.hpp:75-86 (vectors are caller buffers of length dN) */

@@ -120,6 +120,7 @@ struct SolveResult {
   std::int64_t n_accepted = 0, n_failed = 0;
   std::vector<StepRecord> step_log;
   std::vector<StepSnapshot> snapshots;
+  std::vector<Vector> y_eval;  // dense output (D6 extension): one row per reached t_eval
   FlopTally flops;
   double device_ms = 0.0;
   std::int64_t total_steps() const { return n_accepted + n_failed; }
@@ -209,7 +210,7 @@ inline StepOutcome bs32_step(const System& sys, double t, const Vector& x_n, dou
 
 namespace detail {
 template <class F>
-SolveResult run(F&& call, std::size_t dn, const SolverConfig& cfg) {
+SolveResult run(F&& call, std::size_t dn, const SolverConfig& cfg, const std::vector<double>* t_eval = nullptr) {
   SolveResult out;
   out.final_state.resize(dn);
   std::vector<ms_step_record> log(cfg.record_step_log ? static_cast<std::size_t>(cfg.max_iterations) : 0);
@@ -229,6 +230,12 @@ SolveResult run(F&& call, std::size_t dn, const SolverConfig& cfg) {
     r.snapshot_h = hs.data();
     r.snapshot_capacity = scap;
   }
+  std::vector<double> dense(t_eval ? t_eval->size() * dn : 0);
+  if (t_eval && !t_eval->empty()) {
+    r.t_eval = t_eval->data();
+    r.n_eval = static_cast<int64_t>(t_eval->size());
+    r.y_eval = dense.data();
+  }
   call(r);
   out.status = static_cast<SolveStatus>(r.status);
   out.t_reached = r.t_reached;
@@ -239,6 +246,8 @@ SolveResult run(F&& call, std::size_t dn, const SolverConfig& cfg) {
   const int64_t m = r.step_log_count < r.step_log_capacity ? r.step_log_count : r.step_log_capacity;
   for (int64_t i = 0; i < m; ++i)
     out.step_log.push_back({log[i].t, log[i].h, log[i].err, log[i].accepted != 0});
+  for (int64_t q = 0; q < r.n_eval_done; ++q)
+    out.y_eval.emplace_back(dense.begin() + q * dn, dense.begin() + (q + 1) * dn);
   const int64_t ns = std::min<int64_t>(scap, r.snapshot_count);
   for (int64_t k = 0; k < ns; ++k) {
     const double* b = rows.data() + static_cast<std::size_t>(k) * dn;
@@ -255,6 +264,16 @@ inline SolveResult solve(const System& sys, const Vector& x0, double t0, double 
   return detail::run([&](ms_solve_result& r) {
     check(ms_solve(sys.handle(), x0.data(), t0, t_final, &p, &c, &r), "solve");
   }, x0.size(), cfg);
+}
+
+// solve with dense output at the sorted times t_eval in [t0, t_final] (D6 extension)
+inline SolveResult solve(const System& sys, const Vector& x0, double t0, double t_final, const PrecisionPolicy& policy,
+                         const SolverConfig& cfg, const std::vector<double>& t_eval) {
+  const ms_policy p = policy.c();
+  const ms_solver_config c = cfg.c();
+  return detail::run([&](ms_solve_result& r) {
+    check(ms_solve(sys.handle(), x0.data(), t0, t_final, &p, &c, &r), "solve");
+  }, x0.size(), cfg, &t_eval);
 }
 
 inline SolveResult dp54_reference(const System& sys, const Vector& x0, double t0, double t_final,

@@ -558,6 +558,22 @@ void validate(const SolverConfig& cfg, double t0, double t_final) {  // solver.c
   if (!(t_final > t0)) throw std::invalid_argument("solver: need t_final > t0");
 }
 
+// Dense output (D6 extension): cubic Hermite of an accepted step from (x_n, k1)
+// to (x_{n+1}, k_last), in the device kernel's operation order (k_dense).
+double hermite(double th, double h, double xn, double k1, double xn1, double k4) {
+  const double om = 1.0 - th;
+  const double om2 = om * om;
+  const double th2 = th * th;
+  const double h00 = (1.0 + 2.0 * th) * om2;
+  const double h10 = th * om2;
+  const double h01 = th2 * (3.0 - 2.0 * th);
+  const double h11 = th2 * (th - 1.0);
+  double v = h00 * xn;
+  v = v + h10 * (h * k1);
+  v = v + h01 * xn1;
+  return v + h11 * (h * k4);
+}
+
 // solve_core, solver.cpp:226-347
 SolveResult solve_core(const CoupledSystem& sys, const ButcherTableau& tab,
                        const std::vector<StagePrecision>& rows, const StagePrecision& k1_row,
@@ -585,6 +601,11 @@ SolveResult solve_core(const CoupledSystem& sys, const ButcherTableau& tab,
   double t = t0;
   Vec x = x0;
   store(x);
+  std::size_t next_eval = 0;
+  while (next_eval < cfg.t_eval.size() && cfg.t_eval[next_eval] <= t0) {
+    res.y_eval.push_back(x);
+    ++next_eval;
+  }
   Vec k1 = sys.eval_rhs(t0, x, k1_row);
   tally_eval(&res.flops, sys, k1_row);
   if (!all_finite(k1)) {
@@ -636,10 +657,18 @@ SolveResult solve_core(const CoupledSystem& sys, const ButcherTableau& tab,
     if (o.accepted) {
       ++res.n_accepted;
       Vec x_prev;
-      if (cfg.record_snapshots) x_prev = x;
+      if (cfg.record_snapshots || !cfg.t_eval.empty()) x_prev = x;
       x = std::move(o.x_store);
-      if (cfg.record_snapshots) res.snapshots.push_back({std::move(x_prev), x, h_att});
+      const double t_prev = t;
       t = last ? t_final : (round_state ? round_to(t + h_att, FloatFormat::Binary32) : t + h_att);
+      while (next_eval < cfg.t_eval.size() && cfg.t_eval[next_eval] <= t) {
+        const double th = (cfg.t_eval[next_eval] - t_prev) / h_att;
+        Vec y(x.size());
+        for (std::size_t e = 0; e < x.size(); ++e) y[e] = hermite(th, h_att, x_prev[e], k1[e], x[e], o.k4[e]);
+        res.y_eval.push_back(std::move(y));
+        ++next_eval;
+      }
+      if (cfg.record_snapshots) res.snapshots.push_back({std::move(x_prev), x, h_att});
       k1 = std::move(o.k4);
       h = o.h_next;
       if (t >= t_final) {

@@ -234,6 +234,7 @@ struct SolverConfig {  // solver.hpp:39-61
   double controller_exponent = 1.0 / 3.0;
   bool record_step_log = true;
   bool record_snapshots = false;
+  std::vector<double> t_eval;  // dense output times (D6 extension, not in the reference)
 };
 
 enum class SolveStatus : std::uint8_t {  // solver.hpp:63-71
@@ -259,6 +260,7 @@ struct SolveResult {  // solver.hpp:115-126
   std::int64_t n_accepted = 0, n_failed = 0;
   std::vector<StepRecord> step_log;
   std::vector<StepSnapshot> snapshots;
+  std::vector<Vec> y_eval;  // dense output rows, one per t_eval reached
   FlopTally flops;
   std::int64_t total_steps() const { return n_accepted + n_failed; }
 };

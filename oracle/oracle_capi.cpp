@@ -118,6 +118,10 @@ void fill_result(const SolveResult& r, int dn, ms_solve_result* out) {
   out->device_ms = 0.0;
   // StepSnapshots in the C-ABI layout: row 0 = x_before of the first, row k+1
   // = x_after of snapshot k (consecutive snapshots chain, solver.cpp:324-327)
+  out->n_eval_done = static_cast<int64_t>(r.y_eval.size());
+  if (out->y_eval)
+    for (std::size_t q = 0; q < r.y_eval.size() && static_cast<int64_t>(q) < out->n_eval; ++q)
+      std::memcpy(out->y_eval + q * static_cast<size_t>(dn), r.y_eval[q].data(), sizeof(double) * static_cast<size_t>(dn));
   out->snapshot_count = static_cast<int64_t>(r.snapshots.size());
   if (out->snapshots && out->snapshot_h && !r.snapshots.empty()) {
     const int64_t m = std::min<int64_t>(out->snapshot_capacity, out->snapshot_count);
@@ -387,7 +391,9 @@ int orc_solve(void* h, const double* x0, double t0, double tf, const ms_policy* 
   return guard([&] {
     auto* s = static_cast<OrcSystem*>(h);
     const size_t dn = s->sys->size();
-    const SolveResult r = solve(*s->sys, Vec(x0, x0 + dn), t0, tf, policy_of(*pol), cfg_of(*cfg));
+    SolverConfig c = cfg_of(*cfg);
+    if (res->t_eval && res->n_eval > 0) c.t_eval.assign(res->t_eval, res->t_eval + res->n_eval);
+    const SolveResult r = solve(*s->sys, Vec(x0, x0 + dn), t0, tf, policy_of(*pol), c);
     fill_result(r, static_cast<int>(dn), res);
   });
 }

@@ -76,6 +76,7 @@ class SolveResultC(C.Structure):
         ("final_state", _DP), ("step_log", C.POINTER(StepRecordC)),
         ("step_log_capacity", C.c_int64), ("step_log_count", C.c_int64), ("device_ms", C.c_double),
         ("snapshots", _DP), ("snapshot_h", _DP), ("snapshot_capacity", C.c_int64), ("snapshot_count", C.c_int64),
+        ("t_eval", _DP), ("n_eval", C.c_int64), ("y_eval", _DP), ("n_eval_done", C.c_int64),
     ]
 
 
@@ -161,7 +162,7 @@ class CudaError(MixedstepError):
 _lib = None
 
 
-ABI_VERSION = 2  # MS_ABI_VERSION of include/mixedstep_b200.h
+ABI_VERSION = 3  # MS_ABI_VERSION of include/mixedstep_b200.h
 
 
 def lib() -> C.CDLL:

@@ -294,6 +294,10 @@ struct ms_system {
   double* snap = nullptr;
   double* snap_h = nullptr;
   int64_t snap_cap = -1;
+  // dense output: device copy of the output times, then n_eval x dN rows
+  double* dense = nullptr;
+  double* dense_t = nullptr;
+  int64_t dense_cap = -1;
   // host-driven (sharded) loop
   bool loop_active = false;
   SolvePlanStore* loop_plan = nullptr;
@@ -533,6 +537,7 @@ struct SolvePlan {
   int lowest;
   bool k1_elided;
   bool snaps;  // record StepSnapshots (k_snapshot after each finalize)
+  bool dense;  // dense output (k_dense after each finalize)
 };
 
 int snap_grid(const ms_system* s) {
@@ -558,6 +563,23 @@ void ensure_snapshots(ms_system* s, int64_t cap) {
   s->snap_cap = cap;
 }
 
+// dense-output rows for n output times (graphs capture the address: growing drops them)
+void ensure_dense(ms_system* s, int64_t n) {
+  if (n <= s->dense_cap) return;
+  CK(cudaStreamSynchronize(s->stream));
+  for (auto& kv : s->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.g) cudaGraphDestroy(kv.second.g);
+  }
+  s->graphs.clear();
+  if (s->dense) CK(cudaFree(s->dense));
+  s->dense = nullptr;
+  s->dense_cap = -1;
+  CK(cudaMalloc(&s->dense, sizeof(double) * ((size_t)n * (size_t)s->dn() + (size_t)n)));
+  s->dense_t = s->dense + (size_t)n * (size_t)s->dn();
+  s->dense_cap = n;
+}
+
 // one attempt: [k1 recompute] -> stages -> finalize
 void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_handle,
                     cudaGraphConditionalHandle h) {
@@ -580,6 +602,10 @@ void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_
   CK(cudaGetLastError());
   if (P.snaps) {
     k_snapshot<<<snap_grid(s), 256, 0, st>>>(s->B, s->snap, s->snap_h, s->snap_cap, s->dn(), 0);
+    CK(cudaGetLastError());
+  }
+  if (P.dense) {
+    k_dense<<<snap_grid(s), 256, 0, st>>>(s->B, T.S, s->dense, s->dn(), 0, 0);
     CK(cudaGetLastError());
   }
 }
@@ -658,8 +684,8 @@ void init_ctl(ms_system* s, Ctl& c, const ms_solver_config& cfg, double t0, doub
 
 std::string plan_key(const SolvePlan& P) {
   char buf[160];
-  int o = std::snprintf(buf, sizeof(buf), "S%d:st%d:el%d:sn%d:k1%d%d%d", P.T->S, P.storage, (int)P.k1_elided,
-                        (int)P.snaps,
+  int o = std::snprintf(buf, sizeof(buf), "S%d:st%d:el%d:sn%d:dn%d:k1%d%d%d", P.T->S, P.storage, (int)P.k1_elided,
+                        (int)P.snaps, (int)P.dense,
                         P.k1_row.f_prec, P.k1_row.sum_prec, P.k1_row.g_prec);
   for (int l = 0; l < P.T->S - 1; ++l)
     o += std::snprintf(buf + o, sizeof(buf) - o, ":%d%d%d", P.rows[l].f_prec, P.rows[l].sum_prec, P.rows[l].g_prec);
@@ -731,6 +757,17 @@ void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf
   SolvePlan P = P0;
   P.snaps = cfg.record_snapshots && res->snapshots && res->snapshot_h && res->snapshot_capacity >= 0;
   if (P.snaps) ensure_snapshots(s, std::max<int64_t>(res->snapshot_capacity, 1));
+  P.dense = res->t_eval && res->y_eval && res->n_eval > 0;
+  int64_t dense0 = 0;  // output times at or before t0
+  if (P.dense) {
+    for (int64_t q = 0; q < res->n_eval; ++q) {
+      const double tq = res->t_eval[q];
+      if (!(tq >= t0 && tq <= tf) || (q > 0 && tq < res->t_eval[q - 1]))
+        throw InvalidArg("solve: t_eval must be sorted within [t0, t_final]");
+      if (tq <= t0) dense0 = q + 1;
+    }
+    ensure_dense(s, res->n_eval);
+  }
   cudaStream_t st = s->stream;
   if (user_stream && user_stream != st) {
     // order the solve after the caller's prior work on its stream
@@ -743,6 +780,12 @@ void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf
   Ctl& c = *s->ctl_host;
   init_ctl(s, c, cfg, t0, tf, P, cap);
   const int64_t dn = s->dn();
+  if (P.dense) {
+    CK(cudaMemcpyAsync(s->dense_t, res->t_eval, sizeof(double) * res->n_eval, cudaMemcpyHostToDevice, st));
+    c.t_eval = s->dense_t;
+    c.n_eval = res->n_eval;
+    c.eval_next = dense0;
+  }
   CK(cudaMemcpyAsync(s->B.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(s->B.xb[0], x0, sizeof(double) * dn, x0_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                      st));
@@ -752,6 +795,10 @@ void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf
   launch_init(s, st, P, true);
   if (P.snaps) {
     k_snapshot<<<snap_grid(s), 256, 0, st>>>(s->B, s->snap, s->snap_h, s->snap_cap, dn, 1);
+    CK(cudaGetLastError());
+  }
+  if (P.dense && dense0 > 0) {
+    k_dense<<<snap_grid(s), 256, 0, st>>>(s->B, P.T->S, s->dense, dn, 1, dense0);
     CK(cudaGetLastError());
   }
   if (host_loop) {
@@ -788,6 +835,10 @@ void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf
       }
     }
   }
+  res->n_eval_done = P.dense ? c.eval_next : 0;
+  if (P.dense && c.eval_next > 0)
+    CK(cudaMemcpyAsync(res->y_eval, s->dense, sizeof(double) * (size_t)c.eval_next * (size_t)dn,
+                       out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   res->snapshot_count = P.snaps ? c.n_acc : 0;
   if (P.snaps) {
     const int64_t m = std::min<int64_t>(res->snapshot_capacity, c.n_acc);
@@ -1244,6 +1295,7 @@ void run_variants(ms_variants* v, const double* x0, double t0, double tf, const 
   int64_t cap = 1;
   for (int l = 0; l < v->nl; ++l) {
     check_policy(pols[l]);
+    if (res[l].t_eval && res[l].n_eval > 0) throw InvalidArg("variants: dense output is produced by ms_solve only");
     P[l] = plan_bs32(pols[l]);
     if (cfg.record_step_log && res[l].step_log) cap = std::max<int64_t>(cap, res[l].step_log_capacity);
   }
@@ -1535,6 +1587,7 @@ int ms_system_destroy(ms_system_t s) {
     if (s->K) cudaFree(s->K);
     if (s->ws_mem) cudaFree(s->ws_mem);
     if (s->snap) cudaFree(s->snap);
+    if (s->dense) cudaFree(s->dense);
     if (s->ctl_host) cudaFreeHost(s->ctl_host);
     delete s->loop_plan;
     if (s->ev0) cudaEventDestroy(s->ev0);

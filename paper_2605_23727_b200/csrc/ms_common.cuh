@@ -118,6 +118,11 @@ struct Ctl {
   int32_t snap_pending;   // this attempt was accepted: k_snapshot copies x
   int32_t _pad;
   double snap_hv;         // h of the accepted attempt (h_att before loop_check moves on)
+  // dense output (D6 extension): sorted output times, the next unfilled one,
+  // and the range [dense_lo, dense_hi) the accepted attempt covers
+  const double* t_eval;
+  int64_t n_eval, eval_next, dense_lo, dense_hi;
+  double t_prev;          // t at the start of the accepted attempt
 };
 
 struct StepLogRec {

@@ -922,6 +922,8 @@ __device__ inline bool attempt_controller(Ctl* c, int S, int mode, int k1_elided
   c->nf_mask = 0;
   c->snap_pending = (accepted && c->snap_on) ? 1 : 0;
   if (accepted) c->snap_hv = h;
+  c->dense_lo = c->dense_hi = c->eval_next;
+  if (accepted) c->t_prev = c->t;
   if (accepted) {  // solver.cpp:321-336
     c->n_acc += 1;
     c->ix ^= 1;
@@ -933,6 +935,11 @@ __device__ inline bool attempt_controller(Ctl* c, int S, int mode, int k1_elided
       c->status = MS_COMPLETED;
       c->done = 1;
     }
+    // output times inside the accepted step (t_prev, t]
+    int64_t e = c->eval_next;
+    while (e < c->n_eval && c->t_eval[e] <= c->t) ++e;
+    c->dense_hi = e;
+    c->eval_next = e;
   } else {  // solver.cpp:337-341
     c->n_fail += 1;
     c->h = h_next;
@@ -1031,6 +1038,53 @@ __global__ void __launch_bounds__(256) k_snapshot(Bufs B, double* snap, double* 
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dn; e += (int64_t)gridDim.x * blockDim.x)
     dst[e] = x[e];
   if (!row0 && blockIdx.x == 0 && threadIdx.x == 0) snap_h[row - 1] = c->snap_hv;
+}
+
+// Dense output (D6 extension): the cubic Hermite interpolant of
+// an accepted step from (x_n, k1 = f(x_n)) to (x_{n+1}, k_last = f(x_{n+1})),
+//   th = (tau - t_n) / h,  x(tau) = h00 x_n + h10 h k1 + h01 x_{n+1} + h11 h k_last
+// with h00 = (1 + 2 th)(1 - th)^2, h10 = th (1 - th)^2, h01 = th^2 (3 - 2 th),
+// h11 = th^2 (th - 1), evaluated in binary64 in exactly this order (the oracle's
+// dense_eval restates it). After the swap on accept, x_{n+1} = xb[ix] and
+// k_last = kb[k1i]; with row0 = 1 it writes the starting state to the output
+// times <= t0 (before any step).
+__device__ __forceinline__ double hermite(double th, double h, double xn, double k1, double xn1, double k4) {
+  const double om = __dsub_rn(1.0, th);
+  const double om2 = __dmul_rn(om, om);
+  const double th2 = __dmul_rn(th, th);
+  const double h00 = __dmul_rn(__dadd_rn(1.0, __dmul_rn(2.0, th)), om2);
+  const double h10 = __dmul_rn(th, om2);
+  const double h01 = __dmul_rn(th2, __dsub_rn(3.0, __dmul_rn(2.0, th)));
+  const double h11 = __dmul_rn(th2, __dsub_rn(th, 1.0));
+  double v = __dmul_rn(h00, xn);
+  v = __dadd_rn(v, __dmul_rn(h10, __dmul_rn(h, k1)));
+  v = __dadd_rn(v, __dmul_rn(h01, xn1));
+  return __dadd_rn(v, __dmul_rn(h11, __dmul_rn(h, k4)));
+}
+
+__global__ void __launch_bounds__(256) k_dense(Bufs B, int S, double* y, int64_t dn, int row0, int64_t row0_count) {
+  const Ctl* c = B.ctl;
+  int64_t lo, hi;
+  if (row0) {
+    lo = 0;
+    hi = row0_count;
+  } else {
+    if (!c->accepted) return;
+    lo = c->dense_lo;
+    hi = c->dense_hi;
+  }
+  if (lo >= hi) return;
+  const double* xn1 = B.xb[c->ix];
+  const double* xn = B.xb[c->ix ^ 1];
+  const double* k4 = B.kb[c->k1i];
+  const double* k1 = B.kb[S - c->k1i];
+  const double h = c->snap_hv, t0 = c->t_prev;
+  for (int64_t q = lo; q < hi; ++q) {
+    double* dst = y + q * dn;
+    const double th = row0 ? 0.0 : __ddiv_rn(__dsub_rn(c->t_eval[q], t0), h);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dn; e += (int64_t)gridDim.x * blockDim.x)
+      dst[e] = row0 ? xn1[e] : hermite(th, h, xn[e], k1[e], xn1[e], k4[e]);
+  }
 }
 
 // ------------------------------------------------------------------------------

@@ -100,6 +100,7 @@ class SolveResult:  # solver.hpp:115-126
     step_log_count: int = 0
     snapshots: list = field(default_factory=list)
     snapshot_count: int = 0
+    y_eval: np.ndarray | None = None  # dense output rows (D6 extension), one per t_eval
 
     def total_steps(self) -> int:
         return self.n_accepted + self.n_failed
@@ -205,15 +206,24 @@ def _log_buffer(cfg: SolverConfig, capacity: int | None):
 
 
 def solve(sys: DeviceSystem, x0, t0: float, t_final: float, policy: PrecisionPolicy, cfg: SolverConfig,
-          log_capacity: int | None = None, snapshot_capacity: int | None = None) -> SolveResult:
+          log_capacity: int | None = None, snapshot_capacity: int | None = None, t_eval=None) -> SolveResult:
     """Adaptive BS3(2) solve (solver.cpp:462-470); the step loop runs on the device.
     With ``cfg.record_snapshots`` the device copies the state after every
-    accepted step (solver.cpp:324-327) into ``result.snapshots``."""
+    accepted step (solver.cpp:324-327) into ``result.snapshots``. ``t_eval``
+    (sorted, within [t0, t_final]) asks for dense output: the cubic Hermite
+    interpolant of the accepted steps at those times, ``result.y_eval``
+    (rows beyond a premature stop are NaN)."""
     x0 = _f64(x0)
     final = np.empty_like(x0)
     log, cap = _log_buffer(cfg, log_capacity)
     snaps = _snapshot_buffers(cfg, x0.size, snapshot_capacity)
+    te = ye = None
+    if t_eval is not None:
+        te = _f64(t_eval).ravel()
+        ye = np.full((te.size, x0.size), np.nan)
     r = _abi.SolveResultC()
+    if te is not None and te.size:
+        r.t_eval, r.n_eval, r.y_eval = _abi.dptr(te), te.size, _abi.dptr(ye)
     r.final_state = _abi.dptr(final)
     if log is not None:
         r.step_log = C.cast(log, C.POINTER(_abi.StepRecordC))
@@ -224,7 +234,9 @@ def solve(sys: DeviceSystem, x0, t0: float, t_final: float, policy: PrecisionPol
     pol, cc = policy.c(), cfg.c()
     _abi.check(_abi.lib().ms_solve(sys.handle, _abi.dptr(x0), t0, t_final, C.byref(pol), C.byref(cc),
                                    C.byref(r)), "ms_solve")
-    return _result(r, final, log, snaps)
+    out = _result(r, final, log, snaps)
+    out.y_eval = ye
+    return out
 
 
 class DeviceVariants:

@@ -218,7 +218,7 @@ def bs32_step(sys: OracleSystem, t, x_n, h, k1, policy: PrecisionPolicy, cfg: So
                        FlopTally(o.flops_low, o.flops_high, o.rhs_evals))
 
 
-def _run(fn, sys, x0, cap, snap_cap=0):
+def _run(fn, sys, x0, cap, snap_cap=0, t_eval=None):
     x0 = f64(x0)
     final = np.empty_like(x0)
     log = (_abi.StepRecordC * cap)()
@@ -231,22 +231,29 @@ def _run(fn, sys, x0, cap, snap_cap=0):
         rows, hs = np.empty((snap_cap + 1, x0.size)), np.empty(snap_cap)
         r.snapshots, r.snapshot_h = rows.ctypes.data_as(_DP), hs.ctypes.data_as(_DP)
         r.snapshot_capacity = snap_cap
+    te = ye = None
+    if t_eval is not None:
+        te = f64(t_eval).ravel()
+        ye = np.full((te.size, x0.size), np.nan)
+        r.t_eval, r.n_eval, r.y_eval = te.ctypes.data_as(_DP), te.size, ye.ctypes.data_as(_DP)
     check(fn(sys._h, x0.ctypes.data_as(_DP), r), "oracle solve")
     m = min(cap, r.step_log_count)
     steps = [StepRecord(e.t, e.h, e.err, bool(e.accepted)) for e in log[:m]]
     shots = []
     if snap_cap:
         shots = [StepSnapshot(rows[k], rows[k + 1], float(hs[k])) for k in range(min(snap_cap, r.snapshot_count))]
-    return SolveResult(SolveStatus(r.status), final, r.t_reached, r.n_accepted, r.n_failed, steps,
-                       FlopTally(r.flops_low, r.flops_high, r.rhs_evals), 0.0, r.step_log_count,
-                       shots, r.snapshot_count)
+    out = SolveResult(SolveStatus(r.status), final, r.t_reached, r.n_accepted, r.n_failed, steps,
+                      FlopTally(r.flops_low, r.flops_high, r.rhs_evals), 0.0, r.step_log_count,
+                      shots, r.snapshot_count)
+    out.y_eval = ye
+    return out
 
 
 def solve(sys: OracleSystem, x0, t0, tf, policy: PrecisionPolicy, cfg: SolverConfig, cap: int = 200000,
-          snapshot_capacity: int = 4096):
+          snapshot_capacity: int = 4096, t_eval=None):
     pol, cc = policy.c(), cfg.c()
     return _run(lambda h, x, r: lib().orc_solve(h, x, t0, tf, C.byref(pol), C.byref(cc), C.byref(r)),
-                sys, x0, cap, snapshot_capacity if cfg.record_snapshots else 0)
+                sys, x0, cap, snapshot_capacity if cfg.record_snapshots else 0, t_eval)
 
 
 def dp54_reference(sys: OracleSystem, x0, t0, tf, cfg: SolverConfig | None = None, cap: int = 200000):

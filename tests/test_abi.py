@@ -30,7 +30,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert not missing, missing
     bound = {name for name, _, _ in _abi.SIGNATURES}
     assert set(syms) == bound, set(syms) ^ bound
-    assert L.ms_abi_version() == 2
+    assert L.ms_abi_version() == 3
 
 
 def test_struct_layouts_match():
