@@ -251,11 +251,11 @@ __global__ void k_adjust_step(double h, double err, double rel, double safety, d
 template <int MODEL>
 void launch_prep_model(bool fs32, bool gs32, int grid, cudaStream_t st, const PrepArgs& p) {
   if (fs32) {
-    if (gs32) k_prep<MODEL, float, float><<<grid, 256, 0, st>>>(p);
-    else k_prep<MODEL, float, double><<<grid, 256, 0, st>>>(p);
+    if (gs32) CK(launch_k(k_prep<MODEL, float, float>, grid, 256, 0, st, p));
+    else CK(launch_k(k_prep<MODEL, float, double>, grid, 256, 0, st, p));
   } else {
-    if (gs32) k_prep<MODEL, double, float><<<grid, 256, 0, st>>>(p);
-    else k_prep<MODEL, double, double><<<grid, 256, 0, st>>>(p);
+    if (gs32) CK(launch_k(k_prep<MODEL, double, float>, grid, 256, 0, st, p));
+    else CK(launch_k(k_prep<MODEL, double, double>, grid, 256, 0, st, p));
   }
 }
 
@@ -598,14 +598,14 @@ void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_
   FinArgs f = fin_args(s, s->B, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
   f.has_handle = has_handle ? 1 : 0;
   f.handle = h;
-  k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
+  CK(launch_k(k_finalize, s->fin_blocks, kFinThreads, 0, st, f));
   CK(cudaGetLastError());
   if (P.snaps) {
-    k_snapshot<<<snap_grid(s), 256, 0, st>>>(s->B, s->snap, s->snap_h, s->snap_cap, s->dn(), 0);
+    CK(launch_k(k_snapshot, snap_grid(s), 256, 0, st, s->B, s->snap, s->snap_h, s->snap_cap, s->dn(), 0));
     CK(cudaGetLastError());
   }
   if (P.dense) {
-    k_dense<<<snap_grid(s), 256, 0, st>>>(s->B, T.S, s->dense, s->dn(), 0, 0);
+    CK(launch_k(k_dense, snap_grid(s), 256, 0, st, s->B, T.S, s->dense, s->dn(), 0, 0));
     CK(cudaGetLastError());
   }
 }
@@ -613,7 +613,7 @@ void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_
 // initial_step + cold k1 + loop head (solver.cpp:247-269)
 void launch_init(ms_system* s, cudaStream_t st, const SolvePlan& P, bool with_k1) {
   const Tableau& T = *P.T;
-  k_stamp_start<<<1, 1, 0, st>>>(s->B.ctl);
+  CK(launch_k(k_stamp_start, 1, 1, 0, st, s->B.ctl));
   EvalSpec f0;
   f0.S = T.S;
   f0.l = 7;
@@ -626,14 +626,14 @@ void launch_init(ms_system* s, cudaStream_t st, const SolvePlan& P, bool with_k1
   ia.x0 = s->B.xb[0];
   ia.dn = s->dn();
   ia.exponent = 1.0 / static_cast<double>(T.order_high + 1);
-  k_init_a<<<1, 1024, 0, st>>>(ia);
+  CK(launch_k(k_init_a, 1, 1024, 0, st, ia));
   CK(cudaGetLastError());
   EvalSpec f1 = f0;
   f1.kind = PREP_INIT_X1;
   f1.gate = GATE_INIT2;
   f1.out_slot = 2;
   launch_eval(s, st, f1, kDDD);
-  k_init_b<<<1, 1024, 0, st>>>(ia);
+  CK(launch_k(k_init_b, 1, 1024, 0, st, ia));
   CK(cudaGetLastError());
   if (!with_k1) return;
   EvalSpec k1;
@@ -644,7 +644,7 @@ void launch_init(ms_system* s, cudaStream_t st, const SolvePlan& P, bool with_k1
   k1.out_slot = SLOT_K1;
   k1.round_x = P.storage == MS_BINARY32 ? 1 : 0;
   launch_eval(s, st, k1, P.k1_row);
-  k_loop_head<<<1, 1, 0, st>>>(s->B.ctl);
+  CK(launch_k(k_loop_head, 1, 1, 0, st, s->B.ctl));
   CK(cudaGetLastError());
 }
 
@@ -794,11 +794,11 @@ void run_solve(ms_system* s, const double* x0, bool x0_dev, double t0, double tf
   CK(cudaEventRecord(s->ev0, st));
   launch_init(s, st, P, true);
   if (P.snaps) {
-    k_snapshot<<<snap_grid(s), 256, 0, st>>>(s->B, s->snap, s->snap_h, s->snap_cap, dn, 1);
+    CK(launch_k(k_snapshot, snap_grid(s), 256, 0, st, s->B, s->snap, s->snap_h, s->snap_cap, dn, 1));
     CK(cudaGetLastError());
   }
   if (P.dense && dense0 > 0) {
-    k_dense<<<snap_grid(s), 256, 0, st>>>(s->B, P.T->S, s->dense, dn, 1, dense0);
+    CK(launch_k(k_dense, snap_grid(s), 256, 0, st, s->B, P.T->S, s->dense, dn, 1, dense0));
     CK(cudaGetLastError());
   }
   if (host_loop) {
@@ -952,14 +952,14 @@ void loop_run(ms_system* s, const SolvePlan& P, int list, int index, cudaStream_
     f.count = CNT_DDD;
     switch (index) {
       case 0:
-        k_stamp_start<<<1, 1, 0, st>>>(s->B.ctl);
+        CK(launch_k(k_stamp_start, 1, 1, 0, st, s->B.ctl));
         f.out_slot = 1;
         launch_eval(s, st, f, kDDD);
         set_exch(s, ex, s->B.kb[1]);
         return;
       case 1:
         launch_scan(s, st, s->B.kb[1], 7);
-        k_init_a<<<1, 1024, 0, st>>>(ia);
+        CK(launch_k(k_init_a, 1, 1024, 0, st, ia));
         CK(cudaGetLastError());
         f.kind = PREP_INIT_X1;
         f.gate = GATE_INIT2;
@@ -968,7 +968,7 @@ void loop_run(ms_system* s, const SolvePlan& P, int list, int index, cudaStream_
         set_exch(s, ex, s->B.kb[2]);
         return;
       case 2: {
-        k_init_b<<<1, 1024, 0, st>>>(ia);
+        CK(launch_k(k_init_b, 1, 1024, 0, st, ia));
         CK(cudaGetLastError());
         EvalSpec k1;
         k1.S = S;
@@ -983,7 +983,7 @@ void loop_run(ms_system* s, const SolvePlan& P, int list, int index, cudaStream_
       }
       case 3:
         launch_scan(s, st, s->B.kb[0], 0);
-        k_loop_head<<<1, 1, 0, st>>>(s->B.ctl);
+        CK(launch_k(k_loop_head, 1, 1, 0, st, s->B.ctl));
         CK(cudaGetLastError());
         return;
       default: throw InvalidArg("loop: bad init segment");
@@ -1019,7 +1019,7 @@ void loop_run(ms_system* s, const SolvePlan& P, int list, int index, cudaStream_
   launch_scan(s, st, out_of(S - 1), S - 1);
   FinArgs f = fin_args(s, s->B, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
   f.fixed_k1 = 1;
-  k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
+  CK(launch_k(k_finalize, s->fin_blocks, kFinThreads, 0, st, f));
   CK(cudaGetLastError());
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((s->dn() + 255) / 256, 2 * s->sms));
   k_fsal_copy<<<grid, 256, 0, st>>>(s->B.ctl, s->B.kb[0], s->B.kb[S], s->dn());
@@ -1168,7 +1168,7 @@ void mlaunch_init(ms_variants* v, cudaStream_t st, const SolvePlan* P) {
   ms_stage_prec sp[kMaxLanes];
   for (int l = 0; l < nl; ++l) {
     on[l] = true;
-    k_stamp_start<<<1, 1, 0, st>>>(v->B[l].ctl);
+    CK(launch_k(k_stamp_start, 1, 1, 0, st, v->B[l].ctl));
     e[l].S = T.S;
     e[l].l = 7;
     e[l].kind = PREP_X;
@@ -1184,7 +1184,7 @@ void mlaunch_init(ms_variants* v, cudaStream_t st, const SolvePlan* P) {
     ia[l].x0 = v->B[l].xb[0];
     ia[l].dn = s->dn();
     ia[l].exponent = 1.0 / static_cast<double>(T.order_high + 1);
-    k_init_a<<<1, 1024, 0, st>>>(ia[l]);
+    CK(launch_k(k_init_a, 1, 1024, 0, st, ia[l]));
     CK(cudaGetLastError());
     e[l].kind = PREP_INIT_X1;
     e[l].gate = GATE_INIT2;
@@ -1192,7 +1192,7 @@ void mlaunch_init(ms_variants* v, cudaStream_t st, const SolvePlan* P) {
   }
   mlaunch_eval(v, st, e, sp, on);
   for (int l = 0; l < nl; ++l) {
-    k_init_b<<<1, 1024, 0, st>>>(ia[l]);
+    CK(launch_k(k_init_b, 1, 1024, 0, st, ia[l]));
     CK(cudaGetLastError());
     e[l] = EvalSpec{};
     e[l].S = T.S;
@@ -1204,7 +1204,7 @@ void mlaunch_init(ms_variants* v, cudaStream_t st, const SolvePlan* P) {
     sp[l] = P[l].k1_row;
   }
   mlaunch_eval(v, st, e, sp, on);
-  for (int l = 0; l < nl; ++l) k_loop_head<<<1, 1, 0, st>>>(v->B[l].ctl);
+  for (int l = 0; l < nl; ++l) CK(launch_k(k_loop_head, 1, 1, 0, st, v->B[l].ctl));
   CK(cudaGetLastError());
 }
 
@@ -1242,7 +1242,7 @@ void mlaunch_attempt(ms_variants* v, cudaStream_t st, const SolvePlan* P, bool h
   for (int l = 0; l < nl; ++l) {
     FinArgs f = fin_args(s, v->B[l], T, FIN_SOLVE, P[l].k1_elided ? 1 : 0);
     f.has_handle = 0;
-    k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
+    CK(launch_k(k_finalize, s->fin_blocks, kFinThreads, 0, st, f));
     CK(cudaGetLastError());
     lc.c[l] = v->B[l].ctl;
   }
@@ -1790,7 +1790,7 @@ int ms_bs32_step(ms_system_t s, double t, const double* x_n, double h, const dou
     CK(cudaMemcpyAsync(s->B.kb[0], k1, sizeof(double) * dn, cudaMemcpyHostToDevice, st));
     for (int l = 1; l < T.S; ++l) launch_eval(s, st, stage_spec(T, l), P.rows[l - 1]);
     FinArgs f = fin_args(s, s->B, T, FIN_STEP, 0);
-    k_finalize<<<s->fin_blocks, kFinThreads, 0, st>>>(f);
+    CK(launch_k(k_finalize, s->fin_blocks, kFinThreads, 0, st, f));
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&c, s->B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

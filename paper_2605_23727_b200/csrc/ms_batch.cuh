@@ -56,11 +56,16 @@ __device__ __forceinline__ double b_fval(const BatchDev& d, int64_t e, int fs32)
   return fs32 ? (double)__double2float_rn(w) : w;
 }
 
-// Per-element inputs of the tensor-core coupling epilogue, written by the prep
-// kernel into the `sc` buffer on that path: one 16-byte load per (b, i).
+// Per-element inputs of the tensor-core coupling epilogue: (s, c) of theta_bi
+// in binary32 (the row side, exact GS values), written by the prep kernel as
+// float2 pairs into the `sc` buffer on that path, and F = RN_FS(omega_bi),
+// which the epilogue reads from omega itself (it never changes).
+#ifndef MS_TC_PACKED
+#define MS_TC_PACKED 1  // 1: prep writes {s, c, F} records (one 16-byte load); 0: (s, c) pairs + omega
+#endif
 struct __align__(16) TcRec {
-  float s, c;  // sin, cos of theta_bi in binary32 (the row side, exact GS values)
-  double f;    // F = RN_FS(omega_bi)
+  float s, c;
+  double f;
 };
 
 struct BPrepArgs {
@@ -122,11 +127,15 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
   GS sv, cv;
   dsincos(xg, &sv, &cv);
   if (p.op_ks) {  // tensor-core path: the epilogue's record
+#if MS_TC_PACKED
     TcRec r;
     r.s = (float)sv;
     r.c = (float)cv;
     r.f = b_fval(d, e, p.fs32);
     reinterpret_cast<TcRec*>(d.sc)[e] = r;
+#else
+    reinterpret_cast<float2*>(d.sc)[e] = make_float2((float)sv, (float)cv);
+#endif
   } else {
     GS* sc = reinterpret_cast<GS*>(d.sc);
     sc[e] = sv;

@@ -75,6 +75,15 @@ template <class S> __device__ __forceinline__ S cvt(double x);
 template <> __device__ __forceinline__ float cvt<float>(double x) { return __double2float_rn(x); }
 template <> __device__ __forceinline__ double cvt<double>(double x) { return x; }
 
+// ---- programmatic dependent launch ---------------------------------------------
+// Every kernel of the attempt chain waits for its predecessor grid here (a no-op
+// when launched without the PDL attribute) and at once lets its successor be
+// scheduled, so a kernel's launch and prologue overlap the previous one's tail.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- coupling storage --------------------------------------------------------
 struct KScalar {};  // no matrix: G uses RN_S(coupling_k)
 template <int KS> struct KElem;

@@ -1,5 +1,7 @@
 // ms_dispatch.h — host launchers of the templated coupling kernels.
 #pragma once
+#include <utility>
+
 #include "ms_kernels.cuh"
 
 namespace msb {
@@ -17,5 +19,24 @@ struct RhsLaunch {
 void launch_rhs_fast(const RhsLaunch& L, const RhsArgs& a);
 // rhs_faithful: one thread per row
 void launch_rhs_faithful(const RhsLaunch& L, const RhsArgs& a);
+
+// Programmatic dependent launch for the kernels of the attempt chain (each
+// starts with pdl_enter()); MS_PDL=off launches them plainly.
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace msb

@@ -115,20 +115,30 @@ __device__ __forceinline__ void tc_ld32(uint32_t addr, uint32_t (&r)[32]) {
 }
 
 // Coupling epilogue of one warp: TMEM lane = row i, columns [c_beg, c_end) of
-// the tile (4 per trajectory: s_hi, s_lo, c_hi, c_lo sums). The record loads
+// the tile (4 per trajectory: s_hi, s_lo, c_hi, c_lo sums). The (s, c, omega) loads
 // of the next 8 trajectories are issued before the current 8 are finished.
 __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr, int i, int tb0, int c_beg, int c_end,
                                             const int* skip, double* const* outp) {
   const BatchDev& d = t.a.d;
   const float mw = (float)d.mw;
-  const TcRec* rec = reinterpret_cast<const TcRec*>(d.sc);
+  const float2* sc2 = reinterpret_cast<const float2*>(d.sc);
   const bool row_ok = i < t.n;
   TcRec cur[8];
   auto load = [&](int c0, TcRec (&v)[8]) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int tq = (c0 >> 2) + q;
-      if (row_ok && !skip[tq]) v[q] = rec[(int64_t)(tb0 + tq) * d.n + i];
+      if (row_ok && !skip[tq]) {
+        const int64_t e = (int64_t)(tb0 + tq) * d.n + i;
+#if MS_TC_PACKED
+        v[q] = reinterpret_cast<const TcRec*>(d.sc)[e];
+#else
+        const float2 p = sc2[e];
+        v[q].s = p.x;
+        v[q].c = p.y;
+        v[q].f = b_fval(d, e, t.a.fs32);
+#endif
+      }
     }
   };
   load(c_beg, cur);

@@ -158,6 +158,7 @@ __device__ __forceinline__ double ws_add(double fval, double coupling, int ws32)
 // prep: one thread per agent.
 template <int MODEL, class FS, class GS>
 __global__ void __launch_bounds__(256) k_prep(PrepArgs p) {
+  pdl_enter();
   Ctl* ctl = p.B.ctl;
   if (stage_skip(ctl, p.l, p.gate)) return;
   const int n = p.md.n, d = p.md.d;
@@ -400,6 +401,7 @@ __device__ __forceinline__ void sweep_step(const uint4 (&kv)[R], int nr, const G
 // (not on the row partition), so sharded runs are bitwise identical.
 template <int MODEL, bool SPLIT, class SS, class GS, int KS>
 __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsArgs a) {
+  pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NCOL = SPLIT ? 2 : 1;
@@ -635,6 +637,7 @@ struct TmaGeom {
 
 template <class SS, class GS, int KS>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(RhsArgs a) {
+  pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   using G = TmaGeom<GS, KS>;
   using KT = typename G::KT;
@@ -964,6 +967,7 @@ __device__ inline double seq_sum(const double* v, int64_t n) {
 
 #ifdef MS_DEFINE_STEP_KERNELS
 __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
+  pdl_enter();
   Ctl* c = f.B.ctl;
   const bool dead = c->done != 0;
   const bool stage_nf = c->nf_mask != 0;
@@ -1029,6 +1033,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
 // state, written once after initialisation with row0 = 1).
 __global__ void __launch_bounds__(256) k_snapshot(Bufs B, double* snap, double* snap_h, int64_t cap, int64_t dn,
                                                   int row0) {
+  pdl_enter();
   const Ctl* c = B.ctl;
   if (!row0 && !c->snap_pending) return;
   const int64_t row = row0 ? 0 : c->n_acc;
@@ -1063,6 +1068,7 @@ __device__ __forceinline__ double hermite(double th, double h, double xn, double
 }
 
 __global__ void __launch_bounds__(256) k_dense(Bufs B, int S, double* y, int64_t dn, int row0, int64_t row0_count) {
+  pdl_enter();
   const Ctl* c = B.ctl;
   int64_t lo, hi;
   if (row0) {
@@ -1092,6 +1098,7 @@ __global__ void __launch_bounds__(256) k_dense(Bufs B, int S, double* y, int64_t
 // parallel; each of the three sums is then added by one thread in ascending
 // order (the oracle's fixed order).
 __global__ void __launch_bounds__(1024) k_init_a(InitArgs a) {
+  pdl_enter();
   Ctl* c = a.B.ctl;
   if (c->done) return;
   __shared__ int nf;
@@ -1136,6 +1143,7 @@ __global__ void __launch_bounds__(1024) k_init_a(InitArgs a) {
 }
 
 __global__ void __launch_bounds__(1024) k_init_b(InitArgs a) {
+  pdl_enter();
   Ctl* c = a.B.ctl;
   if (c->done) return;
   const bool skip2 = c->init_skip2 != 0;
@@ -1186,6 +1194,7 @@ __global__ void __launch_bounds__(1024) k_init_b(InitArgs a) {
 
 // after the cold k1 (solver.cpp:263-269) and before the first attempt
 __global__ void k_loop_head(Ctl* c) {
+  pdl_enter();
   if (c->done) return;
   if (c->nf_mask & 1) {
     c->status = MS_NON_FINITE;
@@ -1197,7 +1206,10 @@ __global__ void k_loop_head(Ctl* c) {
   loop_check(c);
 }
 
-__global__ void k_stamp_start(Ctl* c) { c->t_start_ns = globaltimer_ns(); }
+__global__ void k_stamp_start(Ctl* c) {
+  pdl_enter();
+  c->t_start_ns = globaltimer_ns();
+}
 
 // sharded loop: finiteness of a gathered stage vector, identical on every rank
 __global__ void k_nf_scan(Ctl* c, const double* v, int64_t n, int l) {

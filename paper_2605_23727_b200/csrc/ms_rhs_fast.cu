@@ -15,7 +15,7 @@ namespace {
 // K sweep selection for the split Kuramoto: MS_SWEEP=ldg keeps the
 // register-fed sweep, MS_SWEEP=tile the 2D-tensor-tiled one-lane k_rhs_multi,
 // anything else (default) the row-copy TMA sweep for f32 K
-bool use_tma_sweep() {
+bool use_tma_sweep_env() {
   const char* v = std::getenv("MS_SWEEP");
   return !(v && std::strcmp(v, "ldg") == 0);
 }
@@ -61,7 +61,8 @@ void go_tma(const RhsLaunch& L, const RhsArgs& a) {
   }
   const int rows = a.row1 - a.row0;
   const int grid = rows < L.num_sms ? rows : L.num_sms;
-  kern<<<grid, kTmaThreads, smem, L.stream>>>(a);
+  cudaError_t e = launch_k(kern, grid, kTmaThreads, smem, L.stream, a);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tma launch: ") + cudaGetErrorString(e));
 }
 
 template <int MODEL, bool SPLIT, class SS, class GS, int KS>
@@ -76,7 +77,7 @@ void go(const RhsLaunch& L, const RhsArgs& a) {
     }
   }
   if constexpr (MODEL == MD_KUR && SPLIT && KS == MS_K_F32) {
-    if (use_tma_sweep()) {
+    if (use_tma_sweep_env()) {
       go_tma<SS, GS, KS>(L, a);
       return;
     }
@@ -92,7 +93,8 @@ void go(const RhsLaunch& L, const RhsArgs& a) {
   const int rows = a.row1 - a.row0;
   const int slots = L.num_sms * kFastMinBlocks;
   const int grid = rows < slots ? rows : slots;
-  kern<<<grid, kFastThreads, smem, L.stream>>>(a);
+  cudaError_t e = launch_k(kern, grid, kFastThreads, smem, L.stream, a);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_fast launch: ") + cudaGetErrorString(e));
 }
 
 template <int MODEL, bool SPLIT, class SS, class GS>
@@ -118,6 +120,14 @@ void by_prec(const RhsLaunch& L, const RhsArgs& a) {
 }
 
 }  // namespace
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("MS_PDL");
+    return !(v && std::strcmp(v, "off") == 0);
+  }();
+  return on;
+}
 
 void launch_rhs_fast(const RhsLaunch& L, const RhsArgs& a) {
   switch (L.model) {

@@ -20,6 +20,8 @@ VARIANTS = {
     # CTA-pair kernel: tile width, ring depth, CTAs per SM, epilogue off (mainloop time)
     "tc2_n512_s4": ("ms_batch.cu", {}),
     "tc2_n512_s4_noepi": ("ms_batch.cu", {"MS_T2_NOEPI": 1}),
+    "tc2_packed": ("ms_batch.cu", {"MS_TC_PACKED": 1}),
+    "tc2_split": ("ms_batch.cu", {"MS_TC_PACKED": 0}),
     "tc2_n512_s3": ("ms_batch.cu", {"MS_T2_STAGES": 3}),
     "tc2_n256_s4": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 4}),
     "tc2_n256_s3x2": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2}),

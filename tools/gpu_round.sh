@@ -1,3 +1,4 @@
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_dense.py tests/test_gpu_snapshots.py tests/test_gpu_solver.py tests/test_gpu_variants.py -q -x --timeout 1000 -p no:cacheprovider > gpurun_out/pytest_dense.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_dense.log
+timeout 900 python tools/tune_tc.py "lib_tc2_*.so" > gpurun_out/tune_tc2b.log 2>&1
+timeout 900 python tools/tune_tc.py "lib_tc2_*.so" >> gpurun_out/tune_tc2b.log 2>&1
