@@ -408,8 +408,8 @@ struct EvalSpec {
 
 // prep of one evaluation into workspace B; false when the model has no
 // coupling sweep (the reference's scalar test fixtures)
-bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp) {
-  const bool fs32 = is32(sp.f_prec), ss32 = is32(sp.sum_prec), gs32 = is32(sp.g_prec);
+PrepArgs prep_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_prec& sp) {
+  const bool fs32 = is32(sp.f_prec), ss32 = is32(sp.sum_prec);
   PrepArgs p{};
   p.md = s->md;
   p.B = B;
@@ -431,6 +431,12 @@ bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e
   p.fs32 = fs32 ? 1 : 0;
   p.ld = s->ld;
   p.xsrc = e.xsrc;
+  return p;
+}
+
+bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp) {
+  const bool fs32 = is32(sp.f_prec), gs32 = is32(sp.g_prec);
+  const PrepArgs p = prep_args(s, B, e, sp);
   const int pgrid = (int)std::max<int64_t>(1, std::min<int64_t>((s->n + 255) / 256, 4 * s->sms));
   if (s->fixture) {
     launch_prep_model<-1>(fs32, gs32, pgrid, st, p);
@@ -443,7 +449,6 @@ bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e
     default: launch_prep_model<MD_CC>(fs32, gs32, pgrid, st, p); break;
   }
   CK(cudaGetLastError());
-  (void)ss32;
   return true;
 }
 
@@ -480,8 +485,18 @@ void launch_sweep(ms_system* s, cudaStream_t st, const RhsArgs& a, const ms_stag
   CK(cudaGetLastError());
 }
 
+// PrepArgs of one evaluation (what launch_prep hands to k_prep)
+PrepArgs prep_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_prec& sp);
+
 void launch_eval(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp,
                  cudaEvent_t mid0 = nullptr, cudaEvent_t mid1 = nullptr) {
+  // small systems: prep fused into the sweep (whole, unsharded handles only:
+  // the fused kernel preps just the rows it sweeps)
+  if (!mid0 && !s->fixture && s->rhs_mode == MS_RHS_FAST && s->row0 == 0 && s->row1 == s->n) {
+    const bool split = s->mkind == MD_KUR;
+    RhsLaunch L{s->mkind, split, is32(sp.sum_prec), is32(sp.g_prec), s->ks, s->sms, st};
+    if (launch_eval_fused(L, prep_args(s, B, e, sp), rhs_args(s, B, e, sp), is32(sp.f_prec))) return;
+  }
   if (!launch_prep(s, B, st, e, sp)) return;
   const RhsArgs a = rhs_args(s, B, e, sp);
   if (mid0) CK(cudaEventRecord(mid0, st));

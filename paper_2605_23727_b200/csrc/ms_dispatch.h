@@ -19,6 +19,10 @@ struct RhsLaunch {
 void launch_rhs_fast(const RhsLaunch& L, const RhsArgs& a);
 // rhs_faithful: one thread per row
 void launch_rhs_faithful(const RhsLaunch& L, const RhsArgs& a);
+// prep + sweep in one launch (k_eval_fused) when the column data fits in shared
+// memory and the row (F, Sigma, G) is SSS / DDS / DDD; false = not applicable
+// (the caller then launches k_prep + the sweep). MS_FUSE=off disables it.
+bool launch_eval_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, bool fs32);
 
 // Programmatic dependent launch for the kernels of the attempt chain (each
 // starts with pdl_enter()); MS_PDL=off launches them plainly.

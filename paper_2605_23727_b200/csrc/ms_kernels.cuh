@@ -156,99 +156,131 @@ __device__ __forceinline__ double ws_add(double fval, double coupling, int ws32)
 
 // ------------------------------------------------------------------------------
 // prep: one thread per agent.
+struct PrepCtx {
+  Ctl* ctl;
+  int k1i, ix;
+  double* x;          // xb[ix]
+  const double* xs;   // the argument's source (x, or an explicit vector)
+  double* out;        // the k slot this evaluation fills
+  double h;
+  bool store32;
+};
+
+__device__ __forceinline__ PrepCtx prep_ctx(const PrepArgs& p) {
+  PrepCtx c;
+  c.ctl = p.B.ctl;
+  c.k1i = c.ctl->k1i;
+  c.ix = c.ctl->ix;
+  c.x = p.B.xb[c.ix];
+  c.xs = p.xsrc ? p.xsrc : c.x;
+  c.out = resolve_slot(p.B, p.S, p.out_slot, c.k1i);
+  c.h = p.kind == PREP_INIT_X1 ? c.ctl->h1 : c.ctl->h_att;
+  c.store32 = c.ctl->store32 != 0;
+  return c;
+}
+
+__device__ __forceinline__ void prep_count(const PrepArgs& p, Ctl* ctl) {
+  if (p.count == CNT_DDD) ctl->evals_ddd += 1;
+  else if (p.count == CNT_K1) ctl->evals_k1 += 1;
+  else if (p.count == CNT_STAGE) ctl->evals_stage[p.l] += 1;
+}
+
+// The stage argument of state element e (rk_step, solver.cpp:130-149). With
+// own = false nothing is written (a fused sweep recomputing other agents'
+// column values); the in-place binary32 rounding of x is idempotent, so
+// readers racing with the owner see the same value either way.
+__device__ __forceinline__ double prep_arg(const PrepArgs& p, const PrepCtx& c, int64_t e, bool own) {
+  double v;
+  if (p.kind == PREP_X) {
+    v = c.xs[e];
+    if (p.round_x) {
+      v = rn32(v);
+      if (own) c.x[e] = v;
+    }
+  } else if (p.kind == PREP_INIT_X1) {
+    v = __dadd_rn(c.xs[e], __dmul_rn(c.h, p.B.kb[1][e]));  // x0 + h1 * f0 (solver.cpp:435)
+  } else {
+    // combo = a_l0*k_0 (+ a_lm*k_m ...), arg = x + h*combo (solver.cpp:130-142)
+    double cm = __dmul_rn(p.coef[0], resolve_slot(p.B, p.S, p.slot[0], c.k1i)[e]);
+    for (int t = 1; t < p.nterms; ++t)
+      cm = __dadd_rn(cm, __dmul_rn(p.coef[t], resolve_slot(p.B, p.S, p.slot[t], c.k1i)[e]));
+    v = __dadd_rn(c.xs[e], __dmul_rn(c.h, cm));
+    if (p.is_last) {
+      if (c.store32) {
+        // combine_binary32 (solver.cpp:86-104)
+        const float hf = __double2float_rn(c.h);
+        float acc = __double2float_rn(c.xs[e]);
+        for (int t = 0; t < p.nterms; ++t) {
+          const float cf = __fmul_rn(hf, __double2float_rn(p.coef[t]));
+          acc = __fadd_rn(acc, __fmul_rn(cf, __double2float_rn(resolve_slot(p.B, p.S, p.slot[t], c.k1i)[e])));
+        }
+        if (own) p.B.xn[e] = v;  // x_next
+        v = (double)acc;
+      }
+      if (own) p.B.xb[c.ix ^ 1][e] = v;  // x_store (= x_next under binary64 storage)
+    }
+  }
+  return v;
+}
+
+// Every per-agent output of one evaluation for agent i: F in FS, the uncoupled
+// slots, the coupled slot's F (fvc), the column value(s) (gin) and the CC row
+// constant (systems.cpp:35-62). Returns whether an output is non-finite.
+template <int MODEL, class FS, class GS>
+__device__ __forceinline__ bool prep_agent(const PrepArgs& p, const PrepCtx& c, int i) {
+  const int d = p.md.d;
+  bool nonfinite = false;
+  double a[4];
+  for (int s = 0; s < d; ++s) a[s] = prep_arg(p, c, (int64_t)i * d + s, true);
+  if (MODEL < 0) {
+    // reference test fixtures (test_support.hpp:21-53): the whole RHS is F
+    const int kind = p.md.kind;
+    for (int s = 0; s < d; ++s) {
+      double o;
+      if (kind == MS_MODEL_SCALAR_EXP) o = p.fs32 ? rn32(a[s]) : a[s];  // round_to(x, f_prec)
+      else if (kind == MS_MODEL_SCALAR_ZERO) o = 0.0;
+      else o = __longlong_as_double(0x7ff8000000000000ll);
+      c.out[(int64_t)i * d + s] = o;
+      nonfinite |= !isfinite(o);
+    }
+    return nonfinite;
+  }
+  FS f[4];
+  model_f<FS>(p.md, i, a, f);
+  const int cs = p.md.cs;
+  for (int s = 0; s < d; ++s) {
+    if (s == cs) continue;
+    const double o = ws_add((double)f[s], 0.0, p.ws32);  // acc of an uncoupled slot is +0
+    c.out[(int64_t)i * d + s] = o;
+    nonfinite |= !isfinite(o);
+  }
+  p.B.fvc[i] = (double)f[cs];
+  GS* gin = reinterpret_cast<GS*>(p.B.gin);
+  // G reads slot 0 of both agents (x_j0 - x_i0, theta_j - theta_i), whatever
+  // slot it is added to (systems.cpp:123-126, 141-143, 183-184)
+  const GS xg = cvt<GS>(a[0]);
+  if (p.split) {
+    GS sv, cv;
+    dsincos(xg, &sv, &cv);
+    gin[i] = sv;
+    gin[p.ld + i] = cv;
+  } else {
+    gin[i] = xg;
+  }
+  if (MODEL == MD_CC) reinterpret_cast<GS*>(p.B.rowc)[i] = cc_pref<GS>(p.md, i, a[1]);
+  return nonfinite;
+}
+
 template <int MODEL, class FS, class GS>
 __global__ void __launch_bounds__(256) k_prep(PrepArgs p) {
   pdl_enter();
   Ctl* ctl = p.B.ctl;
   if (stage_skip(ctl, p.l, p.gate)) return;
-  const int n = p.md.n, d = p.md.d;
-  const int k1i = ctl->k1i, ix = ctl->ix;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (p.count == CNT_DDD) ctl->evals_ddd += 1;
-    else if (p.count == CNT_K1) ctl->evals_k1 += 1;
-    else if (p.count == CNT_STAGE) ctl->evals_stage[p.l] += 1;
-  }
-  double* x = p.B.xb[ix];
-  const double* xs = p.xsrc ? p.xsrc : x;
-  double* out = resolve_slot(p.B, p.S, p.out_slot, k1i);
-  const double h = p.kind == PREP_INIT_X1 ? ctl->h1 : ctl->h_att;
-  const bool store32 = ctl->store32 != 0;
+  const PrepCtx c = prep_ctx(p);
+  if (blockIdx.x == 0 && threadIdx.x == 0) prep_count(p, ctl);
   bool nonfinite = false;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double a[4];
-    for (int s = 0; s < d; ++s) {
-      const int64_t e = (int64_t)i * d + s;
-      double v;
-      if (p.kind == PREP_X) {
-        v = xs[e];
-        if (p.round_x) {
-          v = rn32(v);
-          x[e] = v;
-        }
-      } else if (p.kind == PREP_INIT_X1) {
-        v = __dadd_rn(xs[e], __dmul_rn(h, p.B.kb[1][e]));  // x0 + h1 * f0 (solver.cpp:435)
-      } else {
-        // combo = a_l0*k_0 (+ a_lm*k_m ...), arg = x + h*combo (solver.cpp:130-142)
-        double c = __dmul_rn(p.coef[0], resolve_slot(p.B, p.S, p.slot[0], k1i)[e]);
-        for (int t = 1; t < p.nterms; ++t)
-          c = __dadd_rn(c, __dmul_rn(p.coef[t], resolve_slot(p.B, p.S, p.slot[t], k1i)[e]));
-        v = __dadd_rn(xs[e], __dmul_rn(h, c));
-        if (p.is_last) {
-          if (store32) {
-            // combine_binary32 (solver.cpp:86-104)
-            const float hf = __double2float_rn(h);
-            float acc = __double2float_rn(xs[e]);
-            for (int t = 0; t < p.nterms; ++t) {
-              const float cf = __fmul_rn(hf, __double2float_rn(p.coef[t]));
-              acc = __fadd_rn(acc, __fmul_rn(cf, __double2float_rn(
-                                                     resolve_slot(p.B, p.S, p.slot[t], k1i)[e])));
-            }
-            p.B.xn[e] = v;  // x_next
-            v = (double)acc;
-          }
-          p.B.xb[ix ^ 1][e] = v;  // x_store (= x_next under binary64 storage)
-        }
-      }
-      a[s] = v;
-    }
-    if (MODEL < 0) {
-      // reference test fixtures (test_support.hpp:21-53): the whole RHS is F
-      const int kind = p.md.kind;
-      for (int s = 0; s < d; ++s) {
-        const int64_t e = (int64_t)i * d + s;
-        double o;
-        if (kind == MS_MODEL_SCALAR_EXP) o = p.fs32 ? rn32(a[s]) : a[s];  // round_to(x, f_prec)
-        else if (kind == MS_MODEL_SCALAR_ZERO) o = 0.0;
-        else o = __longlong_as_double(0x7ff8000000000000ll);
-        out[e] = o;
-        nonfinite |= !isfinite(o);
-      }
-      continue;
-    }
-    FS f[4];
-    model_f<FS>(p.md, i, a, f);
-    const int cs = p.md.cs;
-    for (int s = 0; s < d; ++s) {
-      if (s == cs) continue;
-      const double o = ws_add((double)f[s], 0.0, p.ws32);  // acc of an uncoupled slot is +0
-      out[(int64_t)i * d + s] = o;
-      nonfinite |= !isfinite(o);
-    }
-    p.B.fvc[i] = (double)f[cs];
-    GS* gin = reinterpret_cast<GS*>(p.B.gin);
-    // G reads slot 0 of both agents (x_j0 - x_i0, theta_j - theta_i), whatever
-    // slot it is added to (systems.cpp:123-126, 141-143, 183-184)
-    const GS xg = cvt<GS>(a[0]);
-    if (p.split) {
-      GS sv, cv;
-      dsincos(xg, &sv, &cv);
-      gin[i] = sv;
-      gin[p.ld + i] = cv;
-    } else {
-      gin[i] = xg;
-    }
-    if (MODEL == MD_CC) reinterpret_cast<GS*>(p.B.rowc)[i] = cc_pref<GS>(p.md, i, a[1]);
-  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.md.n; i += gridDim.x * blockDim.x)
+    nonfinite |= prep_agent<MODEL, FS, GS>(p, c, i);
   if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(&ctl->nf_mask, 1 << p.l);
 }
 
@@ -558,6 +590,149 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
       }
     }
     // warp-shuffle reduction of every row, then lane k writes row k
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) {
+        A[k] = add<SS>(A[k], shfl_xor(A[k], m));
+        if (SPLIT) B[k] = add<SS>(B[k], shfl_xor(B[k], m));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (lane == k && k < nr) {
+        const int r = rows[k];
+        SS coup;
+        if (SPLIT) {
+          const SS si = (SS)gin[r], ci = (SS)gin[ld + r];
+          coup = mul<SS>(mw, sub<SS>(mul<SS>(ci, A[k]), mul<SS>(si, B[k])));
+        } else {
+          coup = mul<SS>(mw, A[k]);
+        }
+        const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
+        out[(int64_t)r * a.d + a.cs] = o;
+        nonfinite |= !isfinite(o);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
+}
+
+// ------------------------------------------------------------------------------
+// eval_fused: prep + sweep of one evaluation in ONE launch, for systems whose
+// column data fits in shared memory (the BASELINE C1-C3 sizes). Every CTA
+// recomputes the column value(s) of all N agents from the stage combination
+// (slot 0 only: O(N) work, no transcendental but the split's sin/cos) into
+// shared memory and runs the full per-agent prep for its own rows only; then
+// it sweeps its rows exactly like k_rhs_fast (same lane/column order, same
+// shuffle tree: the result is bit-identical to prep + k_rhs_fast). Small
+// evaluations are latency-bound, and this removes one launch and one
+// dependent global round trip per stage.
+constexpr size_t kFusedMaxSmem = 96 * 1024;
+
+template <int MODEL, bool SPLIT, class FS, class SS, class GS, int KS>
+__global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(PrepArgs p, RhsArgs a) {
+  pdl_enter();
+  if (stage_skip(a.ctl, a.l, a.gate)) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int VEC = KVec<KS>::N;
+  constexpr int COLS_IT = 32 * VEC;
+  constexpr int R = FastRows<SS, GS>::R;
+  GS* colv = reinterpret_cast<GS*>(smem);  // [NCOL][ld]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = a.row1 - a.row0;
+  const int rb = a.row0 + (int)(total * blockIdx.x / gridDim.x);
+  const int re = a.row0 + (int)(total * (blockIdx.x + 1) / gridDim.x);
+  const int ld = (int)a.ld, n = p.md.n, d = p.md.d;
+
+  // ---- phase 1: column values of all agents; full prep of this CTA's rows
+  const PrepCtx c = prep_ctx(p);
+  if (blockIdx.x == 0 && threadIdx.x == 0) prep_count(p, c.ctl);
+  bool nonfinite = false;
+  for (int j = threadIdx.x; j < ld; j += blockDim.x) {
+    if (j < n) {
+      const GS xg = cvt<GS>(prep_arg(p, c, (int64_t)j * d, false));
+      if (SPLIT) {
+        GS sv, cv;
+        dsincos(xg, &sv, &cv);
+        colv[j] = sv;
+        colv[ld + j] = cv;
+      } else {
+        colv[j] = xg;
+      }
+    } else {
+      colv[j] = GS(0);
+      if (SPLIT) colv[ld + j] = GS(0);
+    }
+  }
+  for (int i = rb + (int)threadIdx.x; i < re; i += blockDim.x) nonfinite |= prep_agent<MODEL, FS, GS>(p, c, i);
+  __syncthreads();  // own rows' gin/fvc/rowc (global) and the column values (shared)
+
+  // ---- phase 2: the sweep of k_rhs_fast over one whole-width chunk
+  const int nrows = re - rb;
+  const int per_warp = (nrows + kFastWarps - 1) / kFastWarps;
+  const int nsweeps = (per_warp + R - 1) / R;
+  const GS* gin = reinterpret_cast<const GS*>(a.gin);
+  const SS mw = cvt<SS>(a.mw);
+  const GS kscal = cvt<GS>(a.coupling_k);
+  using KT = typename KElem<KS == MS_K_SCALAR ? MS_K_F32 : KS>::T;
+  const KT* Kbase = reinterpret_cast<const KT*>(a.K);
+  double* out = c.out;
+  const GS* sv = colv;
+  const GS* cv = colv + ld;
+  for (int sw = 0; sw < nsweeps; ++sw) {
+    int rows[R];
+    GS xi[R], pref[R];
+    int nr = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = rb + warp + kFastWarps * (sw * R + k);
+      rows[k] = r < re ? r : -1;
+      if (r < re) nr = k + 1;
+      xi[k] = GS(0);
+      pref[k] = GS(0);
+      if (!SPLIT && r < re) {
+        xi[k] = gin[r];
+        if (MODEL == MD_CC) pref[k] = reinterpret_cast<const GS*>(a.rowc)[r];
+      }
+    }
+    SS A[R], B[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) { A[k] = SS(0); B[k] = SS(0); }
+    if (nr > 0) {
+      for (int col = lane * VEC; col < ld; col += COLS_IT) {
+        GS s_loc[VEC], c_loc[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          s_loc[v] = sv[col + v];
+          if (SPLIT) c_loc[v] = cv[col + v];
+        }
+        if constexpr (KS == MS_K_SCALAR) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            if (k >= nr) break;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              if (SPLIT) {
+                A[k] = add<SS>(A[k], (SS)mul<GS>(kscal, s_loc[v]));
+                B[k] = add<SS>(B[k], (SS)mul<GS>(kscal, c_loc[v]));
+              } else if (col + v < a.n) {
+                GS g;
+                if (MODEL == MD_LCO) g = mul<GS>(kscal, sub<GS>(s_loc[v], xi[k]));
+                else g = mul<GS>(pref[k], mul<GS>(kscal, fatan<GS>(sub<GS>(s_loc[v], xi[k]))));
+                A[k] = add<SS>(A[k], (SS)g);
+              }
+            }
+          }
+        } else {
+          uint4 kv[R];
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (k < nr) kv[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + col);
+          sweep_step<MODEL, SPLIT, SS, GS, KS, R, VEC>(kv, nr, s_loc, c_loc, xi, pref, A, B);
+        }
+      }
+    }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
 #pragma unroll

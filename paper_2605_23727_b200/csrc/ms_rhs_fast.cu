@@ -121,6 +121,70 @@ void by_prec(const RhsLaunch& L, const RhsArgs& a) {
 
 }  // namespace
 
+namespace {
+
+template <int MODEL, bool SPLIT, class FS, class SS, class GS, int KS>
+void go_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, size_t smem) {
+  auto kern = k_eval_fused<MODEL, SPLIT, FS, SS, GS, KS>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedMaxSmem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("eval_fused attribute: ") + cudaGetErrorString(e));
+    attr_done = true;
+  }
+  const int rows = a.row1 - a.row0;
+  const int slots = L.num_sms * kFastMinBlocks;
+  const int grid = rows < slots ? rows : slots;
+  cudaError_t e = launch_k(kern, grid, kFastThreads, smem, L.stream, p, a);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("eval_fused launch: ") + cudaGetErrorString(e));
+}
+
+template <int MODEL, bool SPLIT, class FS, class SS, class GS>
+void fused_by_k(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, size_t smem) {
+  switch (L.ks) {
+    case MS_K_SCALAR: go_fused<MODEL, SPLIT, FS, SS, GS, MS_K_SCALAR>(L, p, a, smem); break;
+    case MS_K_F32: go_fused<MODEL, SPLIT, FS, SS, GS, MS_K_F32>(L, p, a, smem); break;
+    case MS_K_F16: go_fused<MODEL, SPLIT, FS, SS, GS, MS_K_F16>(L, p, a, smem); break;
+    default: go_fused<MODEL, SPLIT, FS, SS, GS, MS_K_BF16>(L, p, a, smem); break;
+  }
+}
+
+template <int MODEL, bool SPLIT>
+bool fused_by_prec(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, bool fs32) {
+  const size_t ncol = SPLIT ? 2 : 1;
+  if (fs32 && L.ss32 && L.gs32) {
+    const size_t smem = ncol * (size_t)a.ld * 4;
+    if (smem > kFusedMaxSmem) return false;
+    fused_by_k<MODEL, SPLIT, float, float, float>(L, p, a, smem);
+  } else if (!fs32 && !L.ss32 && L.gs32) {
+    const size_t smem = ncol * (size_t)a.ld * 4;
+    if (smem > kFusedMaxSmem) return false;
+    fused_by_k<MODEL, SPLIT, double, double, float>(L, p, a, smem);
+  } else if (!fs32 && !L.ss32 && !L.gs32) {
+    const size_t smem = ncol * (size_t)a.ld * 8;
+    if (smem > kFusedMaxSmem) return false;
+    fused_by_k<MODEL, SPLIT, double, double, double>(L, p, a, smem);
+  } else {
+    return false;
+  }
+  return true;
+}
+
+}  // namespace
+
+bool launch_eval_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, bool fs32) {
+  const char* env = std::getenv("MS_FUSE");
+  if (env && std::strcmp(env, "off") == 0) return false;
+  switch (L.model) {
+    case MD_LCO: return fused_by_prec<MD_LCO, false>(L, p, a, fs32);
+    // the split Kuramoto would recompute N sin/cos pairs in every CTA: measured
+    // 2x slower than prep + TMA sweep at C2 (N = 4096), so it keeps two launches
+    case MD_KUR: return false;
+    case MD_CC: return fused_by_prec<MD_CC, false>(L, p, a, fs32);
+    default: return false;
+  }
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("MS_PDL");

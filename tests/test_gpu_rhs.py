@@ -195,3 +195,34 @@ def test_tile_sweep_bitwise_equals_register_sweep(gpu, k_storage, n, sp, monkeyp
     part = DeviceSystem(spec)
     c = part.eval_rhs(0.0, x, sp)
     assert np.array_equal(c[5:n - 3], b[5:n - 3])
+
+
+@pytest.mark.parametrize("model", ["lco", "lco_c1", "cc"])
+@pytest.mark.parametrize("k_storage", ["scalar", "f32", "f16"])
+@pytest.mark.parametrize("sp", [StagePrecision(B32, B32, B32), StagePrecision(B64, B64, B32),
+                                StagePrecision(B64, B64, B64)], ids=str)
+def test_fused_eval_bitwise_equals_prep_plus_sweep(gpu, model, k_storage, sp, monkeypatch):
+    """k_eval_fused (prep + sweep in one launch, small systems) against the
+    two-kernel path: identical RHS rows, bit for bit."""
+    from paper_2605_23727_b200.systems import SystemSpec
+    n = 700
+    kw = dict(k_storage=k_storage, rhs_mode="fast", coupling_k=1.3)
+    if k_storage != "scalar":
+        kw["k_uniform"] = (5, 2, 0.0, 2.0)
+    if model == "lco_c1":
+        spec = SystemSpec("lco", n, coupled_slot=1, **kw)
+    elif model == "kuramoto":
+        spec = SystemSpec("kuramoto", n, omega=rng_uniform(1, 0, n, -1.0, 1.0), **kw)
+    elif model == "cc":
+        from paper_2605_23727_b200.systems import cc_parameters
+        k1, th = cc_parameters(n, 3)
+        spec = SystemSpec("cc", n, cc_k1=k1, cc_theta_h=th, stimulus_i0=0.2, **kw)
+    else:
+        spec = SystemSpec(model, n, **kw)
+    dev = DeviceSystem(spec)
+    x = rng_uniform(9, 1, n * spec.dim, -1.0, 1.0)
+    monkeypatch.setenv("MS_FUSE", "off")
+    a = dev.eval_rhs(0.0, x, sp)
+    monkeypatch.delenv("MS_FUSE")
+    b = dev.eval_rhs(0.0, x, sp)
+    assert np.array_equal(a, b, equal_nan=True)
