@@ -500,7 +500,9 @@ void launch_eval(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e
   if (!launch_prep(s, B, st, e, sp)) return;
   const RhsArgs a = rhs_args(s, B, e, sp);
   if (mid0) CK(cudaEventRecord(mid0, st));
-  launch_sweep(s, st, a, sp);
+  const bool split = s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST;
+  RhsLaunch L{s->mkind, split, is32(sp.sum_prec), is32(sp.g_prec), s->ks, s->sms, st};
+  if (!(split && launch_sweep_small(L, prep_args(s, B, e, sp), a))) launch_sweep(s, st, a, sp);
   if (mid1) CK(cudaEventRecord(mid1, st));
 }
 

@@ -23,6 +23,9 @@ void launch_rhs_faithful(const RhsLaunch& L, const RhsArgs& a);
 // memory and the row (F, Sigma, G) is SSS / DDS / DDD; false = not applicable
 // (the caller then launches k_prep + the sweep). MS_FUSE=off disables it.
 bool launch_eval_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, bool fs32);
+// the split Kuramoto's sweep for small N after k_prep (column values staged in
+// shared memory, one row per warp), MS_SWEEP=small only; false = not used
+bool launch_sweep_small(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a);
 
 // Programmatic dependent launch for the kernels of the attempt chain (each
 // starts with pdl_enter()); MS_PDL=off launches them plainly.

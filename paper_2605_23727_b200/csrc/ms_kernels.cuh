@@ -629,15 +629,29 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
 // evaluations are latency-bound, and this removes one launch and one
 // dependent global round trip per stage.
 constexpr size_t kFusedMaxSmem = 96 * 1024;
+#ifndef MS_FUSED_R
+#define MS_FUSED_R 1
+#endif
+#ifndef MS_FUSED_UNROLL
+#define MS_FUSED_UNROLL 8
+#endif
+#define MS_PRAGMA(x) _Pragma(#x)
+#define MS_UNROLL(n) MS_PRAGMA(unroll n)
 
-template <int MODEL, bool SPLIT, class FS, class SS, class GS, int KS>
+// PREPPED: the column values were written by k_prep (gin) and are only staged
+// into shared memory — the split Kuramoto's sin/cos are too costly to recompute
+// in every CTA, but its small sweeps gain from the same one-row-per-warp,
+// unrolled loop.
+template <int MODEL, bool SPLIT, class FS, class SS, class GS, int KS, bool PREPPED = false>
 __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(PrepArgs p, RhsArgs a) {
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int VEC = KVec<KS>::N;
   constexpr int COLS_IT = 32 * VEC;
-  constexpr int R = FastRows<SS, GS>::R;
+  // few rows per CTA at these sizes: 1 row per warp and the column loop
+  // unrolled, so a lane's K loads of several steps are in flight together
+  constexpr int R = MS_FUSED_R;
   GS* colv = reinterpret_cast<GS*>(smem);  // [NCOL][ld]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t total = a.row1 - a.row0;
@@ -647,10 +661,14 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
 
   // ---- phase 1: column values of all agents; full prep of this CTA's rows
   const PrepCtx c = prep_ctx(p);
-  if (blockIdx.x == 0 && threadIdx.x == 0) prep_count(p, c.ctl);
+  if (!PREPPED && blockIdx.x == 0 && threadIdx.x == 0) prep_count(p, c.ctl);
   bool nonfinite = false;
   for (int j = threadIdx.x; j < ld; j += blockDim.x) {
-    if (j < n) {
+    if (PREPPED) {
+      const GS* g = reinterpret_cast<const GS*>(a.gin);
+      colv[j] = j < n ? g[j] : GS(0);
+      if (SPLIT) colv[ld + j] = j < n ? g[ld + j] : GS(0);
+    } else if (j < n) {
       const GS xg = cvt<GS>(prep_arg(p, c, (int64_t)j * d, false));
       if (SPLIT) {
         GS sv, cv;
@@ -665,7 +683,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
       if (SPLIT) colv[ld + j] = GS(0);
     }
   }
-  for (int i = rb + (int)threadIdx.x; i < re; i += blockDim.x) nonfinite |= prep_agent<MODEL, FS, GS>(p, c, i);
+  if (!PREPPED)
+    for (int i = rb + (int)threadIdx.x; i < re; i += blockDim.x) nonfinite |= prep_agent<MODEL, FS, GS>(p, c, i);
   __syncthreads();  // own rows' gin/fvc/rowc (global) and the column values (shared)
 
   // ---- phase 2: the sweep of k_rhs_fast over one whole-width chunk
@@ -700,6 +719,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
 #pragma unroll
     for (int k = 0; k < R; ++k) { A[k] = SS(0); B[k] = SS(0); }
     if (nr > 0) {
+      MS_UNROLL(MS_FUSED_UNROLL)
       for (int col = lane * VEC; col < ld; col += COLS_IT) {
         GS s_loc[VEC], c_loc[VEC];
 #pragma unroll

@@ -123,9 +123,9 @@ void by_prec(const RhsLaunch& L, const RhsArgs& a) {
 
 namespace {
 
-template <int MODEL, bool SPLIT, class FS, class SS, class GS, int KS>
+template <int MODEL, bool SPLIT, class FS, class SS, class GS, int KS, bool PREPPED = false>
 void go_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, size_t smem) {
-  auto kern = k_eval_fused<MODEL, SPLIT, FS, SS, GS, KS>;
+  auto kern = k_eval_fused<MODEL, SPLIT, FS, SS, GS, KS, PREPPED>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedMaxSmem);
@@ -170,7 +170,30 @@ bool fused_by_prec(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, bool
   return true;
 }
 
+// the split Kuramoto's small sweep over prepped column values (any FS: the
+// prep already ran)
+template <class SS, class GS>
+bool small_split(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a) {
+  const size_t smem = 2 * (size_t)a.ld * sizeof(GS);
+  if (smem > kFusedMaxSmem) return false;
+  switch (L.ks) {
+    case MS_K_F32: go_fused<MD_KUR, true, SS, SS, GS, MS_K_F32, true>(L, p, a, smem); return true;
+    case MS_K_F16: go_fused<MD_KUR, true, SS, SS, GS, MS_K_F16, true>(L, p, a, smem); return true;
+    case MS_K_BF16: go_fused<MD_KUR, true, SS, SS, GS, MS_K_BF16, true>(L, p, a, smem); return true;
+    default: return false;
+  }
+}
+
 }  // namespace
+
+bool launch_sweep_small(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a) {
+  // measured slower than prep + k_rhs_tma / k_rhs_fast at C2 (73.7 vs 54 us per
+  // attempt: the split's rows want the pipelined sweeps), so opt-in only
+  const char* v = std::getenv("MS_SWEEP");
+  if (!(v && std::strcmp(v, "small") == 0) || L.model != MD_KUR || !L.split) return false;
+  if (L.ss32) return L.gs32 ? small_split<float, float>(L, p, a) : small_split<float, double>(L, p, a);
+  return L.gs32 ? small_split<double, float>(L, p, a) : small_split<double, double>(L, p, a);
+}
 
 bool launch_eval_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, bool fs32) {
   const char* env = std::getenv("MS_FUSE");

@@ -226,3 +226,20 @@ def test_fused_eval_bitwise_equals_prep_plus_sweep(gpu, model, k_storage, sp, mo
     monkeypatch.delenv("MS_FUSE")
     b = dev.eval_rhs(0.0, x, sp)
     assert np.array_equal(a, b, equal_nan=True)
+
+
+@pytest.mark.parametrize("k_storage", ["f32", "f16", "bf16"])
+@pytest.mark.parametrize("n", [1000, 4096, 8200])
+@pytest.mark.parametrize("sp", [StagePrecision(B32, B32, B32), StagePrecision(B64, B64, B32),
+                                StagePrecision(B64, B64, B64)], ids=str)
+def test_small_split_sweep_bitwise_equals_register_sweep(gpu, k_storage, n, sp, monkeypatch):
+    """The small split-Kuramoto sweep (MS_SWEEP=small: column values staged in
+    shared memory, one row per warp, unrolled) against k_rhs_fast."""
+    spec = kur_spec(n, k_storage, "fast", coupling_k=1.0)
+    dev = DeviceSystem(spec)
+    x = rng_uniform(8, 1, n, 0.0, 50.0)
+    monkeypatch.setenv("MS_SWEEP", "ldg")
+    a = dev.eval_rhs(0.0, x, sp)
+    monkeypatch.setenv("MS_SWEEP", "small")
+    b = dev.eval_rhs(0.0, x, sp)
+    assert np.array_equal(a, b)

@@ -29,6 +29,14 @@ VARIANTS = {
     "tc2_n512_s4_e16": ("ms_batch.cu", {"MS_T2_EPI": 16}),
     "tc2_n512_s3_e16": ("ms_batch.cu", {"MS_T2_EPI": 16, "MS_T2_STAGES": 3}),
     "tc2_n256_s3x2_e16": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_EPI": 16}),
+    # fused small-system evaluation: rows per warp x column-loop unroll
+    "fused_r2u4": ("ms_rhs_fast.cu", {}),
+    "fused_r1u8": ("ms_rhs_fast.cu", {"MS_FUSED_R": 1, "MS_FUSED_UNROLL": 8}),
+    "fused_r2u8": ("ms_rhs_fast.cu", {"MS_FUSED_R": 2, "MS_FUSED_UNROLL": 8}),
+    "fused_r4u2": ("ms_rhs_fast.cu", {"MS_FUSED_R": 4, "MS_FUSED_UNROLL": 2}),
+    "fused_r8u1": ("ms_rhs_fast.cu", {"MS_FUSED_R": 8, "MS_FUSED_UNROLL": 1}),
+    "fused_r1u16": ("ms_rhs_fast.cu", {"MS_FUSED_R": 1, "MS_FUSED_UNROLL": 16}),
+    "fused_r1u4": ("ms_rhs_fast.cu", {"MS_FUSED_R": 1, "MS_FUSED_UNROLL": 4}),
     # concurrent-variant sweep (ms_multi.cuh): consumer warps x rows per warp
     "multi_w8r4": ("ms_multi.cu", {}),
     "multi_w16r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 16, "MS_MULTI_R": 2}),
