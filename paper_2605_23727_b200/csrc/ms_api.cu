@@ -280,7 +280,7 @@ struct ms_system {
   bool ws_ready = false;
   void* ws_mem = nullptr;
   Bufs B{};
-  int fin_blocks = 1;
+  int fin_blocks = 1, fin_threads = kFinThreads;
   int64_t log_cap = 0;
   Ctl* ctl_host = nullptr;  // pinned mirror
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -377,6 +377,11 @@ void ensure_workspace(ms_system* s, int64_t log_cap) {
   }
   s->fin_blocks = (int)std::min<int64_t>((s->dn() + kFinThreads - 1) / kFinThreads, 2 * s->sms);
   if (s->fin_blocks < 1) s->fin_blocks = 1;
+  s->fin_threads = kFinThreads;
+  if (s->dn() <= kFinSmallMax) {
+    s->fin_blocks = 1;
+    s->fin_threads = kFinSmallThreads;
+  }
   const size_t total = bufs_bytes(s, log_cap);
   char* base = nullptr;
   CK(cudaMalloc(&base, total));
@@ -615,7 +620,7 @@ void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_
   FinArgs f = fin_args(s, s->B, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
   f.has_handle = has_handle ? 1 : 0;
   f.handle = h;
-  CK(launch_k(k_finalize, s->fin_blocks, kFinThreads, 0, st, f));
+  CK(launch_k(k_finalize, s->fin_blocks, s->fin_threads, 0, st, f));
   CK(cudaGetLastError());
   if (P.snaps) {
     CK(launch_k(k_snapshot, snap_grid(s), 256, 0, st, s->B, s->snap, s->snap_h, s->snap_cap, s->dn(), 0));
@@ -1036,7 +1041,7 @@ void loop_run(ms_system* s, const SolvePlan& P, int list, int index, cudaStream_
   launch_scan(s, st, out_of(S - 1), S - 1);
   FinArgs f = fin_args(s, s->B, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
   f.fixed_k1 = 1;
-  CK(launch_k(k_finalize, s->fin_blocks, kFinThreads, 0, st, f));
+  CK(launch_k(k_finalize, s->fin_blocks, s->fin_threads, 0, st, f));
   CK(cudaGetLastError());
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((s->dn() + 255) / 256, 2 * s->sms));
   k_fsal_copy<<<grid, 256, 0, st>>>(s->B.ctl, s->B.kb[0], s->B.kb[S], s->dn());
@@ -1259,7 +1264,7 @@ void mlaunch_attempt(ms_variants* v, cudaStream_t st, const SolvePlan* P, bool h
   for (int l = 0; l < nl; ++l) {
     FinArgs f = fin_args(s, v->B[l], T, FIN_SOLVE, P[l].k1_elided ? 1 : 0);
     f.has_handle = 0;
-    CK(launch_k(k_finalize, s->fin_blocks, kFinThreads, 0, st, f));
+    CK(launch_k(k_finalize, s->fin_blocks, s->fin_threads, 0, st, f));
     CK(cudaGetLastError());
     lc.c[l] = v->B[l].ctl;
   }
@@ -1807,7 +1812,7 @@ int ms_bs32_step(ms_system_t s, double t, const double* x_n, double h, const dou
     CK(cudaMemcpyAsync(s->B.kb[0], k1, sizeof(double) * dn, cudaMemcpyHostToDevice, st));
     for (int l = 1; l < T.S; ++l) launch_eval(s, st, stage_spec(T, l), P.rows[l - 1]);
     FinArgs f = fin_args(s, s->B, T, FIN_STEP, 0);
-    CK(launch_k(k_finalize, s->fin_blocks, kFinThreads, 0, st, f));
+    CK(launch_k(k_finalize, s->fin_blocks, s->fin_threads, 0, st, f));
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&c, s->B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

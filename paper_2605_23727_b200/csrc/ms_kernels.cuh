@@ -1071,6 +1071,10 @@ struct FinArgs {
 };
 
 constexpr int kFinThreads = 256;
+// small state vectors: one 1024-thread block does the whole reduction and the
+// controller, without the grid ticket (one dependent round trip fewer)
+constexpr int kFinSmallThreads = 1024;
+constexpr int64_t kFinSmallMax = 2048;  // measured: C1 (2048) -3 %, C3 (8192) +20 % per attempt
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000ll); }
 
@@ -1161,13 +1165,13 @@ __device__ inline double seq_sum(const double* v, int64_t n) {
 }
 
 #ifdef MS_DEFINE_STEP_KERNELS
-__global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
+__global__ void __launch_bounds__(kFinSmallThreads) k_finalize(FinArgs f) {
   pdl_enter();
   Ctl* c = f.B.ctl;
   const bool dead = c->done != 0;
   const bool stage_nf = c->nf_mask != 0;
-  __shared__ double red[kFinThreads / 32];
-  __shared__ int red_nf[kFinThreads / 32];
+  __shared__ double red[kFinSmallThreads / 32];
+  __shared__ int red_nf[kFinSmallThreads / 32];
   double m = 0.0;
   bool nf = false;
   if (!dead && !stage_nf) {
@@ -1177,6 +1181,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
     const double* xnx = c->store32 ? f.B.xn : xst;
     const double h = c->h_att;
     const double floor_w = __ddiv_rn(c->abs_tol, c->rel_tol);
+#pragma unroll 4
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < f.dn; e += (int64_t)gridDim.x * blockDim.x) {
       // x_tilde = x + h * (sum b~_l k_l), solver.cpp:188-199
       double comb = __dmul_rn(f.bt[0], resolve_slot(f.B, f.S, f.bslot[0], k1i)[e]);
@@ -1195,30 +1200,38 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs f) {
     m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     nf = __any_sync(0xffffffffu, nf);
   }
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) { red[warp] = m; red_nf[warp] = nf; }
   __syncthreads();
-  __shared__ bool is_last;
-  if (threadIdx.x == 0) {
-    double bm = 0.0;
-    int bnf = 0;
-    for (int w = 0; w < kFinThreads / 32; ++w) { bm = fmax(bm, red[w]); bnf |= red_nf[w]; }
-    f.B.part[blockIdx.x] = bm;
-    if (bnf) atomicOr(&c->any_nonfinite, 1);
-    __threadfence();
-    const unsigned t = atomicAdd(&c->ticket, 1u);
-    is_last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!is_last || threadIdx.x != 0) return;
-  __threadfence();
-  c->ticket = 0;
-  const bool any_nf = atomicAdd(&c->any_nonfinite, 0) != 0;
-  c->any_nonfinite = 0;
-
   double e = 0.0;
-  if (!(dead || stage_nf || any_nf))
-    for (int b = 0; b < (int)gridDim.x; ++b) e = fmax(e, f.B.part[b]);
+  bool any_nf;
+  if (gridDim.x == 1) {
+    if (threadIdx.x != 0) return;
+    int bnf = 0;
+    for (int w = 0; w < nwarps; ++w) { e = fmax(e, red[w]); bnf |= red_nf[w]; }
+    any_nf = bnf != 0;
+    if (dead || stage_nf || any_nf) e = 0.0;
+  } else {
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+      double bm = 0.0;
+      int bnf = 0;
+      for (int w = 0; w < nwarps; ++w) { bm = fmax(bm, red[w]); bnf |= red_nf[w]; }
+      f.B.part[blockIdx.x] = bm;
+      if (bnf) atomicOr(&c->any_nonfinite, 1);
+      __threadfence();
+      const unsigned t = atomicAdd(&c->ticket, 1u);
+      is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!is_last || threadIdx.x != 0) return;
+    __threadfence();
+    c->ticket = 0;
+    any_nf = atomicAdd(&c->any_nonfinite, 0) != 0;
+    c->any_nonfinite = 0;
+    if (!(dead || stage_nf || any_nf))
+      for (int b = 0; b < (int)gridDim.x; ++b) e = fmax(e, f.B.part[b]);
+  }
   const bool more = attempt_controller(c, f.S, f.mode, f.k1_elided, f.fixed_k1, dead, stage_nf, any_nf, e, f.B.log);
   if (f.has_handle && f.mode == FIN_SOLVE) cudaGraphSetConditional(f.handle, more ? 1 : 0);
 }
