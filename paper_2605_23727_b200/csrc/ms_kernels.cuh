@@ -281,6 +281,16 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs p) {
   bool nonfinite = false;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.md.n; i += gridDim.x * blockDim.x)
     nonfinite |= prep_agent<MODEL, FS, GS>(p, c, i);
+  // zero the padding columns [n, ld) of the column data in THIS evaluation's
+  // type: the buffer is shared by binary32 and binary64 rows, and the scalar
+  // coupling (no zero-padded K) sums over every column of the chunk
+  if (MODEL >= 0) {
+    GS* gin = reinterpret_cast<GS*>(p.B.gin);
+    for (int j = p.md.n + blockIdx.x * blockDim.x + threadIdx.x; j < p.ld; j += gridDim.x * blockDim.x) {
+      gin[j] = GS(0);
+      if (p.split) gin[p.ld + j] = GS(0);
+    }
+  }
   if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(&ctl->nf_mask, 1 << p.l);
 }
 
