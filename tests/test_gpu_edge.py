@@ -89,3 +89,48 @@ def test_tiny_ensembles(gpu, shape, tc):
     res = bat.solve(x, 0.0, 0.5, policy_for(PolicyVariant.Single), cfg)
     assert all(s == SolveStatus.Completed for s in res.status)
     assert np.all(np.isfinite(res.final_state))
+
+
+@pytest.mark.parametrize("model", ["lco", "kuramoto", "cc"])
+def test_non_finite_inputs_end_as_nonfinite(gpu, model):
+    """A NaN in x0 (initial_step returns NaN, solver.cpp:426) and an infinite
+    K entry (the first stage goes non-finite) end the solve with NonFinite,
+    as in the oracle."""
+    n = 16
+    spec = _spec(model, n, "f32", "fast")
+    dev, orc = DeviceSystem(spec), O.OracleSystem(spec)
+    x = _x(model, n)
+    x[3] = np.nan
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    pol = policy_for(PolicyVariant.Mixed2)
+    r = S.solve(dev, x, 0.0, 1.0, pol, cfg)
+    o = O.solve(orc, x, 0.0, 1.0, pol, cfg)
+    assert r.status == o.status == SolveStatus.NonFinite
+    k = np.full((n, n), 0.5)
+    k[2, 5] = np.inf
+    spec_k = SystemSpec(**{**spec.__dict__, "k_uniform": None, "K": k})
+    devk, orck = DeviceSystem(spec_k), O.OracleSystem(spec_k)
+    xk = _x(model, n)
+    r = S.solve(devk, xk, 0.0, 1.0, pol, cfg)
+    o = O.solve(orck, xk, 0.0, 1.0, pol, cfg)
+    assert r.status == o.status == SolveStatus.NonFinite
+    assert r.n_accepted == o.n_accepted
+
+
+def test_batch_trajectories_fail_independently(gpu):
+    """One trajectory with a NaN start ends NonFinite; the others complete
+    exactly as a clean ensemble of the same trajectories does."""
+    B, n = 4, 64
+    spec = SystemSpec("kuramoto", n, k_storage="f32", omega=np.zeros(n), k_uniform=(4, 2, 0.0, 2.0))
+    omega = rng_normal(4, 0, B * n).reshape(B, n)
+    x = rng_uniform(4, 1, B * n, 0.0, TWO_PI).reshape(B, n)
+    dev = DeviceSystem(spec)
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    clean = DeviceBatch(dev, omega, tensor_cores=False).solve(x, 0.0, 1.0, policy_for(PolicyVariant.Mixed2), cfg)
+    bad = x.copy()
+    bad[2, 7] = np.nan
+    res = DeviceBatch(dev, omega, tensor_cores=False).solve(bad, 0.0, 1.0, policy_for(PolicyVariant.Mixed2), cfg)
+    assert res.status[2] == SolveStatus.NonFinite
+    for b in (0, 1, 3):
+        assert res.status[b] == SolveStatus.Completed
+        assert res.n_accepted[b] == clean.n_accepted[b] and np.array_equal(res.final_state[b], clean.final_state[b])
