@@ -77,21 +77,11 @@ struct BPrepArgs {
   int op_ks;  // 0: no GEMM operand; MS_K_F16 / MS_K_BF16: write the rounded operand
 };
 
-// stage combination + F + sin/cos (+ rounded GEMM operand) for every
-// trajectory: grid (ceil(n/256), B)
+// stage combination + F + sin/cos (+ rounded GEMM operand) of element i of
+// trajectory b (the caller has checked stage_skip and counted the evaluation)
 template <class FS, class GS>
-__global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
-  const int b = blockIdx.y;
+__device__ __forceinline__ void bprep_elem(const BPrepArgs& p, int b, int i, Ctl* c) {
   const BatchDev& d = p.d;
-  Ctl* c = d.ctl + b;
-  if (stage_skip(c, p.l, p.gate)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (p.count == CNT_DDD) c->evals_ddd += 1;
-    else if (p.count == CNT_K1) c->evals_k1 += 1;
-    else if (p.count == CNT_STAGE) c->evals_stage[p.l] += 1;
-  }
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= d.n) return;
   const int64_t e = (int64_t)b * d.n + i;
   const int ix = c->ix;
   double* x = d.xb[ix];
@@ -160,6 +150,23 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
     op[2 * d.ld + i] = ch;
     op[3 * d.ld + i] = __float2half_rn(__fsub_rn(c32, __half2float(ch)));
   }
+}
+
+// every trajectory: grid (ceil(n/256), B)
+template <class FS, class GS>
+__global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
+  const int b = blockIdx.y;
+  const BatchDev& d = p.d;
+  Ctl* c = d.ctl + b;
+  if (stage_skip(c, p.l, p.gate)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.count == CNT_DDD) c->evals_ddd += 1;
+    else if (p.count == CNT_K1) c->evals_k1 += 1;
+    else if (p.count == CNT_STAGE) c->evals_stage[p.l] += 1;
+  }
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.n) return;
+  bprep_elem<FS, GS>(p, b, i, c);
 }
 
 struct BRhsArgs {

@@ -1,3 +1,5 @@
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_edge.py -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_edge.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_edge.log
+timeout 900 python -m pytest tests/test_gpu_batch.py tests/test_gpu_edge.py -q -x --timeout 800 -p no:cacheprovider > gpurun_out/pytest_batch.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_batch.log
+timeout 600 python tools/bench_c5.py --steps 2 > gpurun_out/c5.log 2>&1
+MS_BFUSE=off timeout 600 python tools/bench_c5.py --steps 2 > gpurun_out/c5_off.log 2>&1
