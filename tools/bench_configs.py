@@ -29,10 +29,14 @@ def cpu_attempt_s(w, attempts=2):
     return (time.perf_counter() - t) / attempts
 
 
-def run(name, w, reps=2):
+FINALS = {}
+
+
+def run(name, w, reps=2, compare_to=None):
     dev = DeviceSystem(w.spec)
     S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg)  # warm-up (graph instantiation)
     rs = [S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg) for _ in range(reps)]
+    FINALS[name] = rs[0].final_state
     ms = sum(r.device_ms for r in rs) / reps
     r = rs[0]
     cpu = cpu_attempt_s(w)
@@ -43,6 +47,12 @@ def run(name, w, reps=2):
             "cpu_oracle_s_per_attempt": cpu, "cpu_cores": os.cpu_count(),
             "cpu_oracle_accepted_steps_per_s_est": 1.0 / (cpu * att_per_acc),
             "speedup_vs_cpu_est": (r.n_accepted / (ms / 1e3)) * cpu * att_per_acc}
+    if compare_to in FINALS:
+        # K storage effect: the same solve with K rounded to f16 vs K in f32
+        # (weighted like Eq. 7, floor atol/rtol)
+        ref = FINALS[compare_to]
+        d = np.abs(r.final_state - ref) / np.maximum(np.abs(ref), w.cfg.abs_tol / w.cfg.rel_tol)
+        line["final_state_vs"] = {"run": compare_to, "max_rel_weighted": float(d.max())}
     print(json.dumps(line), flush=True)
     dev.close()
 
@@ -51,5 +61,6 @@ if __name__ == "__main__":
     run("C1 LCO N=1024 K f32", config1_lco())
     for ks in ("f32", "f16"):
         for rtol in (1e-3, 1e-4, 1e-6, 1e-8):
-            run(f"C2 Kuramoto N=4096 K {ks} rtol {rtol:g}", config2_kuramoto(rtol=rtol, k_storage=ks), reps=1)
+            run(f"C2 Kuramoto N=4096 K {ks} rtol {rtol:g}", config2_kuramoto(rtol=rtol, k_storage=ks), reps=1,
+                compare_to=f"C2 Kuramoto N=4096 K f32 rtol {rtol:g}" if ks == "f16" else None)
     run("C3 CC N=2048 K f32 t in [0,240]", config3_cc(), reps=1)
