@@ -13,16 +13,20 @@ namespace msb {
 namespace {
 
 // K sweep selection for the split Kuramoto: MS_SWEEP=ldg keeps the
-// register-fed sweep, MS_SWEEP=tile the 2D-tensor-tiled one-lane k_rhs_multi,
-// anything else (default) the row-copy TMA sweep for f32 K
+// register-fed sweep, MS_SWEEP=tile the 2D-tensor-tiled one-lane k_rhs_multi;
+// by default f32 K takes the row-copy TMA sweep and 16-bit K the tile sweep
 bool use_tma_sweep_env() {
   const char* v = std::getenv("MS_SWEEP");
   return !(v && std::strcmp(v, "ldg") == 0);
 }
-bool use_tile_sweep(int ks) {
+// 16-bit K at moderate N defaults to the 2D-tile sweep (C2, N = 4096: 53 vs
+// 59-64 us per attempt); at C4 (N = 32768) the register sweep stays ahead
+// (bench: 726 vs 698 steps/s). f32 K keeps the row-copy TMA sweep.
+bool use_tile_sweep(int ks, int64_t ld) {
   const char* v = std::getenv("MS_SWEEP");
-  (void)ks;
-  return v && std::strcmp(v, "tile") == 0;
+  if (v && std::strcmp(v, "tile") == 0) return true;
+  if (v && (std::strcmp(v, "ldg") == 0 || std::strcmp(v, "small") == 0)) return false;
+  return (ks == MS_K_F16 || ks == MS_K_BF16) && ld <= 8192;
 }
 
 template <class SS, class GS, int KS>
@@ -71,7 +75,7 @@ void go(const RhsLaunch& L, const RhsArgs& a) {
   // row copies get small and the s/c traffic per K byte doubles, and the
   // register-fed sweep stays ahead (profiles/r1_tune_tma.txt)
   if constexpr (MODEL == MD_KUR && SPLIT && KS != MS_K_SCALAR && !(sizeof(SS) == 4 && sizeof(GS) == 8)) {
-    if (use_tile_sweep(KS)) {
+    if (use_tile_sweep(KS, a.ld)) {
       go_tile<SS, GS, KS>(L, a);
       return;
     }

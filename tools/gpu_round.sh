@@ -1,10 +1,5 @@
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
-export MS_LOOP=host
-timeout 300 python tools/bench_c5.py --tf 0.5 --steps 1 > gpurun_out/c5s.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_tc_gemm2" -s 10 -c 1 -o gpurun_out/prof_tc2_final -f python tools/bench_c5.py --tf 0.5 --steps 1 > gpurun_out/ncu_tc2.log 2>&1
-timeout 300 python tools/prof_variants.py c4 > gpurun_out/pv.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_rhs_multi" -s 6 -c 1 -o gpurun_out/prof_multi_final -f python tools/prof_variants.py c4 > gpurun_out/ncu_multi.log 2>&1
-timeout 300 python tools/prof_small.py c1 > gpurun_out/ps.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_eval_fused" -s 20 -c 1 -o gpurun_out/prof_fused_final -f python tools/prof_small.py c1 > gpurun_out/ncu_fused.log 2>&1
-echo done
+timeout 1200 python -m pytest tests/test_gpu_rhs.py tests/test_gpu_c4_full.py tests/test_gpu_configs_full.py tests/test_gpu_sharded.py -q -x --timeout 1000 -p no:cacheprovider > gpurun_out/pytest_sw.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_sw.log
+timeout 900 python bench.py --kdtype f16 --no-cpu-baseline > gpurun_out/bench_f16.log 2>&1; echo rc=$? >> gpurun_out/bench_f16.log
+for ks in f16 bf16; do timeout 300 python tools/prof_small16.py $ks; done > gpurun_out/c2sweep16.log 2>&1
