@@ -284,6 +284,47 @@ inline SolveResult dp54_reference(const System& sys, const Vector& x0, double t0
   }, x0.size(), cfg);
 }
 
+// Concurrent solves of one system under up to four policies (the harness's
+// variants, harness.cpp:113-121): one K sweep per stage for all of them where the
+// model allows, each result bit-identical to its own solve().
+inline std::vector<SolveResult> solve_variants(const System& sys, const Vector& x0, double t0, double t_final,
+                                               const std::vector<PrecisionPolicy>& policies,
+                                               const SolverConfig& cfg) {
+  const std::size_t nv = policies.size(), dn = x0.size();
+  ms_variants_t vh = nullptr;
+  check(ms_variants_create(sys.handle(), static_cast<int32_t>(nv), &vh), "variants_create");
+  std::vector<ms_policy> pols(nv);
+  for (std::size_t i = 0; i < nv; ++i) pols[i] = policies[i].c();
+  const ms_solver_config c = cfg.c();
+  std::vector<SolveResult> out(nv);
+  std::vector<std::vector<ms_step_record>> logs(nv);
+  std::vector<ms_solve_result> rs(nv);
+  for (std::size_t i = 0; i < nv; ++i) {
+    out[i].final_state.resize(dn);
+    logs[i].resize(cfg.record_step_log ? static_cast<std::size_t>(cfg.max_iterations) : 0);
+    rs[i] = ms_solve_result{};
+    rs[i].final_state = out[i].final_state.data();
+    rs[i].step_log = logs[i].empty() ? nullptr : logs[i].data();
+    rs[i].step_log_capacity = static_cast<int64_t>(logs[i].size());
+  }
+  const int rc = ms_variants_solve(vh, x0.data(), t0, t_final, pols.data(), &c, rs.data());
+  ms_variants_destroy(vh);
+  check(rc, "variants_solve");
+  for (std::size_t i = 0; i < nv; ++i) {
+    const ms_solve_result& r = rs[i];
+    out[i].status = static_cast<SolveStatus>(r.status);
+    out[i].t_reached = r.t_reached;
+    out[i].n_accepted = r.n_accepted;
+    out[i].n_failed = r.n_failed;
+    out[i].flops = {r.flops_low, r.flops_high, r.rhs_evals};
+    out[i].device_ms = r.device_ms;
+    const int64_t m = std::min(r.step_log_count, r.step_log_capacity);
+    for (int64_t k = 0; k < m; ++k)
+      out[i].step_log.push_back({logs[i][k].t, logs[i][k].h, logs[i][k].err, logs[i][k].accepted != 0});
+  }
+  return out;
+}
+
 // ---- host metrics over device results (metrics.hpp / metrics.cpp) ------------
 
 // Analytic propagator of the reference LCO at time t (systems.cpp:270-306):

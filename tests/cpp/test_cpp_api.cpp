@@ -48,6 +48,33 @@ int main() {
     threw = true;
   }
   REQUIRE(threw);
+  // snapshots + dense output (solver.cpp:324-327; D6 extension) and the metrics over them
+  SolverConfig c3;
+  c3.rel_tol = 1e-6;
+  c3.abs_tol = 1e-8;
+  c3.record_snapshots = true;
+  ms_system_desc ld{};
+  ld.model = MS_MODEL_LCO;
+  ld.n_agents = 4;
+  ld.coupling_k = 1.0;
+  System lco(ld);
+  Vector x0 = {0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8};
+  SolveResult rs = solve(lco, x0, 0.0, 2.0, dbl, c3, std::vector<double>{0.0, 1.0, 2.0});
+  REQUIRE(rs.status == SolveStatus::Completed);
+  REQUIRE(static_cast<int64_t>(rs.snapshots.size()) == rs.n_accepted && rs.snapshots.front().x_before == x0);
+  REQUIRE(rs.y_eval.size() == 3 && rs.y_eval.back() == rs.final_state && rs.y_eval.front() == x0);
+  const ErrorReport er = error_report(rs, lco_analytic(x0, 2.0), 4, c3.abs_tol, c3.rel_tol);
+  REQUIRE(er.has_mean_e_analytic && er.mean_e_analytic < c3.rel_tol && er.normalized_final_error < 1e-5);
+  // the four named variants concurrently, each equal to its own solve
+  std::vector<PrecisionPolicy> pols = {policy_for(PolicyVariant::Single), policy_for(PolicyVariant::Mixed1),
+                                       policy_for(PolicyVariant::Mixed2), policy_for(PolicyVariant::Double)};
+  SolverConfig c4 = c3;
+  c4.record_snapshots = false;
+  const std::vector<SolveResult> vr = solve_variants(lco, x0, 0.0, 2.0, pols, c4);
+  for (std::size_t i = 0; i < pols.size(); ++i) {
+    const SolveResult one = solve(lco, x0, 0.0, 2.0, pols[i], c4);
+    REQUIRE(vr[i].final_state == one.final_state && vr[i].n_accepted == one.n_accepted);
+  }
   std::printf("cpp api ok: %lld accepted, %lld evals\n", (long long)r.n_accepted, (long long)r.flops.rhs_evals);
   return 0;
 }
