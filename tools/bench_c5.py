@@ -27,9 +27,10 @@ ap.add_argument("--n", type=int, default=2048)
 ap.add_argument("--tf", type=float, default=20.0)
 ap.add_argument("--tc", type=int, default=1)
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--kdtype", default="bf16", choices=["bf16", "f16"])
 a = ap.parse_args()
 ws, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
-w = config5_batch(batch=a.batch, n=a.n, tf=a.tf)
+w = config5_batch(batch=a.batch, n=a.n, tf=a.tf, k_storage=a.kdtype)
 w.spec.device = local
 dev = DeviceSystem(w.spec)
 if ws > 1:
@@ -56,7 +57,7 @@ ms = sum(r.device_ms for r in res)
 acc = sum(int(r.n_accepted.sum()) for r in res)
 r0 = res[0]
 line = {
-    "workload": f"C5 batched Kuramoto B={a.batch} N={a.n} K bf16, t in [0,{a.tf}], rtol 1e-6 atol 1e-9",
+    "workload": f"C5 batched Kuramoto B={a.batch} N={a.n} K {a.kdtype}, t in [0,{a.tf}], rtol 1e-6 atol 1e-9",
     "n_gpus": ws, "scaling": "strong" if ws > 1 else "weak",
     "parallelism": f"trajectory shards x{ws} (no per-step exchange)" if ws > 1 else "single GPU",
     "tensor_cores": bool(a.tc),
