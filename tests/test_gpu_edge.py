@@ -134,3 +134,36 @@ def test_batch_trajectories_fail_independently(gpu):
     for b in (0, 1, 3):
         assert res.status[b] == SolveStatus.Completed
         assert res.n_accepted[b] == clean.n_accepted[b] and np.array_equal(res.final_state[b], clean.final_state[b])
+
+
+def test_interleaved_api_use_leaves_no_state_behind(gpu):
+    """One handle driven through every entry point in turn (eval_rhs, bs32_step,
+    solves under different policies with and without logs/snapshots/dense
+    output, concurrent variants, DP5(4)) gives the same answers as fresh
+    handles: no workspace, graph or control-block state leaks between calls."""
+    from paper_2605_23727_b200.configs import config2_kuramoto
+    w = config2_kuramoto(n=300, rtol=1e-6)
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    pols = [policy_for(v) for v in (PolicyVariant.Single, PolicyVariant.Mixed1, PolicyVariant.Mixed2,
+                                    PolicyVariant.Double)]
+
+    def fresh(fn):
+        d = DeviceSystem(w.spec)
+        out = fn(d)
+        d.close()
+        return out
+
+    shared = DeviceSystem(w.spec)
+    calls = [
+        lambda d: d.eval_rhs(0.0, w.x0, DDS),
+        lambda d: S.solve(d, w.x0, 0.0, 2.0, pols[0], cfg).final_state,
+        lambda d: S.bs32_step(d, 0.0, w.x0, 1e-3, d.eval_rhs(0.0, w.x0, SSS), pols[0], cfg).x_next,
+        lambda d: S.solve(d, w.x0, 0.0, 2.0, pols[3], SolverConfig(**{**cfg.__dict__, "record_snapshots": True}),
+                          t_eval=[0.5, 1.5]).y_eval,
+        lambda d: np.stack([r.final_state for r in S.solve_variants(d, w.x0, 0.0, 1.0, pols, cfg)]),
+        lambda d: S.solve(d, w.x0, 0.0, 2.0, pols[2], cfg, log_capacity=3).final_state,
+        lambda d: S.dp54_reference(d, w.x0, 0.0, 0.5, cfg).final_state,
+        lambda d: S.solve(d, w.x0, 0.0, 2.0, pols[0], cfg).final_state,
+    ]
+    for k, fn in enumerate(calls):
+        assert np.array_equal(fn(shared), fresh(fn)), k
