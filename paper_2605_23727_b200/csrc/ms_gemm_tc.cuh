@@ -117,8 +117,10 @@ __device__ __forceinline__ void tc_ld32(uint32_t addr, uint32_t (&r)[32]) {
 // Coupling epilogue of one warp: TMEM lane = row i, columns [c_beg, c_end) of
 // the tile (4 per trajectory: s_hi, s_lo, c_hi, c_lo sums). The (s, c, omega) loads
 // of the next 8 trajectories are issued before the current 8 are finished.
+// The first 8 trajectories' records are loaded while the MMAs still run (the
+// epilogue warps are idle until tmem_full), then the accumulators are awaited.
 __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr, int i, int tb0, int c_beg, int c_end,
-                                            const int* skip, double* const* outp) {
+                                            const int* skip, double* const* outp, uint64_t* tmem_full) {
   const BatchDev& d = t.a.d;
   const float mw = (float)d.mw;
   const float2* sc2 = reinterpret_cast<const float2*>(d.sc);
@@ -142,6 +144,8 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
     }
   };
   load(c_beg, cur);
+  tc_wait(tmem_full, 0);
+  tc_fence_after();
 #pragma unroll 1
   for (int c0 = c_beg; c0 < c_end; c0 += 32) {
     uint32_t r[32];
@@ -269,12 +273,10 @@ __global__ void __launch_bounds__(kTcThreads, MS_TC_MINB)
       tc_out[et] = outp;
     }
     asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpiWarps) : "memory");
-    tc_wait(tmem_full, 0);
-    tc_fence_after();
     const int i = m0 + q4 * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
     constexpr int kCols = kTcBN * 4 / kTcEpiWarps;  // columns per epilogue warp
-    tc_epilogue(t, lane_addr, i, tb0, half * kCols, (half + 1) * kCols, tc_skip, tc_out);
+    tc_epilogue(t, lane_addr, i, tb0, half * kCols, (half + 1) * kCols, tc_skip, tc_out, tmem_full);
   }
   tc_fence_before();
   __syncthreads();
@@ -447,14 +449,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
       tc_out[et] = outp;
     }
     asm volatile("bar.sync 1, %0;" ::"r"(32 * kT2EpiWarps) : "memory");
-    tc_wait(tmem_full, 0);
-    tc_fence_after();
     const int i = m0 + q4 * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
     constexpr int kCols = kT2BN / (kT2EpiWarps / 4);  // columns per epilogue warp
 #ifndef MS_T2_NOEPI
-    tc_epilogue(t, lane_addr, i, tb0, part * kCols, (part + 1) * kCols, tc_skip, tc_out);
+    tc_epilogue(t, lane_addr, i, tb0, part * kCols, (part + 1) * kCols, tc_skip, tc_out, tmem_full);
 #else
+    tc_wait(tmem_full, 0);
+    tc_fence_after();
     (void)lane_addr; (void)i; (void)kCols;
 #endif
   }
