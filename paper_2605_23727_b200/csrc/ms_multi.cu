@@ -29,11 +29,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // K tile maps: [rows][ld] row-major, 64-row x (32*VEC)-column boxes, cached per
 // (K pointer, shape, storage)
-const CUtensorMap& k_map(const void* K, int64_t ld, int rows, int ks) {
+const CUtensorMap& k_map(const void* K, int64_t ld, int rows, int ks, int tr) {
   static std::mutex mu;
-  static std::map<std::tuple<const void*, int64_t, int, int>, CUtensorMap> cache;
+  static std::map<std::tuple<const void*, int64_t, int, int, int>, CUtensorMap> cache;
   std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_tuple(K, ld, rows, ks);
+  const auto key = std::make_tuple(K, ld, rows, ks, tr);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   CUtensorMap m;
@@ -44,7 +44,7 @@ const CUtensorMap& k_map(const void* K, int64_t ld, int rows, int ks) {
   const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * (k16 ? 2 : 4)};
   const cuuint32_t box[2] = {(cuuint32_t)(k16 ? MultiGeom<MS_K_F16>::TC : MultiGeom<MS_K_F32>::TC),
-                             (cuuint32_t)kMultiTR};
+                             (cuuint32_t)tr};
   const cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(K), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -110,8 +110,9 @@ void by_s(int ns, int nds, int ndd, const CUtensorMap& tm, const MultiArgs& m, i
 void launch_rhs_multi(const MultiArgs& m, int ns, int nds, int ndd, int ks, const void* K, int sms, cudaStream_t st) {
   if (ns + nds + ndd != m.nl || m.nl < 1 || m.nl > kMaxLanes) throw std::invalid_argument("rhs_multi: lane count");
   const int rows = m.row1 - m.row0;
-  const CUtensorMap& tm = k_map(K, m.ld, rows, ks);
-  const int groups = (rows + kMultiTR - 1) / kMultiTR;
+  const int tr = m.nl == 1 ? MultiGeom<MS_K_F32, 1>::TR : MultiGeom<MS_K_F32>::TR;
+  const CUtensorMap& tm = k_map(K, m.ld, rows, ks, tr);
+  const int groups = (rows + tr - 1) / tr;
   const int grid = groups < sms ? groups : sms;
   switch (ks) {
     case MS_K_F32: by_s<MS_K_F32>(ns, nds, ndd, tm, m, grid, st); break;

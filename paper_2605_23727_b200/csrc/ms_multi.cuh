@@ -62,16 +62,23 @@ constexpr int kMultiR = MS_MULTI_R;              // rows per consumer warp
 constexpr int kMultiTR = kMultiWarps * kMultiR;  // rows per group / K tile
 constexpr int kMultiThreads = (kMultiWarps + 1) * 32;
 
+#ifndef MS_MULTI_R1
+#define MS_MULTI_R1 2    // rows per warp of the one-lane tile sweep (4 measured slower: C4 f16 5.84 vs 6.1 TB/s)
+#endif
 template <int KS, int NL = kMaxLanes>
 struct MultiGeom {
   using KT = typename KElem<KS>::T;
   static constexpr int VEC = KVec<KS>::N;
   static constexpr int TC = 32 * VEC;                          // tile columns = one warp step
-  static constexpr int KTILE = kMultiTR * TC * (int)sizeof(KT);  // 16 KB
+  // one lane: more rows per warp share each staged sin/cos value (the 16-bit
+  // sweep is shared-memory bound at 2 rows)
+  static constexpr int R = NL == 1 ? MS_MULTI_R1 : kMultiR;
+  static constexpr int TR = kMultiWarps * R;                   // rows per group / K tile
+  static constexpr int KTILE = TR * TC * (int)sizeof(KT);
   static constexpr int LANEB = 2 * TC * 8;                     // s + c at the widest GS
   static constexpr int STAGE = KTILE + NL * LANEB;
-  // ring depth: the largest power of two (cheap modulo) that fits
-  static constexpr int NS = (8 * STAGE <= 200 * 1024) ? 8 : (4 * STAGE <= 200 * 1024 ? 4 : 2);
+  // ring depth: as many stages as fit in ~200 KB, at most 8
+  static constexpr int NS = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
   static constexpr size_t SMEM = (size_t)NS * STAGE + 2 * NS * sizeof(uint64_t) + 128;
 };
 
@@ -109,10 +116,10 @@ __device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* tm, uin
 template <int KS, int NS, int NDS, int NDD, bool CHECK>
 __device__ __forceinline__ void multi_tile(const unsigned char* sk, int warp, int col, int nr,
                                            const bool (&act)[NS + NDS + NDD],
-                                           float (&AS)[NS > 0 ? NS : 1][kMultiR][2],
-                                           double (&AD)[NDS + NDD > 0 ? NDS + NDD : 1][kMultiR][2]) {
+                                           float (&AS)[NS > 0 ? NS : 1][MultiGeom<KS, NS + NDS + NDD>::R][2],
+                                           double (&AD)[NDS + NDD > 0 ? NDS + NDD : 1][MultiGeom<KS, NS + NDS + NDD>::R][2]) {
   using G = MultiGeom<KS, NS + NDS + NDD>;
-  constexpr int VEC = G::VEC, TC = G::TC, R = kMultiR;
+  constexpr int VEC = G::VEC, TC = G::TC, R = G::R;
   // this lane's K vectors of the warp's rows, then one lane type at a time
   float kf[R][VEC];
 #pragma unroll
@@ -178,7 +185,7 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
   constexpr int NL = NS + NDS + NDD;
   static_assert(NL >= 1 && NL <= kMaxLanes, "lane count");
   using G = MultiGeom<KS, NL>;
-  constexpr int VEC = G::VEC, TC = G::TC, R = kMultiR;
+  constexpr int VEC = G::VEC, TC = G::TC, R = G::R, TRW = G::TR;
   bool act[NL];
   bool any = false;
 #pragma unroll
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ld = (int)a.ld;
   const int T = a.row1 - a.row0;
-  const int ngroups = (T + kMultiTR - 1) / kMultiTR;
+  const int ngroups = (T + TRW - 1) / TRW;
   const int my_groups = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int ntiles = (ld + TC - 1) / TC;
   const int Q = my_groups * ntiles;
@@ -215,9 +222,10 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
   if (warp == kMultiWarps) {  // producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
+      int st = 0;
+      uint32_t ph = 0;  // ring slot and its phase, advanced without divisions
       for (int q = 0; q < Q; ++q) {
-        const int st = q % G::NS;
-        if (q >= G::NS) mbar_wait(&empty[st], ((q / G::NS) & 1) ^ 1);
+        if (q >= G::NS) mbar_wait(&empty[st], ph ^ 1);
         const int g = (int)blockIdx.x + (q / ntiles) * (int)gridDim.x;
         const int t = q % ntiles;
         const int cc = min(TC, ld - t * TC);
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
           if (act[v]) bytes += 2u * (uint32_t)cc * (v >= NS + NDS ? 8u : 4u);
         unsigned char* sk = smem + (size_t)st * G::STAGE;
         mbar_expect_tx(&full[st], bytes);
-        tma_tile2d(sk, &tmK, &full[st], t * TC, g * kMultiTR);
+        tma_tile2d(sk, &tmK, &full[st], t * TC, g * TRW);
 #pragma unroll
         for (int v = 0; v < NL; ++v) {
           if (!act[v]) continue;
@@ -237,6 +245,10 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
           bulk_g2s(dst, gp + (size_t)t * TC * es, (uint32_t)cc * es, &full[st]);
           bulk_g2s(dst + (size_t)TC * es, gp + ((size_t)ld + (size_t)t * TC) * es, (uint32_t)cc * es, &full[st]);
         }
+        if (++st == G::NS) {
+          st = 0;
+          ph ^= 1;
+        }
       }
     }
     return;
@@ -245,7 +257,8 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
   bool nonfinite[NL];
 #pragma unroll
   for (int v = 0; v < NL; ++v) nonfinite[v] = false;
-  int q = 0;
+  int st = 0;
+  uint32_t ph = 0;
   const int col = lane * VEC;
   for (int gi = 0; gi < my_groups; ++gi) {
     const int g = (int)blockIdx.x + gi * (int)gridDim.x;
@@ -254,7 +267,7 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const int rl = warp + kMultiWarps * k;
-      const int r = g * kMultiTR + rl;
+      const int r = g * TRW + rl;
       rows[k] = r < T ? rl : -1;
       if (r < T) nr = k + 1;
     }
@@ -268,9 +281,8 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
 #pragma unroll
       for (int v = 0; v < NDS + NDD; ++v) AD[v][k][0] = AD[v][k][1] = 0.0;
     }
-    for (int t = 0; t < ntiles; ++t, ++q) {
-      const int st = q % G::NS;
-      mbar_wait(&full[st], (q / G::NS) & 1);
+    for (int t = 0; t < ntiles; ++t) {
+      mbar_wait(&full[st], ph);
       const unsigned char* sk = smem + (size_t)st * G::STAGE;
       if (nr > 0 && t * TC + col < ld) {
         if (fast) multi_tile<KS, NS, NDS, NDD, false>(sk, warp, col, nr, act, AS, AD);
@@ -278,6 +290,10 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == G::NS) {
+        st = 0;
+        ph ^= 1;
+      }
     }
     // the single sweep's shuffle tree per lane, then lane k writes row k
 #pragma unroll
@@ -299,7 +315,7 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       if (lane != k || k >= nr) continue;
-      const int r = a.row0 + g * kMultiTR + rows[k];
+      const int r = a.row0 + g * TRW + rows[k];
 #pragma unroll
       for (int v = 0; v < NL; ++v) {
         if (!act[v]) continue;
