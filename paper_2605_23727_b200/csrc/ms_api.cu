@@ -439,9 +439,8 @@ PrepArgs prep_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stag
   return p;
 }
 
-bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp) {
+bool launch_prep(ms_system* s, cudaStream_t st, const PrepArgs& p, const ms_stage_prec& sp) {
   const bool fs32 = is32(sp.f_prec), gs32 = is32(sp.g_prec);
-  const PrepArgs p = prep_args(s, B, e, sp);
   const int pgrid = (int)std::max<int64_t>(1, std::min<int64_t>((s->n + 255) / 256, 4 * s->sms));
   if (s->fixture) {
     launch_prep_model<-1>(fs32, gs32, pgrid, st, p);
@@ -455,6 +454,10 @@ bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e
   }
   CK(cudaGetLastError());
   return true;
+}
+
+bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp) {
+  return launch_prep(s, st, prep_args(s, B, e, sp), sp);
 }
 
 RhsArgs rhs_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_prec& sp) {
@@ -514,6 +517,34 @@ void launch_eval(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e
 void launch_eval(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp,
                  cudaEvent_t mid0 = nullptr, cudaEvent_t mid1 = nullptr) {
   launch_eval(s, s->B, st, e, sp, mid0, mid1);
+}
+
+// one evaluation of the row-sharded loop: the finiteness scan of the previous
+// stage's gathered vector (scan, all rows; NULL = none) runs inside the prep,
+// and the sweep, not the prep, counts the evaluation, so an evaluation the scan
+// cancels is not counted (the separate-scan order of the one-GPU loop)
+void launch_scan(ms_system* s, cudaStream_t st, const double* buf, int l);
+
+void launch_eval_loop(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp, const double* scan,
+                      int scan_bit) {
+  PrepArgs p = prep_args(s, s->B, e, sp);
+  // MS_LOOP_SCAN=separate: the unfolded order (a scan launch before the
+  // evaluation, the prep counting) -- the A/B check of the folded one
+  const char* ls = std::getenv("MS_LOOP_SCAN");
+  if (s->fixture || (ls && std::strcmp(ls, "separate") == 0)) {  // fixtures: no sweep to count in
+    if (scan) launch_scan(s, st, scan, scan_bit);
+    if (launch_prep(s, st, p, sp)) launch_sweep(s, st, rhs_args(s, s->B, e, sp), sp);
+    return;
+  }
+  p.scan = scan;
+  p.scan_n = scan ? s->dn() : 0;
+  p.scan_bit = scan_bit;
+  p.count = CNT_NONE;
+  if (!launch_prep(s, st, p, sp)) return;
+  RhsArgs a = rhs_args(s, s->B, e, sp);
+  a.count_ctl = s->B.ctl;
+  a.count = e.count;
+  launch_sweep(s, st, a, sp);
 }
 
 // stage l of an attempt (rk_step, solver.cpp:130-154)
@@ -1031,14 +1062,18 @@ void loop_run(ms_system* s, const SolvePlan& P, int list, int index, cudaStream_
   auto out_of = [&](int l) { return l == S - 1 ? s->B.kb[S] : s->B.kb[l]; };
   const int l = idx + 1;
   if (l < S) {
-    if (l > 1) launch_scan(s, st, out_of(l - 1), l - 1);
-    else if (!P.k1_elided) launch_scan(s, st, s->B.kb[0], 0);
-    launch_eval(s, st, stage_spec(T, l), P.rows[l - 1]);
+    if (l > 1) launch_eval_loop(s, st, stage_spec(T, l), P.rows[l - 1], out_of(l - 1), l - 1);
+    else launch_eval_loop(s, st, stage_spec(T, l), P.rows[l - 1], P.k1_elided ? nullptr : s->B.kb[0], 0);
     set_exch(s, ex, out_of(l));
     return;
   }
   if (l != S) throw InvalidArg("loop: bad attempt segment");
-  launch_scan(s, st, out_of(S - 1), S - 1);
+  // no scan of the gathered last stage: a non-finite element of it makes
+  // x_tilde non-finite (b~_S != 0), and the finalize's any_nf takes the same
+  // reject branch as stage_nf would
+  const char* ls = std::getenv("MS_LOOP_SCAN");
+  if (T.b_tilde[S - 1] == 0.0 || s->fixture || (ls && std::strcmp(ls, "separate") == 0))
+    launch_scan(s, st, out_of(S - 1), S - 1);
   FinArgs f = fin_args(s, s->B, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
   f.fixed_k1 = 1;
   CK(launch_k(k_finalize, s->fin_blocks, s->fin_threads, 0, st, f));

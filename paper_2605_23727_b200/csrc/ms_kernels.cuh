@@ -69,6 +69,11 @@ struct PrepArgs {
   int fs32;       // F precision is binary32 (fixtures: round_to(x, f_prec))
   int ld;         // padded column count
   const double* xsrc;  // PREP_X source (NULL = xb[ix])
+  // row-sharded loop: the finiteness scan of the previous stage's gathered
+  // vector (all rows) folded into this prep; bit scan_bit of nf_mask
+  const double* scan;
+  int64_t scan_n;
+  int scan_bit;
 };
 
 struct RhsArgs {
@@ -86,7 +91,19 @@ struct RhsArgs {
   double mw;
   double coupling_k;
   int ws32;
+  // row-sharded loop: the sweep (not the prep) counts the evaluation, so an
+  // evaluation skipped after the prep's folded scan is not counted
+  Ctl* count_ctl;
+  int count;
 };
+
+__device__ __forceinline__ void sweep_count(const RhsArgs& a) {
+  if (a.count_ctl && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.count == CNT_DDD) a.count_ctl->evals_ddd += 1;
+    else if (a.count == CNT_K1) a.count_ctl->evals_k1 += 1;
+    else if (a.count == CNT_STAGE) a.count_ctl->evals_stage[a.l] += 1;
+  }
+}
 
 __device__ __forceinline__ double* resolve_slot(const Bufs& B, int S, int slot, int k1i) {
   if (slot == SLOT_K1) return B.kb[k1i];
@@ -279,6 +296,12 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs p) {
   const PrepCtx c = prep_ctx(p);
   if (blockIdx.x == 0 && threadIdx.x == 0) prep_count(p, ctl);
   bool nonfinite = false;
+  if (p.scan) {
+    bool bad = false;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.scan_n; e += (int64_t)gridDim.x * blockDim.x)
+      bad |= !isfinite(p.scan[e]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&ctl->nf_mask, 1 << p.scan_bit);
+  }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.md.n; i += gridDim.x * blockDim.x)
     nonfinite |= prep_agent<MODEL, FS, GS>(p, c, i);
   // zero the padding columns [n, ld) of the column data in THIS evaluation's
@@ -466,6 +489,7 @@ template <int MODEL, bool SPLIT, class SS, class GS, int KS>
 __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsArgs a) {
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
+  sweep_count(a);
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NCOL = SPLIT ? 2 : 1;
   constexpr int VEC = KVec<KS>::N;
@@ -865,6 +889,7 @@ template <class SS, class GS, int KS>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(RhsArgs a) {
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
+  sweep_count(a);
   using G = TmaGeom<GS, KS>;
   using KT = typename G::KT;
   constexpr int VEC = KVec<KS>::N;
@@ -1009,6 +1034,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(RhsArgs a) {
 template <int MODEL, class SS, class GS, int KS>
 __global__ void __launch_bounds__(128) k_rhs_faithful(RhsArgs a) {
   if (stage_skip(a.ctl, a.l, a.gate)) return;
+  sweep_count(a);
   const int r = a.row0 + blockIdx.x * blockDim.x + threadIdx.x;
   bool nonfinite = false;
   if (r < a.row1) {

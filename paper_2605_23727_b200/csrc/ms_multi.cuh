@@ -49,6 +49,8 @@ struct MultiArgs {
   int64_t ld;
   int n, row0, row1;
   double mw;
+  Ctl* count_ctl;  // single-lane row-sharded loop: the sweep counts (RhsArgs::count)
+  int count;
 };
 
 #ifndef MS_MULTI_WARPS
@@ -194,6 +196,11 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
     any |= act[v];
   }
   if (!any) return;
+  if (NL == 1 && a.count_ctl && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.count == CNT_DDD) a.count_ctl->evals_ddd += 1;
+    else if (a.count == CNT_K1) a.count_ctl->evals_k1 += 1;
+    else if (a.count == CNT_STAGE) a.count_ctl->evals_stage[a.l] += 1;
+  }
   bool all_act = true;
 #pragma unroll
   for (int v = 0; v < NL; ++v) all_act &= act[v];

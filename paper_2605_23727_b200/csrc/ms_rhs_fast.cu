@@ -42,6 +42,8 @@ void go_tile(const RhsLaunch& L, const RhsArgs& a) {
   m.row0 = a.row0;
   m.row1 = a.row1;
   m.mw = a.mw;
+  m.count_ctl = a.count_ctl;
+  m.count = a.count;
   LaneArgs& ln = m.lane[0];
   ln.ctl = a.ctl;
   ln.nf_mask = a.nf_mask;
