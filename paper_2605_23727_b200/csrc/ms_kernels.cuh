@@ -867,6 +867,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
 #ifndef MS_TMA_KB_K16
 #define MS_TMA_KB_K16 32768
 #endif
+#ifndef MS_TMA_RPW_K16
+#define MS_TMA_RPW_K16 1
+#endif
 constexpr int kTmaConsumers = 16;
 constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
 constexpr int kTmaStages = 4;
@@ -874,7 +877,7 @@ constexpr int kTmaStages = 4;
 template <class GS, int KS>
 struct TmaGeom {
   using KT = typename KElem<KS>::T;
-  static constexpr int RPW = sizeof(GS) == 8 ? MS_TMA_RPW_F64 : MS_TMA_RPW_F32;
+  static constexpr int RPW = sizeof(KT) == 2 ? MS_TMA_RPW_K16 : (sizeof(GS) == 8 ? MS_TMA_RPW_F64 : MS_TMA_RPW_F32);
   static constexpr int RG = kTmaConsumers * RPW;  // rows per group
   static constexpr int KBYTES = sizeof(KT) == 2 ? MS_TMA_KB_K16 : (sizeof(GS) == 8 ? MS_TMA_KB_F64 : MS_TMA_KB_F32);
   static constexpr int TC = KBYTES / (RG * (int)sizeof(KT));   // columns per tile

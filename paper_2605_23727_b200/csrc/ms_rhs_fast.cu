@@ -19,6 +19,11 @@ bool use_tma_sweep_env() {
   const char* v = std::getenv("MS_SWEEP");
   return !(v && std::strcmp(v, "ldg") == 0);
 }
+// 16-bit K through the row-copy TMA sweep (MS_SWEEP=tma16; tuning)
+bool use_tma16_env() {
+  const char* v = std::getenv("MS_SWEEP");
+  return v && std::strcmp(v, "tma16") == 0;
+}
 // 16-bit K at moderate N defaults to the 2D-tile sweep (C2, N = 4096: 53 vs
 // 59-64 us per attempt); at C4 (N = 32768) the register sweep stays ahead
 // (bench: 726 vs 698 steps/s). f32 K keeps the row-copy TMA sweep.
@@ -84,6 +89,12 @@ void go(const RhsLaunch& L, const RhsArgs& a) {
   }
   if constexpr (MODEL == MD_KUR && SPLIT && KS == MS_K_F32) {
     if (use_tma_sweep_env()) {
+      go_tma<SS, GS, KS>(L, a);
+      return;
+    }
+  }
+  if constexpr (MODEL == MD_KUR && SPLIT && (KS == MS_K_F16 || KS == MS_K_BF16)) {
+    if (use_tma16_env()) {
       go_tma<SS, GS, KS>(L, a);
       return;
     }

@@ -93,3 +93,21 @@ def test_c4_device_k_rows_match_generator(gpu):
         ref = (0.0 + 2.0 * _splitmix_uniform(3, 2, idx)).astype(np.float32).astype(np.float64).reshape(8, n)
         assert np.array_equal(part.get_k(), ref)
         part.close()
+
+
+def test_c4_whole_solve_benchmark_policy(c4):
+    """The whole benchmark solve (SSS rows, t in [0, 20]) on the device and in
+    the oracle (OpenMP over rows, bitwise its sequential order; a few minutes):
+    the BASELINE.md §2 gate -- counts within 1 %, final state within 1e-5
+    weighted, else global error vs a tight DP5(4) run no worse than the
+    oracle's."""
+    import time
+    from _gates import gate
+    w, dev, orc = c4
+    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg)
+    t = time.perf_counter()
+    o = O.solve(orc, w.x0, w.t0, w.tf, w.policy, w.cfg)
+    print(f"oracle whole C4 solve: {time.perf_counter() - t:.1f} s on {os.cpu_count()} threads; "
+          f"device {r.device_ms:.1f} ms")
+    assert r.status == o.status == S.SolveStatus.Completed
+    gate(r, o, w.cfg, dev, w)

@@ -48,6 +48,13 @@ VARIANTS = {
     "multi_w20r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 20, "MS_MULTI_R": 2}),
     "multi_w16r4": ("ms_multi.cu", {"MS_MULTI_WARPS": 16, "MS_MULTI_R": 4}),
     "multi_w24r2": ("ms_multi.cu", {"MS_MULTI_WARPS": 24, "MS_MULTI_R": 2}),
+    # cp.async.bulk K sweep with 16-bit K: rows per consumer warp x K bytes per stage
+    "base": ("ms_rhs_fast.cu", {}),
+    "t16_r2_32k": ("ms_rhs_fast.cu", {"MS_TMA_RPW_K16": 2}),
+    "t16_r4_32k": ("ms_rhs_fast.cu", {"MS_TMA_RPW_K16": 4}),
+    "t16_r2_64k": ("ms_rhs_fast.cu", {"MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 65536}),
+    "t16_r4_64k": ("ms_rhs_fast.cu", {"MS_TMA_RPW_K16": 4, "MS_TMA_KB_K16": 65536}),
+    "t16_r1_64k": ("ms_rhs_fast.cu", {"MS_TMA_KB_K16": 65536}),
     "tc2_n256_s3x2_noepi": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_NOEPI": 1}),
 }
 
