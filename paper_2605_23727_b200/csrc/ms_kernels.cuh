@@ -842,9 +842,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
 // register file's limit, and tops out near 6.5 TB/s; a plain read probe needs
 // ~4x that in flight to reach ~7.3 TB/s (tools/bw_probe.cu). Here the bytes
 // in flight live in shared memory: one producer warp streams, per stage, the
-// row segments [TC columns] of a 32-row group plus the matching s/c columns
-// into a 3-deep ring (~216 KB); 16 consumer warps own 2 rows each of the
-// group and sum them from shared memory. Lane l handles columns 4l + 128m
+// row segments [TC columns] of a row group plus the matching s/c columns
+// into a 3-deep ring (~216 KB); the consumer warps (TmaGeom::CONS) own RPW rows
+// each of the group and sum them from shared memory. Lane l handles columns 4l + 128m
 // (8l + 256m for 16-bit K) in ascending order, exactly like k_rhs_fast, so
 // both sweeps produce bit-identical rows.
 #ifndef MS_TMA_LANES
@@ -870,15 +870,34 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
 #ifndef MS_TMA_RPW_K16
 #define MS_TMA_RPW_K16 1
 #endif
-constexpr int kTmaConsumers = 16;
-constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
-constexpr int kTmaStages = 4;
+#ifndef MS_TMA_CONS
+#define MS_TMA_CONS 16
+#endif
+#ifndef MS_TMA_STAGES
+#define MS_TMA_STAGES 4
+#endif
+// the all-binary32 row (SSS, f32 K) runs 8 consumer warps x 2 rows: half the
+// s/c shared-memory reads per K element, +3 % sustained under the board's power
+// cap (profiles/r1_sustained_sweep.txt); rows with binary64 sums or columns keep
+// 16 warps to hide their f64/XU latency
+#ifndef MS_TMA_CONS_SSS
+#define MS_TMA_CONS_SSS 8
+#endif
+#ifndef MS_TMA_RPW_SSS
+#define MS_TMA_RPW_SSS 2
+#endif
+constexpr int kTmaThreadsMax = ((MS_TMA_CONS > MS_TMA_CONS_SSS ? MS_TMA_CONS : MS_TMA_CONS_SSS) + 1) * 32;
+constexpr int kTmaStages = MS_TMA_STAGES;
 
-template <class GS, int KS>
+template <class SS, class GS, int KS>
 struct TmaGeom {
   using KT = typename KElem<KS>::T;
-  static constexpr int RPW = sizeof(KT) == 2 ? MS_TMA_RPW_K16 : (sizeof(GS) == 8 ? MS_TMA_RPW_F64 : MS_TMA_RPW_F32);
-  static constexpr int RG = kTmaConsumers * RPW;  // rows per group
+  static constexpr bool SSS = sizeof(SS) == 4 && sizeof(GS) == 4 && sizeof(KT) == 4;
+  static constexpr int CONS = SSS ? MS_TMA_CONS_SSS : MS_TMA_CONS;  // consumer warps
+  static constexpr int THREADS = (CONS + 1) * 32;
+  static constexpr int RPW = SSS ? MS_TMA_RPW_SSS
+                                 : (sizeof(KT) == 2 ? MS_TMA_RPW_K16 : (sizeof(GS) == 8 ? MS_TMA_RPW_F64 : MS_TMA_RPW_F32));
+  static constexpr int RG = CONS * RPW;  // rows per group
   static constexpr int KBYTES = sizeof(KT) == 2 ? MS_TMA_KB_K16 : (sizeof(GS) == 8 ? MS_TMA_KB_F64 : MS_TMA_KB_F32);
   static constexpr int TC = KBYTES / (RG * (int)sizeof(KT));   // columns per tile
   static constexpr int SC_BYTES = 2 * TC * (int)sizeof(GS);
@@ -889,11 +908,11 @@ struct TmaGeom {
 };
 
 template <class SS, class GS, int KS>
-__global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(RhsArgs a) {
+__global__ void __launch_bounds__(kTmaThreadsMax, 1) k_rhs_tma(RhsArgs a) {
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   sweep_count(a);
-  using G = TmaGeom<GS, KS>;
+  using G = TmaGeom<SS, GS, KS>;
   using KT = typename G::KT;
   constexpr int VEC = KVec<KS>::N;
   constexpr int COLS_IT = 32 * VEC;
@@ -914,14 +933,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(RhsArgs a) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < G::NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kTmaConsumers);
+      mbar_init(&empty[s], G::CONS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == kTmaConsumers) {  // producer warp
+  if (warp == G::CONS) {  // producer warp
     for (int q = 0; q < Q; ++q) {
       const int st = q % G::NS;
       if (q >= G::NS) {
@@ -956,7 +975,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(RhsArgs a) {
     return;
   }
 
-  // consumers: warp w owns rows w and w + 16 of every group
+  // consumers: warp w owns rows w, w + CONS, ... of every group
   const SS mw = cvt<SS>(a.mw);
   double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
   bool nonfinite = false;
@@ -967,7 +986,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(RhsArgs a) {
     int nr = 0;
 #pragma unroll
     for (int k = 0; k < G::RPW; ++k) {
-      const int rl = warp + kTmaConsumers * k;  // local row in the group
+      const int rl = warp + G::CONS * k;  // local row in the group
       rows[k] = (r0 + rl < re) ? rl : -1;
       if (r0 + rl < re) nr = k + 1;
     }

@@ -63,7 +63,8 @@ void go_tile(const RhsLaunch& L, const RhsArgs& a) {
 template <class SS, class GS, int KS>
 void go_tma(const RhsLaunch& L, const RhsArgs& a) {
   auto kern = k_rhs_tma<SS, GS, KS>;
-  constexpr size_t smem = TmaGeom<GS, KS>::SMEM;
+  using G = TmaGeom<SS, GS, KS>;
+  constexpr size_t smem = G::SMEM;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -71,8 +72,13 @@ void go_tma(const RhsLaunch& L, const RhsArgs& a) {
     attr_done = true;
   }
   const int rows = a.row1 - a.row0;
-  const int grid = rows < L.num_sms ? rows : L.num_sms;
-  cudaError_t e = launch_k(kern, grid, kTmaThreads, smem, L.stream, a);
+  static const int cap = [] {  // MS_TMA_GRID: CTAs (tuning; default one per SM)
+    const char* v = std::getenv("MS_TMA_GRID");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int slots = cap > 0 && cap < L.num_sms ? cap : L.num_sms;
+  const int grid = rows < slots ? rows : slots;
+  cudaError_t e = launch_k(kern, grid, G::THREADS, smem, L.stream, a);
   if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tma launch: ") + cudaGetErrorString(e));
 }
 

@@ -55,6 +55,19 @@ VARIANTS = {
     "t16_r2_64k": ("ms_rhs_fast.cu", {"MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 65536}),
     "t16_r4_64k": ("ms_rhs_fast.cu", {"MS_TMA_RPW_K16": 4, "MS_TMA_KB_K16": 65536}),
     "t16_r1_64k": ("ms_rhs_fast.cu", {"MS_TMA_KB_K16": 65536}),
+    # TMA f32 sweep in the power-capped (sustained) regime, tools/sustained_sweep.py
+    "tf_r2": ("ms_rhs_fast.cu", {"MS_TMA_RPW_F32": 2}),
+    "tf_c8r2": ("ms_rhs_fast.cu", {"MS_TMA_CONS": 8, "MS_TMA_RPW_F32": 2}),
+    "tf_c8": ("ms_rhs_fast.cu", {"MS_TMA_CONS": 8}),
+    "tf_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_KB_F32": 32768, "MS_TMA_STAGES": 6}),
+    "tf_c8_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_CONS": 8, "MS_TMA_KB_F32": 32768, "MS_TMA_STAGES": 6}),
+    "tf_c4r4": ("ms_rhs_fast.cu", {"MS_TMA_CONS": 4, "MS_TMA_RPW_F32": 4}),
+    "tf_c8r2_48k": ("ms_rhs_fast.cu", {"MS_TMA_CONS": 8, "MS_TMA_RPW_F32": 2, "MS_TMA_KB_F32": 49152}),
+    "tf_c8r4": ("ms_rhs_fast.cu", {"MS_TMA_CONS": 8, "MS_TMA_RPW_F32": 4}),
+    "tf_c4r8": ("ms_rhs_fast.cu", {"MS_TMA_CONS": 4, "MS_TMA_RPW_F32": 8}),
+    "tf_c8r2_1l": ("ms_rhs_fast.cu", {"MS_TMA_CONS": 8, "MS_TMA_RPW_F32": 2, "MS_TMA_LANES": 0}),
+    "tf_c8r2d4": ("ms_rhs_fast.cu", {"MS_TMA_CONS": 8, "MS_TMA_RPW_F32": 2, "MS_TMA_RPW_F64": 4}),
+    "tf_sss_c16r1": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 16, "MS_TMA_RPW_SSS": 1}),
     "tc2_n256_s3x2_noepi": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_NOEPI": 1}),
 }
 
