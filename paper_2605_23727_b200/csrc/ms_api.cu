@@ -482,6 +482,9 @@ RhsArgs rhs_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_
   a.mw = s->md.m[s->cs];
   a.coupling_k = s->md.coupling_k;
   a.ws32 = (is32(sp.f_prec) && is32(sp.sum_prec)) ? 1 : 0;
+  // K beyond ~3/4 of the 126 MB L2 cannot stay resident between evaluations
+  const int64_t kbytes = (int64_t)(s->row1 - s->row0) * s->ld * (s->ks == MS_K_F32 ? 4 : 2);
+  a.k_stream = (s->ks != MS_K_SCALAR && kbytes > ((int64_t)96 << 20)) ? 1 : 0;
   return a;
 }
 

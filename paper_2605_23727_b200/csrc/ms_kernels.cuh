@@ -95,6 +95,8 @@ struct RhsArgs {
   // evaluation skipped after the prep's folded scan is not counted
   Ctl* count_ctl;
   int count;
+  // K larger than L2 can hold across evaluations: stream it evict-first
+  int k_stream;
 };
 
 __device__ __forceinline__ void sweep_count(const RhsArgs& a) {
@@ -370,11 +372,48 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// the same copy with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint4 ldg_stream(const void* ptr) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(ptr));
+  return r;
+}
+// evict-first K loads in the register sweep: measured -1.5 % on C4 f16 whole
+// solves (profiles/r1_sustained_sweep.txt), so off; the TMA sweep keeps them
+#ifndef MS_LDG_KHINT
+#define MS_LDG_KHINT 0
+#endif
+__device__ __forceinline__ uint4 ldg_stream(const void* ptr, uint64_t pol) {
+  if (!MS_LDG_KHINT) return ldg_stream(ptr);
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr), "l"(pol));
   return r;
 }
 
@@ -540,6 +579,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
   const KT* Kbase = reinterpret_cast<const KT*>(a.K);
   double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
   bool nonfinite = false;
+  const uint64_t kpol = a.k_stream ? l2_evict_first() : l2_evict_normal();
 
   int q = 0;
   for (int sw = 0; sw < nsweeps; ++sw) {
@@ -582,13 +622,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
         uint4 kv[R];
 #pragma unroll
         for (int k = 0; k < R; ++k)
-          if (k < nr && col < cc) kv[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + col);
+          if (k < nr && col < cc) kv[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + col, kpol);
         for (; col < cc; col += COLS_IT) {
           uint4 kn[R];
           const int nc = col + COLS_IT;
 #pragma unroll
           for (int k = 0; k < R; ++k)
-            if (k < nr && nc < cc) kn[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + nc);
+            if (k < nr && nc < cc) kn[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + nc, kpol);
           GS s_loc[VEC], c_loc[VEC];
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
@@ -629,7 +669,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
             uint4 kv[R];
 #pragma unroll
             for (int k = 0; k < R; ++k)
-              if (k < nr) kv[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + col);
+              if (k < nr) kv[k] = ldg_stream(Kbase + (size_t)(rows[k] - a.row0) * ld + c0 + col, kpol);
             sweep_step<MODEL, SPLIT, SS, GS, KS, R, VEC>(kv, nr, s_loc, c_loc, xi, pref, A, B);
           }
         }
@@ -880,6 +920,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
 // s/c shared-memory reads per K element, +3 % sustained under the board's power
 // cap (profiles/r1_sustained_sweep.txt); rows with binary64 sums or columns keep
 // 16 warps to hide their f64/XU latency
+#ifndef MS_TMA_KHINT
+#define MS_TMA_KHINT 1
+#endif
 #ifndef MS_TMA_CONS_SSS
 #define MS_TMA_CONS_SSS 8
 #endif
@@ -941,6 +984,11 @@ __global__ void __launch_bounds__(kTmaThreadsMax, 1) k_rhs_tma(RhsArgs a) {
   __syncthreads();
 
   if (warp == G::CONS) {  // producer warp
+#if MS_TMA_KHINT
+    // K is streamed once per evaluation: evict it first; the s/c columns are
+    // re-read by every CTA
+    const uint64_t pol_k = a.k_stream ? l2_evict_first() : l2_evict_normal(), pol_sc = l2_evict_last();
+#endif
     for (int q = 0; q < Q; ++q) {
       const int st = q % G::NS;
       if (q >= G::NS) {
@@ -958,13 +1006,23 @@ __global__ void __launch_bounds__(kTmaThreadsMax, 1) k_rhs_tma(RhsArgs a) {
       GS* ss = reinterpret_cast<GS*>(sk + G::KBYTES);
       if (lane == 0) {
         mbar_expect_tx(&full[st], kbytes * nr + 2 * sbytes);
+#if MS_TMA_KHINT
+        bulk_g2s_hint(ss, gin + c0, sbytes, &full[st], pol_sc);
+        bulk_g2s_hint(ss + G::TC, gin + (size_t)ld + c0, sbytes, &full[st], pol_sc);
+#else
         bulk_g2s(ss, gin + c0, sbytes, &full[st]);
         bulk_g2s(ss + G::TC, gin + (size_t)ld + c0, sbytes, &full[st]);
+#endif
       }
       if (MS_TMA_LANES) {
         for (int r = lane; r < nr; r += 32)
+#if MS_TMA_KHINT
+          bulk_g2s_hint(sk + (size_t)r * G::TC * sizeof(KT), Kbase + (size_t)(r0 + r - a.row0) * ld + c0, kbytes,
+                        &full[st], pol_k);
+#else
           bulk_g2s(sk + (size_t)r * G::TC * sizeof(KT), Kbase + (size_t)(r0 + r - a.row0) * ld + c0, kbytes,
                    &full[st]);
+#endif
       } else if (lane == 0) {
         for (int r = 0; r < nr; ++r)
           bulk_g2s(sk + (size_t)r * G::TC * sizeof(KT), Kbase + (size_t)(r0 + r - a.row0) * ld + c0, kbytes,
