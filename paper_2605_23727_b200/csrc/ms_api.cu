@@ -460,6 +460,13 @@ bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e
   return launch_prep(s, st, prep_args(s, B, e, sp), sp);
 }
 
+// K beyond ~3/4 of the 126 MB L2 cannot stay resident between evaluations:
+// the sweeps stream it with an evict-first policy
+int k_stream_of(const ms_system* s) {
+  const int64_t kbytes = (int64_t)(s->row1 - s->row0) * s->ld * (s->ks == MS_K_F32 ? 4 : 2);
+  return (s->ks != MS_K_SCALAR && kbytes > ((int64_t)96 << 20)) ? 1 : 0;
+}
+
 RhsArgs rhs_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_prec& sp) {
   RhsArgs a{};
   a.ctl = B.ctl;
@@ -482,9 +489,7 @@ RhsArgs rhs_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_
   a.mw = s->md.m[s->cs];
   a.coupling_k = s->md.coupling_k;
   a.ws32 = (is32(sp.f_prec) && is32(sp.sum_prec)) ? 1 : 0;
-  // K beyond ~3/4 of the 126 MB L2 cannot stay resident between evaluations
-  const int64_t kbytes = (int64_t)(s->row1 - s->row0) * s->ld * (s->ks == MS_K_F32 ? 4 : 2);
-  a.k_stream = (s->ks != MS_K_SCALAR && kbytes > ((int64_t)96 << 20)) ? 1 : 0;
+  a.k_stream = k_stream_of(s);
   return a;
 }
 
@@ -1200,6 +1205,7 @@ void mlaunch_eval(ms_variants* v, cudaStream_t st, const EvalSpec* e, const ms_s
     m.row0 = s->row0;
     m.row1 = s->row1;
     m.mw = s->md.m[s->cs];
+    m.k_stream = k_stream_of(s);
     for (int i = 0; i < np; ++i) {
       const int l = order[i];
       LaneArgs& L = m.lane[i];

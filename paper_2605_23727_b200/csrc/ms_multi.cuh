@@ -51,6 +51,7 @@ struct MultiArgs {
   double mw;
   Ctl* count_ctl;  // single-lane row-sharded loop: the sweep counts (RhsArgs::count)
   int count;
+  int k_stream;    // K beyond L2: evict-first tile loads (RhsArgs::k_stream)
 };
 
 #ifndef MS_MULTI_WARPS
@@ -84,6 +85,9 @@ struct MultiGeom {
   static constexpr size_t SMEM = (size_t)NS * STAGE + 2 * NS * sizeof(uint64_t) + 128;
 };
 
+#ifndef MS_MULTI_KHINT
+#define MS_MULTI_KHINT 1
+#endif
 #ifndef MS_MULTI_INTCVT
 #define MS_MULTI_INTCVT 0
 #endif
@@ -105,6 +109,14 @@ __device__ __forceinline__ double widen(float f) {
 #endif
 }
 
+__device__ __forceinline__ void tma_tile2d_hint(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1,
+                                                uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -229,6 +241,7 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
   if (warp == kMultiWarps) {  // producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
+      const uint64_t kpol = (MS_MULTI_KHINT && a.k_stream) ? l2_evict_first() : l2_evict_normal();
       int st = 0;
       uint32_t ph = 0;  // ring slot and its phase, advanced without divisions
       for (int q = 0; q < Q; ++q) {
@@ -242,7 +255,7 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
           if (act[v]) bytes += 2u * (uint32_t)cc * (v >= NS + NDS ? 8u : 4u);
         unsigned char* sk = smem + (size_t)st * G::STAGE;
         mbar_expect_tx(&full[st], bytes);
-        tma_tile2d(sk, &tmK, &full[st], t * TC, g * TRW);
+        tma_tile2d_hint(sk, &tmK, &full[st], t * TC, g * TRW, kpol);
 #pragma unroll
         for (int v = 0; v < NL; ++v) {
           if (!act[v]) continue;

@@ -49,6 +49,7 @@ void go_tile(const RhsLaunch& L, const RhsArgs& a) {
   m.mw = a.mw;
   m.count_ctl = a.count_ctl;
   m.count = a.count;
+  m.k_stream = a.k_stream;
   LaneArgs& ln = m.lane[0];
   ln.ctl = a.ctl;
   ln.nf_mask = a.nf_mask;

@@ -70,6 +70,7 @@ VARIANTS = {
     "tf_sss_c16r1": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 16, "MS_TMA_RPW_SSS": 1}),
     "tf_khint": ("ms_rhs_fast.cu", {"MS_TMA_KHINT": 1}),
     "hint_off": ("ms_rhs_fast.cu", {"MS_TMA_KHINT": 0, "MS_LDG_KHINT": 0}),
+    "multi_nohint": ("ms_multi.cu", {"MS_MULTI_KHINT": 0}),
     "tc2_n256_s3x2_noepi": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_NOEPI": 1}),
 }
 
