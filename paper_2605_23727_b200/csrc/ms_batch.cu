@@ -70,6 +70,7 @@ struct BFinArgs {
 // attempt ends without a separate condition kernel
 constexpr int kBFinThreads = 256;
 __global__ void __launch_bounds__(kBFinThreads) kb_finalize(BFinArgs f, int has_handle, cudaGraphConditionalHandle h) {
+  pdl_enter();
   const int b = blockIdx.x;
   const BatchDev& d = f.d;
   Ctl* c = d.ctl + b;
@@ -302,17 +303,17 @@ struct BEval {
 template <class FS>
 void launch_bprep(ms_batch* m, cudaStream_t st, const BPrepArgs& p, bool gs32) {
   dim3 grid((m->d.n + 255) / 256, m->B);
-  if (gs32) kb_prep<FS, float><<<grid, 256, 0, st>>>(p);
-  else kb_prep<FS, double><<<grid, 256, 0, st>>>(p);
+  if (gs32) BCK(launch_k(kb_prep<FS, float>, grid, 256, 0, st, p));
+  else BCK(launch_k(kb_prep<FS, double>, grid, 256, 0, st, p));
 }
 
 template <class SS, class GS>
 void launch_brhs_cc(ms_batch* m, cudaStream_t st, const BRhsArgs& a) {
   dim3 grid((m->d.n + kBT_I - 1) / kBT_I, (m->B + kBT_B - 1) / kBT_B);
   switch (m->sv.ks) {
-    case MS_K_F32: kb_rhs_cc<SS, GS, MS_K_F32><<<grid, 256, 0, st>>>(a); break;
-    case MS_K_F16: kb_rhs_cc<SS, GS, MS_K_F16><<<grid, 256, 0, st>>>(a); break;
-    default: kb_rhs_cc<SS, GS, MS_K_BF16><<<grid, 256, 0, st>>>(a); break;
+    case MS_K_F32: BCK(launch_k(kb_rhs_cc<SS, GS, MS_K_F32>, grid, 256, 0, st, a)); break;
+    case MS_K_F16: BCK(launch_k(kb_rhs_cc<SS, GS, MS_K_F16>, grid, 256, 0, st, a)); break;
+    default: BCK(launch_k(kb_rhs_cc<SS, GS, MS_K_BF16>, grid, 256, 0, st, a)); break;
   }
 }
 
@@ -420,8 +421,7 @@ void battempt(ms_batch* m, cudaStream_t st, const BPlan& P, bool has_handle, cud
     ++f.nbt;
   }
   if (f.nbt != 4) throw InvalidArg("batch: finalize expects the four BS3(2) error weights");
-  kb_finalize<<<m->B, kBFinThreads, 0, st>>>(f, has_handle ? 1 : 0, h);
-  BCK(cudaGetLastError());
+  BCK(launch_k(kb_finalize, m->B, kBFinThreads, 0, st, f, has_handle ? 1 : 0, h));
 }
 
 void binit(ms_batch* m, cudaStream_t st, const BPlan& P) {

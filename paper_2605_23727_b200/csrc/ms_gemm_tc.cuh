@@ -32,6 +32,7 @@
 #include <string>
 
 #include "ms_batch.cuh"
+#include "ms_dispatch.h"
 
 namespace msb {
 
@@ -381,6 +382,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
   cluster_sync_all();  // the peer's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the prologue above (barriers, TMEM, tensor-map prefetch) overlaps the
+  // prep's tail; everything below reads what the prep wrote. The successor is
+  // not released early (its blocks would sit on the SMs through the mainloop)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer (both CTAs): own smem, completion on the leader's barrier
@@ -538,7 +543,8 @@ inline void launch_tc_gemm(const TcGemm& g, const BRhsArgs& a, cudaStream_t st) 
   dim3 grid(g.grid_m, g.grid_n);
   if (g.pair) {
     t.idesc = tc_idesc(a.d.ks, 2 * kT2BM);
-    k_tc_gemm2<<<grid, kT2Threads, kT2Smem, st>>>(g.tmA, g.tmB2, t);
+    cudaError_t e = launch_k(k_tc_gemm2, grid, kT2Threads, kT2Smem, st, g.tmA, g.tmB2, t);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("tc gemm2 launch: ") + cudaGetErrorString(e));
   } else {
     t.idesc = tc_idesc(a.d.ks, kTcBM);
     k_tc_gemm<<<grid, kTcThreads, kTcSmem, st>>>(g.tmA, g.tmB, t);
