@@ -307,6 +307,32 @@ void launch_bprep(ms_batch* m, cudaStream_t st, const BPrepArgs& p, bool gs32) {
   else BCK(launch_k(kb_prep<FS, double>, grid, 256, 0, st, p));
 }
 
+// the specialised tensor-core stage prep (kb_prep_tc); false = not applicable
+template <int OPKS>
+bool launch_bprep_tc_ks(ms_batch* m, cudaStream_t st, const BPrepArgs& p) {
+  dim3 grid((m->d.n + 256 * kPrepTcElems - 1) / (256 * kPrepTcElems), m->B);
+  auto go = [&](auto kern) { BCK(launch_k(kern, grid, 256, 0, st, p)); return true; };
+  if (p.is_last) {
+    if (p.nterms == 1) return go(kb_prep_tc<OPKS, 1, true>);
+    if (p.nterms == 2) return go(kb_prep_tc<OPKS, 2, true>);
+    if (p.nterms == 3) return go(kb_prep_tc<OPKS, 3, true>);
+  } else {
+    if (p.nterms == 1) return go(kb_prep_tc<OPKS, 1, false>);
+    if (p.nterms == 2) return go(kb_prep_tc<OPKS, 2, false>);
+    if (p.nterms == 3) return go(kb_prep_tc<OPKS, 3, false>);
+  }
+  return false;
+}
+
+bool launch_bprep_tc(ms_batch* m, cudaStream_t st, const BPrepArgs& p) {
+  const char* v = std::getenv("MS_PREP_TC");  // read per launch (graphs capture it once)
+  const bool on = !(v && std::strcmp(v, "0") == 0);
+  if (!on || !MS_TC_PACKED || p.kind != PREP_STAGE || p.count != CNT_STAGE || !p.fs32) return false;
+  if (p.op_ks == MS_K_BF16) return launch_bprep_tc_ks<MS_K_BF16>(m, st, p);
+  if (p.op_ks == MS_K_F16) return launch_bprep_tc_ks<MS_K_F16>(m, st, p);
+  return false;
+}
+
 template <class SS, class GS>
 void launch_brhs_cc(ms_batch* m, cudaStream_t st, const BRhsArgs& a) {
   dim3 grid((m->d.n + kBT_I - 1) / kBT_I, (m->B + kBT_B - 1) / kBT_B);
@@ -339,8 +365,10 @@ void beval(ms_batch* m, cudaStream_t st, const BEval& e, const ms_stage_prec& sp
   p.ws32 = fs32 && ss32;
   p.fs32 = fs32;
   p.op_ks = use_tc ? m->op_ks : 0;
-  if (fs32) launch_bprep<float>(m, st, p, gs32);
-  else launch_bprep<double>(m, st, p, gs32);
+  if (!(use_tc && launch_bprep_tc(m, st, p))) {
+    if (fs32) launch_bprep<float>(m, st, p, gs32);
+    else launch_bprep<double>(m, st, p, gs32);
+  }
   BCK(cudaGetLastError());
   BRhsArgs a{};
   a.d = m->d;

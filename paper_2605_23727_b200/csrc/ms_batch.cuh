@@ -170,6 +170,88 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
   bprep_elem<FS, GS>(p, b, i, c);
 }
 
+// The tensor-core path's stage prep (binary32 row, BS3 stage with NT terms,
+// LAST = the x_next stage), specialised: the trajectory's pointers and h are
+// resolved once per block into shared memory, each thread prepares
+// kPrepTcElems elements. Same arithmetic as bprep_elem<float, float> (bitwise;
+// MS_PREP_TC=0 keeps the generic kernel).
+constexpr int kPrepTcElems = 2;
+template <int OPKS, int NT, bool LAST>
+__global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
+  pdl_enter();
+  const int b = blockIdx.y;
+  const BatchDev& d = p.d;
+  Ctl* c = d.ctl + b;
+  struct Row {
+    const double* x;
+    const double* k[NT];
+    double* xst;
+    double* xn;
+    double h;
+    int store32;
+  };
+  __shared__ Row row;
+  __shared__ int skip;
+  if (threadIdx.x == 0) {
+    skip = stage_skip(c, p.l, p.gate) ? 1 : 0;
+    if (!skip) {
+      if (blockIdx.x == 0) c->evals_stage[p.l] += 1;  // CNT_STAGE
+      const int64_t o = (int64_t)b * d.n;
+      const int ix = c->ix;
+      row.x = d.xb[ix] + o;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) row.k[t] = bslot(d, p.S, p.slot[t], c) + o;
+      row.xst = d.xb[ix ^ 1] + o;
+      row.xn = d.xn + o;
+      row.h = c->h_att;
+      row.store32 = c->store32;
+    }
+  }
+  __syncthreads();
+  if (skip) return;
+  using T = typename K16<OPKS>::T;
+  T* op = reinterpret_cast<T*>(d.op) + (int64_t)b * 4 * d.ld;
+  TcRec* rec = reinterpret_cast<TcRec*>(d.sc) + (int64_t)b * d.n;
+  const double* om = d.omega + (int64_t)b * d.n;
+  const double h = row.h;
+#pragma unroll
+  for (int u = 0; u < kPrepTcElems; ++u) {
+    const int i = (blockIdx.x * kPrepTcElems + u) * blockDim.x + threadIdx.x;
+    if (i >= d.n) break;
+    double cm = __dmul_rn(p.coef[0], row.k[0][i]);
+#pragma unroll
+    for (int t = 1; t < NT; ++t) cm = __dadd_rn(cm, __dmul_rn(p.coef[t], row.k[t][i]));
+    const double xi = row.x[i];
+    double v = __dadd_rn(xi, __dmul_rn(h, cm));
+    if (LAST) {
+      if (row.store32) {
+        const float hf = __double2float_rn(h);
+        float acc = __double2float_rn(xi);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const float cf = __fmul_rn(hf, __double2float_rn(p.coef[t]));
+          acc = __fadd_rn(acc, __fmul_rn(cf, __double2float_rn(row.k[t][i])));
+        }
+        row.xn[i] = v;
+        v = (double)acc;
+      }
+      row.xst[i] = v;
+    }
+    float sv, cv;
+    dsincos(__double2float_rn(v), &sv, &cv);
+    TcRec r;
+    r.s = sv;
+    r.c = cv;
+    r.f = (double)__double2float_rn(om[i]);  // b_fval, fs32
+    rec[i] = r;
+    const T sh = K16<OPKS>::from(sv), ch = K16<OPKS>::from(cv);
+    op[i] = sh;
+    op[d.ld + i] = K16<OPKS>::from(__fsub_rn(sv, (float)sh));
+    op[2 * d.ld + i] = ch;
+    op[3 * d.ld + i] = K16<OPKS>::from(__fsub_rn(cv, (float)ch));
+  }
+}
+
 struct BRhsArgs {
   BatchDev d;
   int S, l, gate, out_slot, ws32, fs32;

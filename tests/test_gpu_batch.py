@@ -135,3 +135,31 @@ def test_batch_solve_vs_oracle(gpu, tc):
     assert abs(tot["dev_rej"] - tot["orc_rej"]) <= max(2, 0.02 * tot["att"])
     assert abs(tot["dev_acc"] - tot["orc_acc"]) <= max(2, 0.01 * tot["orc_acc"])
     assert res.attempts >= int(max(res.n_accepted + res.n_failed))
+
+
+@pytest.mark.parametrize("ks", ["bf16", "f16"])
+@pytest.mark.parametrize("pol", ["SSS_D", "Single", "Mixed1"])
+def test_batch_tc_specialised_prep_is_bitwise(gpu, monkeypatch, ks, pol):
+    """The tensor-core path's specialised stage prep (kb_prep_tc) against the
+    generic kb_prep (MS_PREP_TC=0): identical ensembles, bit for bit."""
+    from paper_2605_23727_b200.configs import SSS_D
+    from paper_2605_23727_b200.precision import PolicyVariant, policy_for
+    from paper_2605_23727_b200.solver import SolverConfig
+    B, n = 40, 256
+    spec, omega, x0 = _ensemble(B, n, ks, seed=11)
+    policy = SSS_D if pol == "SSS_D" else policy_for(getattr(PolicyVariant, pol))
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    dev = DeviceSystem(spec)
+    runs = []
+    for mode in ("generic", "specialised"):
+        if mode == "generic":
+            monkeypatch.setenv("MS_PREP_TC", "0")
+        else:
+            monkeypatch.delenv("MS_PREP_TC", raising=False)
+        runs.append(DeviceBatch(dev, omega, tensor_cores=True).solve(x0, 0.0, 3.0, policy, cfg))
+    a, b = runs
+    assert list(a.status) == list(b.status)
+    assert np.array_equal(a.n_accepted, b.n_accepted) and np.array_equal(a.n_failed, b.n_failed)
+    assert np.array_equal(a.rhs_evals, b.rhs_evals)
+    assert np.array_equal(a.final_state, b.final_state)
+    assert np.array_equal(a.t_reached, b.t_reached)
