@@ -172,10 +172,15 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
 
 // The tensor-core path's stage prep (binary32 row, BS3 stage with NT terms,
 // LAST = the x_next stage), specialised: the trajectory's pointers and h are
-// resolved once per block into shared memory, each thread prepares
-// kPrepTcElems elements. Same arithmetic as bprep_elem<float, float> (bitwise;
-// MS_PREP_TC=0 keeps the generic kernel).
-constexpr int kPrepTcElems = 2;
+// resolved once per block into shared memory, and each thread first loads the
+// inputs of its kPrepTcElems elements (read-only path), then prepares them —
+// the generic prep is latency-bound on one element's dependent loads. Same
+// arithmetic as bprep_elem<float, float> (bitwise; MS_PREP_TC=0 keeps the
+// generic kernel).
+#ifndef MS_PREP_TC_ELEMS
+#define MS_PREP_TC_ELEMS 4
+#endif
+constexpr int kPrepTcElems = MS_PREP_TC_ELEMS;
 template <int OPKS, int NT, bool LAST>
 __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
   pdl_enter();
@@ -214,23 +219,34 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
   TcRec* rec = reinterpret_cast<TcRec*>(d.sc) + (int64_t)b * d.n;
   const double* om = d.omega + (int64_t)b * d.n;
   const double h = row.h;
+  const int i0 = blockIdx.x * kPrepTcElems * blockDim.x + threadIdx.x;
+  double xv[kPrepTcElems], kv[kPrepTcElems][NT], wv[kPrepTcElems];
 #pragma unroll
   for (int u = 0; u < kPrepTcElems; ++u) {
-    const int i = (blockIdx.x * kPrepTcElems + u) * blockDim.x + threadIdx.x;
-    if (i >= d.n) break;
-    double cm = __dmul_rn(p.coef[0], row.k[0][i]);
+    const int i = i0 + u * blockDim.x;
+    if (i < d.n) {
+      xv[u] = __ldg(row.x + i);
 #pragma unroll
-    for (int t = 1; t < NT; ++t) cm = __dadd_rn(cm, __dmul_rn(p.coef[t], row.k[t][i]));
-    const double xi = row.x[i];
-    double v = __dadd_rn(xi, __dmul_rn(h, cm));
+      for (int t = 0; t < NT; ++t) kv[u][t] = __ldg(row.k[t] + i);
+      wv[u] = __ldg(om + i);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kPrepTcElems; ++u) {
+    const int i = i0 + u * blockDim.x;
+    if (i >= d.n) break;
+    double cm = __dmul_rn(p.coef[0], kv[u][0]);
+#pragma unroll
+    for (int t = 1; t < NT; ++t) cm = __dadd_rn(cm, __dmul_rn(p.coef[t], kv[u][t]));
+    double v = __dadd_rn(xv[u], __dmul_rn(h, cm));
     if (LAST) {
       if (row.store32) {
         const float hf = __double2float_rn(h);
-        float acc = __double2float_rn(xi);
+        float acc = __double2float_rn(xv[u]);
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const float cf = __fmul_rn(hf, __double2float_rn(p.coef[t]));
-          acc = __fadd_rn(acc, __fmul_rn(cf, __double2float_rn(row.k[t][i])));
+          acc = __fadd_rn(acc, __fmul_rn(cf, __double2float_rn(kv[u][t])));
         }
         row.xn[i] = v;
         v = (double)acc;
@@ -242,7 +258,7 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
     TcRec r;
     r.s = sv;
     r.c = cv;
-    r.f = (double)__double2float_rn(om[i]);  // b_fval, fs32
+    r.f = (double)__double2float_rn(wv[u]);  // b_fval, fs32
     rec[i] = r;
     const T sh = K16<OPKS>::from(sv), ch = K16<OPKS>::from(cv);
     op[i] = sh;

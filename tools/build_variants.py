@@ -71,6 +71,9 @@ VARIANTS = {
     "tf_khint": ("ms_rhs_fast.cu", {"MS_TMA_KHINT": 1}),
     "hint_off": ("ms_rhs_fast.cu", {"MS_TMA_KHINT": 0, "MS_LDG_KHINT": 0}),
     "multi_nohint": ("ms_multi.cu", {"MS_MULTI_KHINT": 0}),
+    "prep_e2": ("ms_batch.cu", {"MS_PREP_TC_ELEMS": 2}),
+    "prep_e4": ("ms_batch.cu", {"MS_PREP_TC_ELEMS": 4}),
+    "prep_e8": ("ms_batch.cu", {"MS_PREP_TC_ELEMS": 8}),
     "tc2_n256_s3x2_noepi": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_NOEPI": 1}),
 }
 
