@@ -69,7 +69,12 @@ struct BFinArgs {
 // the last CTA to finish (ticket) also evaluates the loop condition, so an
 // attempt ends without a separate condition kernel
 constexpr int kBFinThreads = 256;
-__global__ void __launch_bounds__(kBFinThreads) kb_finalize(BFinArgs f, int has_handle, cudaGraphConditionalHandle h) {
+// resident blocks per SM: 8 caps registers at 32 so all B = 1024 trajectory
+// blocks run in one wave (61 registers gave 4 blocks per SM, 1.7 waves)
+#ifndef MS_BFIN_MINB
+#define MS_BFIN_MINB 8
+#endif
+__global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinArgs f, int has_handle, cudaGraphConditionalHandle h) {
   pdl_enter();
   const int b = blockIdx.x;
   const BatchDev& d = f.d;

@@ -74,6 +74,9 @@ VARIANTS = {
     "prep_e2": ("ms_batch.cu", {"MS_PREP_TC_ELEMS": 2}),
     "prep_e4": ("ms_batch.cu", {"MS_PREP_TC_ELEMS": 4}),
     "prep_e8": ("ms_batch.cu", {"MS_PREP_TC_ELEMS": 8}),
+    "fin_m4": ("ms_batch.cu", {"MS_BFIN_MINB": 1}),
+    "fin_m6": ("ms_batch.cu", {"MS_BFIN_MINB": 6}),
+    "fin_m8": ("ms_batch.cu", {"MS_BFIN_MINB": 8}),
     "tc2_n256_s3x2_noepi": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_NOEPI": 1}),
 }
 
