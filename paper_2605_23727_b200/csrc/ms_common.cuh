@@ -70,6 +70,26 @@ template <> __device__ __forceinline__ double sub<double>(double a, double b) { 
 template <> __device__ __forceinline__ double mul<double>(double a, double b) { return __dmul_rn(a, b); }
 template <> __device__ __forceinline__ double dvd<double>(double a, double b) { return __ddiv_rn(a, b); }
 
+// (a, b) = (a + x, b + y): two independent single-rounding adds. For binary32
+// one packed FADD2 (sm_100): the same two IEEE adds in one issue slot. The
+// products fed in must come from scalar mul.rn (FMUL): ptxas contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under -fmad=false, but never a
+// scalar mul.rn into a packed add (checked in the SASS, tests/test_abi.py).
+template <class S, bool PACK = true> __device__ __forceinline__ void add2(S& a, S& b, S x, S y) {
+#ifndef MS_NO_FADD2
+  if constexpr (PACK && sizeof(S) == 4) {
+    unsigned long long acc, p;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(a), "f"(b));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(x), "f"(y));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(p));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(acc));
+    return;
+  }
+#endif
+  a = add<S>(a, x);
+  b = add<S>(b, y);
+}
+
 // RN into S of a double
 template <class S> __device__ __forceinline__ S cvt(double x);
 template <> __device__ __forceinline__ float cvt<float>(double x) { return __double2float_rn(x); }

@@ -473,6 +473,10 @@ template <> struct KVec<MS_K_SCALAR> {
 #ifndef MS_NS
 #define MS_NS 4              // mbarrier ring depth
 #endif
+#ifndef MS_FAST_FADD2
+#define MS_FAST_FADD2 0      // packed FADD2 accumulation in the register sweep: measured slower (f16 K)
+#endif
+constexpr bool kFastFadd2 = MS_FAST_FADD2;
 constexpr int kFastThreads = MS_FAST_THREADS;
 constexpr int kFastMinBlocks = MS_FAST_MINB;
 constexpr int kFastWarps = kFastThreads / 32;
@@ -504,8 +508,7 @@ __device__ __forceinline__ void sweep_step(const uint4 (&kv)[R], int nr, const G
       for (int v = 0; v < VEC; ++v) {
         const GS kg = (GS)kf[v];
         if (SPLIT) {
-          A[k] = add<SS>(A[k], (SS)mul<GS>(kg, s_loc[v]));
-          B[k] = add<SS>(B[k], (SS)mul<GS>(kg, c_loc[v]));
+          add2<SS, kFastFadd2>(A[k], B[k], (SS)mul<GS>(kg, s_loc[v]), (SS)mul<GS>(kg, c_loc[v]));
         } else {
           GS g;
           if (MODEL == MD_LCO) g = mul<GS>(kg, sub<GS>(s_loc[v], xi[k]));
@@ -655,8 +658,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
 #pragma unroll
               for (int v = 0; v < VEC; ++v) {
                 if (SPLIT) {
-                  A[k] = add<SS>(A[k], (SS)mul<GS>(kscal, s_loc[v]));
-                  B[k] = add<SS>(B[k], (SS)mul<GS>(kscal, c_loc[v]));
+                  add2<SS, kFastFadd2>(A[k], B[k], (SS)mul<GS>(kscal, s_loc[v]), (SS)mul<GS>(kscal, c_loc[v]));
                 } else if (c0 + col + v < a.n) {
                   GS g;
                   if (MODEL == MD_LCO) g = mul<GS>(kscal, sub<GS>(s_loc[v], xi[k]));
@@ -829,8 +831,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
 #pragma unroll
             for (int v = 0; v < VEC; ++v) {
               if (SPLIT) {
-                A[k] = add<SS>(A[k], (SS)mul<GS>(kscal, s_loc[v]));
-                B[k] = add<SS>(B[k], (SS)mul<GS>(kscal, c_loc[v]));
+                add2<SS, kFastFadd2>(A[k], B[k], (SS)mul<GS>(kscal, s_loc[v]), (SS)mul<GS>(kscal, c_loc[v]));
               } else if (col + v < a.n) {
                 GS g;
                 if (MODEL == MD_LCO) g = mul<GS>(kscal, sub<GS>(s_loc[v], xi[k]));
@@ -905,13 +906,16 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
 #define MS_TMA_KB_F64 65536
 #endif
 #ifndef MS_TMA_KB_K16
-#define MS_TMA_KB_K16 32768
+#define MS_TMA_KB_K16 65536
 #endif
 #ifndef MS_TMA_RPW_K16
-#define MS_TMA_RPW_K16 1
+#define MS_TMA_RPW_K16 4
 #endif
 #ifndef MS_TMA_CONS
 #define MS_TMA_CONS 16
+#endif
+#ifndef MS_TMA_CONS_K16
+#define MS_TMA_CONS_K16 8
 #endif
 #ifndef MS_TMA_STAGES
 #define MS_TMA_STAGES 4
@@ -929,14 +933,19 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
 #ifndef MS_TMA_RPW_SSS
 #define MS_TMA_RPW_SSS 2
 #endif
-constexpr int kTmaThreadsMax = ((MS_TMA_CONS > MS_TMA_CONS_SSS ? MS_TMA_CONS : MS_TMA_CONS_SSS) + 1) * 32;
+constexpr int kTmaConsMax = MS_TMA_CONS > MS_TMA_CONS_SSS ? MS_TMA_CONS : MS_TMA_CONS_SSS;
+constexpr int kTmaThreadsMax = ((kTmaConsMax > MS_TMA_CONS_K16 ? kTmaConsMax : MS_TMA_CONS_K16) + 1) * 32;
 constexpr int kTmaStages = MS_TMA_STAGES;
+#ifndef MS_TMA_UNROLL
+#define MS_TMA_UNROLL 4    // column steps unrolled in the full-tile consumer loop
+#endif
+constexpr int kTmaUnroll = MS_TMA_UNROLL;
 
 template <class SS, class GS, int KS>
 struct TmaGeom {
   using KT = typename KElem<KS>::T;
   static constexpr bool SSS = sizeof(SS) == 4 && sizeof(GS) == 4 && sizeof(KT) == 4;
-  static constexpr int CONS = SSS ? MS_TMA_CONS_SSS : MS_TMA_CONS;  // consumer warps
+  static constexpr int CONS = SSS ? MS_TMA_CONS_SSS : (sizeof(KT) == 2 ? MS_TMA_CONS_K16 : MS_TMA_CONS);  // consumer warps
   static constexpr int THREADS = (CONS + 1) * 32;
   static constexpr int RPW = SSS ? MS_TMA_RPW_SSS
                                  : (sizeof(KT) == 2 ? MS_TMA_RPW_K16 : (sizeof(GS) == 8 ? MS_TMA_RPW_F64 : MS_TMA_RPW_F32));
@@ -949,6 +958,35 @@ struct TmaGeom {
   static constexpr size_t SMEM = (size_t)NS * STAGE_BYTES + 2 * kTmaStages * sizeof(uint64_t) + 128;
   static_assert(TC % (32 * KVec<KS>::N) == 0, "tile width must be a whole number of warp steps");
 };
+
+// One warp step of the TMA sweep: lane columns [col, col + VEC) of the
+// staged tile against each of the warp's rows (A += K s, B += K c; ascending
+// columns per lane, as in k_rhs_fast).
+template <class SS, class GS, int KS, int RPW, int TC, bool CHECK>
+__device__ __forceinline__ void tma_col_step(const unsigned char* sk, const GS* sv, const GS* cv, int col,
+                                             const int (&rows)[RPW], int nr, SS (&A)[RPW], SS (&B)[RPW]) {
+  using KT = typename KElem<KS>::T;
+  constexpr int VEC = KVec<KS>::N;
+  GS s_loc[VEC], c_loc[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    s_loc[v] = sv[col + v];
+    c_loc[v] = cv[col + v];
+  }
+#pragma unroll
+  for (int k = 0; k < RPW; ++k) {
+    if (!CHECK || k < nr) {
+      const uint4 kv = *reinterpret_cast<const uint4*>(sk + ((size_t)rows[k] * TC + col) * sizeof(KT));
+      float kf[VEC];
+      KVec<KS>::unpack(kv, kf);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const GS kg = (GS)kf[v];
+        add2<SS>(A[k], B[k], (SS)mul<GS>(kg, s_loc[v]), (SS)mul<GS>(kg, c_loc[v]));
+      }
+    }
+  }
+}
 
 template <class SS, class GS, int KS>
 __global__ void __launch_bounds__(kTmaThreadsMax, 1) k_rhs_tma(RhsArgs a) {
@@ -1058,29 +1096,15 @@ __global__ void __launch_bounds__(kTmaThreadsMax, 1) k_rhs_tma(RhsArgs a) {
       const unsigned char* sk = smem + (size_t)st * G::STAGE_BYTES;
       const GS* sv = reinterpret_cast<const GS*>(sk + G::KBYTES);
       const GS* cv = sv + G::TC;
-      if (nr > 0) {
-        for (int col = lane * VEC; col < cc; col += COLS_IT) {
-          GS s_loc[VEC], c_loc[VEC];
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            s_loc[v] = sv[col + v];
-            c_loc[v] = cv[col + v];
-          }
-#pragma unroll
-          for (int k = 0; k < G::RPW; ++k) {
-            if (k < nr) {
-              const uint4 kv = *reinterpret_cast<const uint4*>(sk + ((size_t)rows[k] * G::TC + col) * sizeof(KT));
-              float kf[VEC];
-              KVec<KS>::unpack(kv, kf);
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) {
-                const GS kg = (GS)kf[v];
-                A[k] = add<SS>(A[k], (SS)mul<GS>(kg, s_loc[v]));
-                B[k] = add<SS>(B[k], (SS)mul<GS>(kg, c_loc[v]));
-              }
-            }
-          }
-        }
+      if (nr == G::RPW && cc == G::TC) {
+        // full tile, every row valid: a fixed trip count the compiler unrolls,
+        // so the shared-memory loads of later column steps are issued ahead
+#pragma unroll kTmaUnroll
+        for (int it = 0; it < G::TC / COLS_IT; ++it)
+          tma_col_step<SS, GS, KS, G::RPW, G::TC, false>(sk, sv, cv, lane * VEC + it * COLS_IT, rows, nr, A, B);
+      } else if (nr > 0) {
+        for (int col = lane * VEC; col < cc; col += COLS_IT)
+          tma_col_step<SS, GS, KS, G::RPW, G::TC, true>(sk, sv, cv, col, rows, nr, A, B);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);

@@ -161,8 +161,7 @@ __device__ __forceinline__ void multi_tile(const unsigned char* sk, int warp, in
       for (int e = 0; e < VEC; ++e) {
         const float ps = __fmul_rn(kf[k][e], s0[e]), pc = __fmul_rn(kf[k][e], c0[e]);
         if (v < NS) {
-          AS[v][k][0] = __fadd_rn(AS[v][k][0], ps);
-          AS[v][k][1] = __fadd_rn(AS[v][k][1], pc);
+          add2<float>(AS[v][k][0], AS[v][k][1], ps, pc);
         } else {
           AD[v - NS][k][0] = __dadd_rn(AD[v - NS][k][0], (double)ps);
           AD[v - NS][k][1] = __dadd_rn(AD[v - NS][k][1], widen(pc));

@@ -91,3 +91,19 @@ def test_invalid_descriptors_are_rejected_before_device_work():
         DeviceSystem(SystemSpec("kuramoto", 0, omega=np.zeros(1)))
     with pytest.raises(ValueError):
         DeviceSystem(SystemSpec("kuramoto", 4))  # omega missing
+
+
+def test_library_sass_has_no_packed_fma():
+    """The arithmetic contract forbids contracting a product into a sum. The
+    sweeps accumulate with packed add.rn.f32x2 (FADD2) fed by scalar mul.rn;
+    ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under
+    -fmad=false, so no packed multiply may reach a packed add: no FFMA2 in
+    the shipped SASS."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(tool).exists():
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", str(_abi.LIB_PATH)], capture_output=True, text=True, check=True).stdout
+    assert "FADD2" in sass  # the packed accumulation is in use
+    assert "FFMA2" not in sass

@@ -78,6 +78,24 @@ VARIANTS = {
     "fin_m6": ("ms_batch.cu", {"MS_BFIN_MINB": 6}),
     "fin_m8": ("ms_batch.cu", {"MS_BFIN_MINB": 8}),
     "tc2_n256_s3x2_noepi": ("ms_batch.cu", {"MS_T2_BN": 256, "MS_T2_STAGES": 3, "MS_T2_MINB": 2, "MS_T2_NOEPI": 1}),
+    # packed FADD2 accumulation (ms_common.cuh add2) and the 16-bit K TMA sweep geometry
+    "nofadd2": ("ms_rhs_fast.cu", {"MS_NO_FADD2": 1}),
+    "k16_c8r2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 8, "MS_TMA_RPW_K16": 2}),
+    "k16_c8r2_64k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 8, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 65536}),
+    "k16_c8r2_64k_nofadd2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 8, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 65536,
+                                                "MS_NO_FADD2": 1}),
+    "k16_c8r4_64k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 8, "MS_TMA_RPW_K16": 4, "MS_TMA_KB_K16": 65536}),
+    "k16_c16r2_64k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 16, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 65536}),
+    "k16_c4r4_64k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 4, "MS_TMA_RPW_K16": 4, "MS_TMA_KB_K16": 65536}),
+    "u1": ("ms_rhs_fast.cu", {"MS_TMA_UNROLL": 1}),
+    "u2": ("ms_rhs_fast.cu", {"MS_TMA_UNROLL": 2}),
+    "u8": ("ms_rhs_fast.cu", {"MS_TMA_UNROLL": 8}),
+    "k16_c16r2_64k_u2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 16, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 65536,
+                                            "MS_TMA_UNROLL": 2}),
+    "k16_c16r2_64k_nofadd2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 16, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 65536,
+                                                 "MS_NO_FADD2": 1}),
+    "fast_fadd2": ("ms_rhs_fast.cu", {"MS_FAST_FADD2": 1}),
+    "k16_c12r2_48k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 12, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 49152}),
 }
 
 

@@ -40,7 +40,8 @@ print("JSON" + json.dumps({"burst_GBps": nbytes / b / 1e6, "sustained_GBps": nby
 def main(specs):
     for spec in specs or ["tma", "ldg", "tile"]:
         mode, _, lib = spec.partition(":")
-        for ks in ("f32",) if mode == "tma" else ("f32", "f16"):
+        kss = os.environ.get("SW_KS", "f32" if mode == "tma" else "f32,f16")
+        for ks in kss.split(","):
             env = dict(os.environ, MS_SWEEP=mode)
             if lib:
                 env["MS_LIB_PATH"] = str(ROOT / "paper_2605_23727_b200" / "_variants" / f"lib_{lib}.so")
