@@ -548,7 +548,7 @@ int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t vec = al(sizeof(double) * bn);
     size_t total = vec /*omega*/ + 2 * vec + (kMaxStages + 1) * vec + 3 * vec /*xn, scr0, scr1*/ +
-                   2 * vec /*sc*/ + al(sizeof(uint16_t) * 4 * (size_t)batch * ld) /*op*/ + vec /*fvc*/ +
+                   2 * vec /*sc*/ + al(sizeof(uint16_t) * 4 * (size_t)batch * ld) /*op*/ + vec /*fvc*/ + 2 * vec /*rec*/ +
                    al(sizeof(Ctl) * batch) + al(sizeof(int));
     char* base = nullptr;
     BCK(cudaMalloc(&base, total));
@@ -576,11 +576,18 @@ int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t
     d.sc = take(sizeof(double) * 2 * bn);
     d.op = take(sizeof(uint16_t) * 4 * (size_t)batch * ld);
     d.fvc = reinterpret_cast<double*>(take(sizeof(double) * bn));
+    d.rec = take(2 * sizeof(double) * bn);
     d.ctl = reinterpret_cast<Ctl*>(take(sizeof(Ctl) * batch));
     d.flag = reinterpret_cast<int*>(take(2 * sizeof(int)));
     d.ticket = reinterpret_cast<unsigned*>(d.flag + 1);
     d.mw = 1.0 / n;
     BCK(cudaMemcpy(m->omega, omega, sizeof(double) * bn, cudaMemcpyHostToDevice));
+    {  // the records' F: RN32(omega), F of a binary32 row (systems.cpp:136-139; the
+       // host cast rounds to nearest); the tensor-core path runs binary32 rows only
+      std::vector<TcRec> r(bn);
+      for (size_t e = 0; e < bn; ++e) r[e] = TcRec{0.f, 0.f, (double)(float)omega[e]};
+      BCK(cudaMemcpy(d.rec, r.data(), sizeof(TcRec) * bn, cudaMemcpyHostToDevice));
+    }
     BCK(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
     BCK(cudaEventCreate(&m->ev0));
     BCK(cudaEventCreate(&m->ev1));

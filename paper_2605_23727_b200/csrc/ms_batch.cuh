@@ -28,6 +28,7 @@ struct BatchDev {
   void* sc;                       // GS-typed s (first B*n) and c (next B*n)
   void* op;                       // GEMM operand [B][4][ld] in K's 16-bit format: s_hi, s_lo, c_hi, c_lo
   double* fvc;                    // F (omega in FS) [B][n]
+  void* rec;                      // tensor-core epilogue records TcRec [B][n]; F written once at creation
   Ctl* ctl;                       // [B]
   int* flag;                      // [1] any trajectory still running (host loop / conditional)
   unsigned* ticket;               // [1] finalize last-block counter (reset by the last block)
@@ -61,7 +62,13 @@ __device__ __forceinline__ double b_fval(const BatchDev& d, int64_t e, int fs32)
 // float2 pairs into the `sc` buffer on that path, and F = RN_FS(omega_bi),
 // which the epilogue reads from omega itself (it never changes).
 #ifndef MS_TC_PACKED
-#define MS_TC_PACKED 1  // 1: prep writes {s, c, F} records (one 16-byte load); 0: (s, c) pairs + omega
+// 2: {s, c, F} records in their own buffer with F = RN32(omega) written once at
+//    creation: the prep stores only the (s, c) half and never reads omega, the
+//    epilogue still takes one 16-byte load. (Splitting the record into (s, c)
+//    pairs + a separate F array instead measured 21 vs 26 us per prep but a
+//    64 vs 41 us contraction.)
+// 1: the prep writes whole {s, c, F} records every stage; 0: (s, c) pairs + omega
+#define MS_TC_PACKED 2
 #endif
 struct __align__(16) TcRec {
   float s, c;
@@ -117,12 +124,14 @@ __device__ __forceinline__ void bprep_elem(const BPrepArgs& p, int b, int i, Ctl
   GS sv, cv;
   dsincos(xg, &sv, &cv);
   if (p.op_ks) {  // tensor-core path: the epilogue's record
-#if MS_TC_PACKED
+#if MS_TC_PACKED == 1
     TcRec r;
     r.s = (float)sv;
     r.c = (float)cv;
     r.f = b_fval(d, e, p.fs32);
     reinterpret_cast<TcRec*>(d.sc)[e] = r;
+#elif MS_TC_PACKED == 2
+    *reinterpret_cast<float2*>(reinterpret_cast<TcRec*>(d.rec) + e) = make_float2((float)sv, (float)cv);
 #else
     reinterpret_cast<float2*>(d.sc)[e] = make_float2((float)sv, (float)cv);
 #endif
@@ -216,11 +225,18 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
   if (skip) return;
   using T = typename K16<OPKS>::T;
   T* op = reinterpret_cast<T*>(d.op) + (int64_t)b * 4 * d.ld;
+#if MS_TC_PACKED == 1
   TcRec* rec = reinterpret_cast<TcRec*>(d.sc) + (int64_t)b * d.n;
   const double* om = d.omega + (int64_t)b * d.n;
+#else
+  TcRec* rec = reinterpret_cast<TcRec*>(d.rec) + (int64_t)b * d.n;
+#endif
   const double h = row.h;
   const int i0 = blockIdx.x * kPrepTcElems * blockDim.x + threadIdx.x;
-  double xv[kPrepTcElems], kv[kPrepTcElems][NT], wv[kPrepTcElems];
+  double xv[kPrepTcElems], kv[kPrepTcElems][NT];
+#if MS_TC_PACKED == 1
+  double wv[kPrepTcElems];
+#endif
 #pragma unroll
   for (int u = 0; u < kPrepTcElems; ++u) {
     const int i = i0 + u * blockDim.x;
@@ -228,7 +244,9 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
       xv[u] = __ldg(row.x + i);
 #pragma unroll
       for (int t = 0; t < NT; ++t) kv[u][t] = __ldg(row.k[t] + i);
+#if MS_TC_PACKED == 1
       wv[u] = __ldg(om + i);
+#endif
     }
   }
 #pragma unroll
@@ -255,11 +273,15 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
     }
     float sv, cv;
     dsincos(__double2float_rn(v), &sv, &cv);
+#if MS_TC_PACKED == 1
     TcRec r;
     r.s = sv;
     r.c = cv;
     r.f = (double)__double2float_rn(wv[u]);  // b_fval, fs32
     rec[i] = r;
+#else
+    *reinterpret_cast<float2*>(rec + i) = make_float2(sv, cv);  // F was written at creation
+#endif
     const T sh = K16<OPKS>::from(sv), ch = K16<OPKS>::from(cv);
     op[i] = sh;
     op[d.ld + i] = K16<OPKS>::from(__fsub_rn(sv, (float)sh));

@@ -133,8 +133,10 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
       const int tq = (c0 >> 2) + q;
       if (row_ok && !skip[tq]) {
         const int64_t e = (int64_t)(tb0 + tq) * d.n + i;
-#if MS_TC_PACKED
+#if MS_TC_PACKED == 1
         v[q] = reinterpret_cast<const TcRec*>(d.sc)[e];
+#elif MS_TC_PACKED == 2
+        v[q] = reinterpret_cast<const TcRec*>(d.rec)[e];
 #else
         const float2 p = sc2[e];
         v[q].s = p.x;

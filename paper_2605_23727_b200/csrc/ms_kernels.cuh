@@ -1235,7 +1235,10 @@ constexpr int kFinThreads = 256;
 // small state vectors: one 1024-thread block does the whole reduction and the
 // controller, without the grid ticket (one dependent round trip fewer)
 constexpr int kFinSmallThreads = 1024;
-constexpr int64_t kFinSmallMax = 2048;  // measured: C1 (2048) -3 %, C3 (8192) +20 % per attempt
+#ifndef MS_FIN_SMALL_MAX
+#define MS_FIN_SMALL_MAX 2048
+#endif
+constexpr int64_t kFinSmallMax = MS_FIN_SMALL_MAX;  // measured: C1 (2048) -3 %, C3 (8192) +20 % per attempt
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000ll); }
 

@@ -94,6 +94,18 @@ VARIANTS = {
                                             "MS_TMA_UNROLL": 2}),
     "k16_c16r2_64k_nofadd2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 16, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 65536,
                                                  "MS_NO_FADD2": 1}),
+    "k16_c8r8_64k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 8, "MS_TMA_RPW_K16": 8}),
+    "k16_c4r8_64k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 4, "MS_TMA_RPW_K16": 8}),
+    "k16_c8r4_48k": ("ms_rhs_fast.cu", {"MS_TMA_KB_K16": 49152}),
+    "k16_c8r4_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_KB_K16": 32768, "MS_TMA_STAGES": 6}),
+    "k16_c8r4_u1": ("ms_rhs_fast.cu", {"MS_TMA_UNROLL": 1}),
+    "k16_c8r4_u2": ("ms_rhs_fast.cu", {"MS_TMA_UNROLL": 2}),
+    "fin_small4k": ("ms_api.cu", {"MS_FIN_SMALL_MAX": 4096}),
+    "tf_sss_c16r1_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 16, "MS_TMA_RPW_SSS": 1, "MS_TMA_KB_F32": 32768,
+                                               "MS_TMA_STAGES": 6}),
+    "tf_sss_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_KB_F32": 32768, "MS_TMA_STAGES": 6}),
+    "tf_sss_16k_s8": ("ms_rhs_fast.cu", {"MS_TMA_KB_F32": 16384, "MS_TMA_STAGES": 8}),
+    "tc_rec1": ("ms_batch.cu", {"MS_TC_PACKED": 1}),
     "fast_fadd2": ("ms_rhs_fast.cu", {"MS_FAST_FADD2": 1}),
     "k16_c12r2_48k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 12, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 49152}),
 }
