@@ -331,7 +331,7 @@ size_t bufs_bytes(const ms_system* s, int64_t log_cap) {
   total += 2 * vec;                                      // xb
   total += (kMaxStages + 1) * vec;                       // kb
   total += 3 * vec;                                      // xn, xt, scratch
-  total += al256(sizeof(double) * 2 * s->ld);            // gin
+  total += 2 * al256(sizeof(double) * 2 * s->ld);        // gin, gin2
   total += al256(sizeof(double) * s->ld);                // rowc
   total += al256(sizeof(double) * s->n);                 // fvc
   total += al256(sizeof(double) * fin_blocks);           // part
@@ -355,6 +355,7 @@ void carve_bufs(const ms_system* s, char* base, int64_t log_cap, Bufs& B) {
   B.xt = reinterpret_cast<double*>(take(sizeof(double) * dn));
   B.scratch = reinterpret_cast<double*>(take(sizeof(double) * dn));
   B.gin = take(sizeof(double) * 2 * s->ld);
+  B.gin2 = take(sizeof(double) * 2 * s->ld);
   B.rowc = take(sizeof(double) * s->ld);
   B.fvc = reinterpret_cast<double*>(take(sizeof(double) * s->n));
   B.part = reinterpret_cast<double*>(take(sizeof(double) * fin_blocks));
@@ -642,6 +643,48 @@ void ensure_dense(ms_system* s, int64_t n) {
 }
 
 // one attempt: [k1 recompute] -> stages -> finalize
+// Stage l of an attempt (BS3/DP5 stage spec e on row sp). prepped: its prep
+// already ran at the end of the previous sweep, into gin_now. With a next
+// stage (en, spn) whose prep can be folded into this sweep (fuse_next_ok),
+// the sweep runs it into the other column buffer; returns whether it did
+// (gin_now then names that buffer). The counters stay those of k_prep + sweep:
+// a folded prep does not count, the sweep of its stage does.
+bool launch_stage(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_stage_prec& sp, bool prepped,
+                  void*& gin_now, const EvalSpec* en, const ms_stage_prec* spn) {
+  Bufs B = s->B;
+  B.gin = gin_now;
+  const bool split = s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST;
+  RhsLaunch L{s->mkind, split, is32(sp.sum_prec), is32(sp.g_prec), s->ks, s->sms, st};
+  const bool whole = s->row0 == 0 && s->row1 == s->n;
+  const bool can = en && whole && !s->fixture && split && fuse_next_ok(L, is32(spn->f_prec), is32(spn->g_prec));
+  if (!prepped && !can) {
+    launch_eval(s, B, st, e, sp);
+    return false;
+  }
+  if (!prepped && !launch_prep(s, B, st, e, sp)) return false;
+  RhsArgs a = rhs_args(s, B, e, sp);
+  if (prepped) {
+    a.count_ctl = B.ctl;
+    a.count = e.count;
+  }
+  PrepArgs pn{};
+  bool fused = false;
+  void* other = gin_now == s->B.gin ? s->B.gin2 : s->B.gin;
+  if (can) {
+    Bufs B2 = s->B;
+    B2.gin = other;
+    pn = prep_args(s, B2, *en, *spn);
+    L.next = &pn;
+    L.next_fs32 = is32(spn->f_prec);
+    L.next_gs32 = is32(spn->g_prec);
+    L.fused = &fused;
+  }
+  launch_rhs_fast(L, a);
+  CK(cudaGetLastError());
+  if (fused) gin_now = other;
+  return fused;
+}
+
 void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_handle,
                     cudaGraphConditionalHandle h) {
   const Tableau& T = *P.T;
@@ -655,7 +698,17 @@ void launch_attempt(ms_system* s, cudaStream_t st, const SolvePlan& P, bool has_
     e.out_slot = SLOT_K1;
     launch_eval(s, st, e, P.k1_row);
   }
-  for (int l = 1; l < T.S; ++l) launch_eval(s, st, stage_spec(T, l), P.rows[l - 1]);
+  void* gin_now = s->B.gin;
+  bool prepped = false;
+  for (int l = 1; l < T.S; ++l) {
+    const EvalSpec e = stage_spec(T, l);
+    if (l + 1 < T.S) {
+      const EvalSpec en = stage_spec(T, l + 1);
+      prepped = launch_stage(s, st, e, P.rows[l - 1], prepped, gin_now, &en, &P.rows[l]);
+    } else {
+      launch_stage(s, st, e, P.rows[l - 1], prepped, gin_now, nullptr, nullptr);
+    }
+  }
   FinArgs f = fin_args(s, s->B, T, FIN_SOLVE, P.k1_elided ? 1 : 0);
   f.has_handle = has_handle ? 1 : 0;
   f.handle = h;

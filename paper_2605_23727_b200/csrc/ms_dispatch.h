@@ -13,7 +13,18 @@ struct RhsLaunch {
   int ks;      // MS_K_*
   int num_sms;
   cudaStream_t stream;
+  // optional: the prep of the attempt's next stage, run at the end of this
+  // sweep when fuse_next_ok() holds (*fused is set when it did)
+  const PrepArgs* next = nullptr;
+  bool next_fs32 = false, next_gs32 = false;
+  bool* fused = nullptr;
 };
+
+// whether launch_rhs_fast folds the next stage's prep (row F/G precisions
+// next_fs32/next_gs32) into this sweep: the split Kuramoto's row-copy TMA sweep
+// of f32 K, next row with F in this row's sum format and the same G format,
+// whole (unsharded) handles; MS_FUSE_NEXT=off disables it
+bool fuse_next_ok(const RhsLaunch& L, bool next_fs32, bool next_gs32);
 
 // rhs_fast over rows [a.row0, a.row1): one persistent CTA per SM
 void launch_rhs_fast(const RhsLaunch& L, const RhsArgs& a);

@@ -988,8 +988,14 @@ __device__ __forceinline__ void tma_col_step(const unsigned char* sk, const GS* 
   }
 }
 
-template <class SS, class GS, int KS>
-__global__ void __launch_bounds__(kTmaThreadsMax, 1) k_rhs_tma(RhsArgs a) {
+// NEXT: the prep of the attempt's next stage (pn) runs at the end of this
+// sweep, for this CTA's own rows: every per-agent input of that prep (x, the
+// k slots including the k_l this CTA just wrote) is row-local, so only the
+// column data needs another buffer (pn.B.gin: the other CTAs still read this
+// stage's). The arithmetic is prep_agent's, so the results are bit-identical to
+// k_prep + sweep; host side: launch_attempt (fuse_next_ok in ms_rhs_fast.cu).
+template <class SS, class GS, int KS, bool NEXT = false>
+__global__ void __launch_bounds__(kTmaThreadsMax, 1) k_rhs_tma(RhsArgs a, PrepArgs pn) {
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   sweep_count(a);
@@ -1130,6 +1136,22 @@ __global__ void __launch_bounds__(kTmaThreadsMax, 1) k_rhs_tma(RhsArgs a) {
     }
   }
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
+  if constexpr (NEXT) {
+    // the k_l rows of this CTA are written by the consumer warps (the producer
+    // warp has returned): a named barrier over the consumers only
+    asm volatile("bar.sync 1, %0;" ::"r"(G::CONS * 32) : "memory");
+    const PrepCtx c = prep_ctx(pn);
+    bool nfp = false;
+    for (int i = rb + (int)threadIdx.x; i < re; i += G::CONS * 32) nfp |= prep_agent<MD_KUR, SS, GS>(pn, c, i);
+    if (__any_sync(0xffffffffu, nfp) && lane == 0) atomicOr(a.nf_mask, 1 << pn.l);
+    if (blockIdx.x == 0) {  // the padding columns of the target buffer (k_prep does the same)
+      GS* g = reinterpret_cast<GS*>(pn.B.gin);
+      for (int j = pn.md.n + (int)threadIdx.x; j < pn.ld; j += G::CONS * 32) {
+        g[j] = GS(0);
+        g[pn.ld + j] = GS(0);
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------

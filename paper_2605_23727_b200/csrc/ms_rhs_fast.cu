@@ -61,9 +61,9 @@ void go_tile(const RhsLaunch& L, const RhsArgs& a) {
   launch_rhs_multi(m, !ss64 ? 1 : 0, ss64 && !gs64 ? 1 : 0, ss64 && gs64 ? 1 : 0, KS, a.K, L.num_sms, L.stream);
 }
 
-template <class SS, class GS, int KS>
-void go_tma(const RhsLaunch& L, const RhsArgs& a) {
-  auto kern = k_rhs_tma<SS, GS, KS>;
+template <class SS, class GS, int KS, bool NEXT = false>
+void go_tma(const RhsLaunch& L, const RhsArgs& a, const PrepArgs& pn = PrepArgs{}) {
+  auto kern = k_rhs_tma<SS, GS, KS, NEXT>;
   using G = TmaGeom<SS, GS, KS>;
   constexpr size_t smem = G::SMEM;
   static bool attr_done = false;
@@ -79,7 +79,7 @@ void go_tma(const RhsLaunch& L, const RhsArgs& a) {
   }();
   const int slots = cap > 0 && cap < L.num_sms ? cap : L.num_sms;
   const int grid = rows < slots ? rows : slots;
-  cudaError_t e = launch_k(kern, grid, G::THREADS, smem, L.stream, a);
+  cudaError_t e = launch_k(kern, grid, G::THREADS, smem, L.stream, a, pn);
   if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tma launch: ") + cudaGetErrorString(e));
 }
 
@@ -96,6 +96,11 @@ void go(const RhsLaunch& L, const RhsArgs& a) {
   }
   if constexpr (MODEL == MD_KUR && SPLIT && KS == MS_K_F32) {
     if (use_tma_sweep_env()) {
+      if (L.next && fuse_next_ok(L, L.next_fs32, L.next_gs32)) {
+        go_tma<SS, GS, KS, true>(L, a, *L.next);
+        if (L.fused) *L.fused = true;
+        return;
+      }
       go_tma<SS, GS, KS>(L, a);
       return;
     }
@@ -230,6 +235,17 @@ bool launch_eval_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, 
     case MD_CC: return fused_by_prec<MD_CC, false>(L, p, a, fs32);
     default: return false;
   }
+}
+
+bool fuse_next_ok(const RhsLaunch& L, bool next_fs32, bool next_gs32) {
+  static const bool on = [] {
+    const char* v = std::getenv("MS_FUSE_NEXT");
+    return !(v && std::strcmp(v, "off") == 0);
+  }();
+  const char* v = std::getenv("MS_SWEEP");
+  const bool tma = !(v && (std::strcmp(v, "ldg") == 0 || std::strcmp(v, "tile") == 0 || std::strcmp(v, "small") == 0));
+  // the kernel runs prep_agent<KUR, FS = SS, GS>: the next row's F must be this row's sum format
+  return on && tma && L.model == MD_KUR && L.split && L.ks == MS_K_F32 && next_fs32 == L.ss32 && next_gs32 == L.gs32;
 }
 
 bool pdl_enabled() {
