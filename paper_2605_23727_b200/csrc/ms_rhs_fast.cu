@@ -238,10 +238,8 @@ bool launch_eval_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, 
 }
 
 bool fuse_next_ok(const RhsLaunch& L, bool next_fs32, bool next_gs32) {
-  static const bool on = [] {
-    const char* v = std::getenv("MS_FUSE_NEXT");
-    return !(v && std::strcmp(v, "off") == 0);
-  }();
+  const char* f = std::getenv("MS_FUSE_NEXT");  // read per launch (graphs capture it once)
+  const bool on = !(f && std::strcmp(f, "off") == 0);
   const char* v = std::getenv("MS_SWEEP");
   const bool tma = !(v && (std::strcmp(v, "ldg") == 0 || std::strcmp(v, "tile") == 0 || std::strcmp(v, "small") == 0));
   // the kernel runs prep_agent<KUR, FS = SS, GS>: the next row's F must be this row's sum format

@@ -277,3 +277,29 @@ def test_config3_cc_reduced(gpu):
     w = config3_cc(n=128)
     w.tf = 24.0
     _parity(w, 1e-5)
+
+
+@pytest.mark.parametrize("variant", [None, PolicyVariant.Single, PolicyVariant.Mixed1, PolicyVariant.Mixed2,
+                                     PolicyVariant.Double])
+@pytest.mark.parametrize("n", [1000, 4096])
+def test_folded_next_prep_is_bitwise_the_separate_prep(gpu, variant, n, monkeypatch):
+    """The f32 TMA sweep can run the next stage's prep for its own rows
+    (MS_FUSE_NEXT, launch_stage in ms_api.cu): the whole solve — final state,
+    counts, evaluation tallies and every step record — must equal the solve
+    with k_prep launched for every stage, for every named policy (Mixed1 also
+    switches rows between stages, where the fold does not apply)."""
+    w = config2_kuramoto(n=n, rtol=1e-6, k_storage="f32")
+    w.tf = 5.0
+    pol = w.policy if variant is None else policy_for(variant)  # None: C2's own {SSS x3, storage D}
+    res = []
+    for f in ("on", "off"):
+        monkeypatch.setenv("MS_FUSE_NEXT", f)
+        dev = DeviceSystem(w.spec)  # its own graph cache: the env is read while capturing
+        res.append(S.solve(dev, w.x0, w.t0, w.tf, pol, w.cfg))
+        dev.close()
+    a, b = res
+    assert a.status == b.status == SolveStatus.Completed
+    assert (a.n_accepted, a.n_failed) == (b.n_accepted, b.n_failed)
+    assert a.flops.rhs_evals == b.flops.rhs_evals
+    assert np.array_equal(a.final_state, b.final_state)
+    assert [(r.t, r.h, r.err, r.accepted) for r in a.step_log] == [(r.t, r.h, r.err, r.accepted) for r in b.step_log]
