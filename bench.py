@@ -289,7 +289,12 @@ def run_ours(args):
                "l2_over_sqrtN": float(np.linalg.norm(r0_.final_state - rd.final_state) / np.sqrt(n)),
                "double_steps": [rd.n_accepted, rd.n_failed]}
 
-    per_attempt = 11 if shard else 7  # (prep + sweep [+ scan]) x 3 + finalize [+ fsal copy]
+    # launches per attempt: (prep + sweep [+ scan]) x 3 + finalize [+ fsal copy]; the f32
+    # TMA sweep of stages 1 and 2 also runs the next stage's prep (MS_FUSE_NEXT), 5 then
+    sweep_env = os.environ.get("MS_SWEEP", "tma")
+    folded = (not shard and args.kdtype == "f32" and os.environ.get("MS_FUSE_NEXT", "on") != "off"
+              and sweep_env not in ("ldg", "tile", "small"))
+    per_attempt = 11 if shard else (5 if folded else 7)
     gpu_launches = sum(10 + per_attempt * (r.n_accepted + r.n_failed) for r in results)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
