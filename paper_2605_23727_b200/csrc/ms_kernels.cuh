@@ -939,6 +939,9 @@ constexpr int kTmaStages = MS_TMA_STAGES;
 #ifndef MS_TMA_UNROLL
 #define MS_TMA_UNROLL 4    // column steps unrolled in the full-tile consumer loop
 #endif
+#ifndef MS_TMA_MINB
+#define MS_TMA_MINB 1      // resident CTAs per SM (grid = SMs x MINB; the ring must fit MINB times)
+#endif
 constexpr int kTmaUnroll = MS_TMA_UNROLL;
 
 template <class SS, class GS, int KS>
@@ -954,7 +957,7 @@ struct TmaGeom {
   static constexpr int TC = KBYTES / (RG * (int)sizeof(KT));   // columns per tile
   static constexpr int SC_BYTES = 2 * TC * (int)sizeof(GS);
   static constexpr int STAGE_BYTES = KBYTES + SC_BYTES;
-  static constexpr int NS = (232448 - 512) / STAGE_BYTES < kTmaStages ? (232448 - 512) / STAGE_BYTES : kTmaStages;
+  static constexpr int NS = (232448 / MS_TMA_MINB - 1536) / STAGE_BYTES < kTmaStages ? (232448 / MS_TMA_MINB - 1536) / STAGE_BYTES : kTmaStages;
   static constexpr size_t SMEM = (size_t)NS * STAGE_BYTES + 2 * kTmaStages * sizeof(uint64_t) + 128;
   static_assert(TC % (32 * KVec<KS>::N) == 0, "tile width must be a whole number of warp steps");
 };
@@ -995,7 +998,7 @@ __device__ __forceinline__ void tma_col_step(const unsigned char* sk, const GS* 
 // stage's). The arithmetic is prep_agent's, so the results are bit-identical to
 // k_prep + sweep; host side: launch_attempt (fuse_next_ok in ms_rhs_fast.cu).
 template <class SS, class GS, int KS, bool NEXT = false>
-__global__ void __launch_bounds__(kTmaThreadsMax, 1) k_rhs_tma(RhsArgs a, PrepArgs pn) {
+__global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs a, PrepArgs pn) {
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   sweep_count(a);

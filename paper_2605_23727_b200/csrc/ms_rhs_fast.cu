@@ -77,7 +77,7 @@ void go_tma(const RhsLaunch& L, const RhsArgs& a, const PrepArgs& pn = PrepArgs{
     const char* v = std::getenv("MS_TMA_GRID");
     return v ? std::atoi(v) : 0;
   }();
-  const int slots = cap > 0 && cap < L.num_sms ? cap : L.num_sms;
+  const int slots = cap > 0 && cap < L.num_sms * MS_TMA_MINB ? cap : L.num_sms * MS_TMA_MINB;
   const int grid = rows < slots ? rows : slots;
   cudaError_t e = launch_k(kern, grid, G::THREADS, smem, L.stream, a, pn);
   if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tma launch: ") + cudaGetErrorString(e));

@@ -105,6 +105,9 @@ VARIANTS = {
                                                "MS_TMA_STAGES": 6}),
     "tf_sss_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_KB_F32": 32768, "MS_TMA_STAGES": 6}),
     "tf_sss_16k_s8": ("ms_rhs_fast.cu", {"MS_TMA_KB_F32": 16384, "MS_TMA_STAGES": 8}),
+    "tma_m2_32k_s3": ("ms_rhs_fast.cu", {"MS_TMA_MINB": 2, "MS_TMA_KB_F32": 32768, "MS_TMA_STAGES": 3}),
+    "tma_m2_48k_s2": ("ms_rhs_fast.cu", {"MS_TMA_MINB": 2, "MS_TMA_KB_F32": 49152, "MS_TMA_STAGES": 2}),
+    "tma_m2_24k_s4": ("ms_rhs_fast.cu", {"MS_TMA_MINB": 2, "MS_TMA_KB_F32": 24576, "MS_TMA_STAGES": 4}),
     "tc_rec1": ("ms_batch.cu", {"MS_TC_PACKED": 1}),
     "fast_fadd2": ("ms_rhs_fast.cu", {"MS_FAST_FADD2": 1}),
     "k16_c12r2_48k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 12, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 49152}),
