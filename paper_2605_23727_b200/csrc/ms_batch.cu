@@ -63,6 +63,7 @@ struct BFinArgs {
   int S, nbt, k1_elided;
   double bt[kMaxStages];
   int bslot_[kMaxStages];
+  int use_p;  // the last prep wrote P = b~1 k1 + b~2 k2 + b~3 k3 into scr1
 };
 
 // x_tilde, weighted max-norm and the controller of one trajectory per CTA;
@@ -98,10 +99,16 @@ __global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinAr
     const double h = c->h_att;
     const double floor_w = __ddiv_rn(c->abs_tol, c->rel_tol);
 #pragma unroll 4
+    const double* __restrict__ pp = d.scr1 + o;
     for (int i = threadIdx.x; i < d.n; i += kBFinThreads) {
-      double comb = __dmul_rn(b0, k0[i]);
-      comb = __dadd_rn(comb, __dmul_rn(b1, k1[i]));
-      comb = __dadd_rn(comb, __dmul_rn(b2, k2[i]));
+      double comb;
+      if (f.use_p) {
+        comb = pp[i];
+      } else {
+        comb = __dmul_rn(b0, k0[i]);
+        comb = __dadd_rn(comb, __dmul_rn(b1, k1[i]));
+        comb = __dadd_rn(comb, __dmul_rn(b2, k2[i]));
+      }
       comb = __dadd_rn(comb, __dmul_rn(b3, k3[i]));
       const double xi = x[i];
       const double xt = __dadd_rn(xi, __dmul_rn(h, comb));
@@ -305,6 +312,12 @@ struct BEval {
   int is_last = 0, round_x = 0;
 };
 
+// MS_BFIN_P=off: the finalize combines k1..k4 itself (read per launch; graphs capture it once)
+bool bfin_p_enabled() {
+  const char* v = std::getenv("MS_BFIN_P");
+  return !(v && std::strcmp(v, "off") == 0);
+}
+
 template <class FS>
 void launch_bprep(ms_batch* m, cudaStream_t st, const BPrepArgs& p, bool gs32) {
   dim3 grid((m->d.n + 255) / 256, m->B);
@@ -370,6 +383,13 @@ void beval(ms_batch* m, cudaStream_t st, const BEval& e, const ms_stage_prec& sp
   p.ws32 = fs32 && ss32;
   p.fs32 = fs32;
   p.op_ks = use_tc ? m->op_ks : 0;
+  // the BS3 last stage combines k1, k2, k3 (slots K1, 1, 2), the first three terms
+  // of the finalize's x_tilde sum in its order
+  if (e.kind == PREP_STAGE && e.is_last && e.nterms == 3 && e.slot[0] == SLOT_K1 && e.slot[1] == 1 &&
+      e.slot[2] == 2 && bfin_p_enabled()) {
+    p.write_p = 1;
+    for (int t = 0; t < 3; ++t) p.pb[t] = kBT.bt[t];
+  }
   if (!(use_tc && launch_bprep_tc(m, st, p))) {
     if (fs32) launch_bprep<float>(m, st, p, gs32);
     else launch_bprep<double>(m, st, p, gs32);
@@ -454,6 +474,7 @@ void battempt(ms_batch* m, cudaStream_t st, const BPlan& P, bool has_handle, cud
     ++f.nbt;
   }
   if (f.nbt != 4) throw InvalidArg("batch: finalize expects the four BS3(2) error weights");
+  f.use_p = bfin_p_enabled() ? 1 : 0;
   BCK(launch_k(kb_finalize, m->B, kBFinThreads, 0, st, f, has_handle ? 1 : 0, h));
 }
 

@@ -82,6 +82,11 @@ struct BPrepArgs {
   int slot[kMaxStages];
   int is_last, round_x, ws32, fs32;
   int op_ks;  // 0: no GEMM operand; MS_K_F16 / MS_K_BF16: write the rounded operand
+  // last stage: also write P = b~1 k1 + b~2 k2 + b~3 k3 (the first three terms of
+  // x_tilde's combination, in its order) into scr1, so the finalize reads P and
+  // k4 instead of k1..k4 (bit-identical: the same operations in the same order)
+  int write_p;
+  double pb[3];
 };
 
 // stage combination + F + sin/cos (+ rounded GEMM operand) of element i of
@@ -118,6 +123,11 @@ __device__ __forceinline__ void bprep_elem(const BPrepArgs& p, int b, int i, Ctl
         v = (double)acc;
       }
       d.xb[ix ^ 1][e] = v;
+      if (p.write_p) {
+        double pp = __dmul_rn(p.pb[0], bslot(d, p.S, p.slot[0], c)[e]);
+        pp = __dadd_rn(pp, __dmul_rn(p.pb[1], bslot(d, p.S, p.slot[1], c)[e]));
+        d.scr1[e] = __dadd_rn(pp, __dmul_rn(p.pb[2], bslot(d, p.S, p.slot[2], c)[e]));
+      }
     }
   }
   const GS xg = cvt<GS>(v);
@@ -201,6 +211,7 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
     const double* k[NT];
     double* xst;
     double* xn;
+    double* pp;
     double h;
     int store32;
   };
@@ -217,6 +228,7 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
       for (int t = 0; t < NT; ++t) row.k[t] = bslot(d, p.S, p.slot[t], c) + o;
       row.xst = d.xb[ix ^ 1] + o;
       row.xn = d.xn + o;
+      row.pp = d.scr1 + o;
       row.h = c->h_att;
       row.store32 = c->store32;
     }
@@ -270,6 +282,11 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
         v = (double)acc;
       }
       row.xst[i] = v;
+      if (NT == 3 && p.write_p) {
+        double pp = __dmul_rn(p.pb[0], kv[u][0]);
+        pp = __dadd_rn(pp, __dmul_rn(p.pb[1], kv[u][1]));
+        row.pp[i] = __dadd_rn(pp, __dmul_rn(p.pb[2], kv[u][2]));
+      }
     }
     float sv, cv;
     dsincos(__double2float_rn(v), &sv, &cv);

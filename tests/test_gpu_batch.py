@@ -163,3 +163,29 @@ def test_batch_tc_specialised_prep_is_bitwise(gpu, monkeypatch, ks, pol):
     assert np.array_equal(a.rhs_evals, b.rhs_evals)
     assert np.array_equal(a.final_state, b.final_state)
     assert np.array_equal(a.t_reached, b.t_reached)
+
+
+@pytest.mark.parametrize("tc", [True, False])
+@pytest.mark.parametrize("pol", ["SSS_D", "Single", "Mixed2"])
+def test_batch_finalize_partial_sum_is_bitwise(gpu, monkeypatch, tc, pol):
+    """The last stage prep hands the finalize P = b~1 k1 + b~2 k2 + b~3 k3 (the
+    first three terms of x_tilde's sum, same order): ensembles with and without
+    it (MS_BFIN_P=off) must agree bit for bit, on the tensor-core and the
+    CUDA-core paths."""
+    from paper_2605_23727_b200.configs import SSS_D
+    from paper_2605_23727_b200.precision import PolicyVariant, policy_for
+    from paper_2605_23727_b200.solver import SolverConfig
+    B, n = 40, 256
+    spec, omega, x0 = _ensemble(B, n, "bf16", seed=12)
+    policy = SSS_D if pol == "SSS_D" else policy_for(getattr(PolicyVariant, pol))
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    dev = DeviceSystem(spec)
+    runs = []
+    for mode in ("on", "off"):
+        monkeypatch.setenv("MS_BFIN_P", mode)
+        runs.append(DeviceBatch(dev, omega, tensor_cores=tc).solve(x0, 0.0, 3.0, policy, cfg))
+    a, b = runs
+    assert list(a.status) == list(b.status)
+    assert np.array_equal(a.n_accepted, b.n_accepted) and np.array_equal(a.n_failed, b.n_failed)
+    assert np.array_equal(a.final_state, b.final_state)
+    assert np.array_equal(a.t_reached, b.t_reached)
