@@ -281,7 +281,7 @@ def test_config3_cc_reduced(gpu):
 
 @pytest.mark.parametrize("variant", [None, PolicyVariant.Single, PolicyVariant.Mixed1, PolicyVariant.Mixed2,
                                      PolicyVariant.Double])
-@pytest.mark.parametrize("n", [1000, 4096])
+@pytest.mark.parametrize("n", [1003, 4096])
 def test_folded_next_prep_is_bitwise_the_separate_prep(gpu, variant, n, monkeypatch):
     """The f32 TMA sweep can run the next stage's prep for its own rows
     (MS_FUSE_NEXT, launch_stage in ms_api.cu): the whole solve — final state,
@@ -303,3 +303,23 @@ def test_folded_next_prep_is_bitwise_the_separate_prep(gpu, variant, n, monkeypa
     assert a.flops.rhs_evals == b.flops.rhs_evals
     assert np.array_equal(a.final_state, b.final_state)
     assert [(r.t, r.h, r.err, r.accepted) for r in a.step_log] == [(r.t, r.h, r.err, r.accepted) for r in b.step_log]
+
+
+def test_folded_next_prep_dp54_is_bitwise(gpu, monkeypatch):
+    """DP5(4) (seven stages, five folded preps per attempt, all-binary64 rows on
+    f32 K): the device reference run with and without the fold, bit for bit, and
+    against the oracle's DP5(4) run."""
+    w = config2_kuramoto(n=1003, rtol=1e-6, k_storage="f32")
+    res = []
+    for f in ("on", "off"):
+        monkeypatch.setenv("MS_FUSE_NEXT", f)
+        dev = DeviceSystem(w.spec)
+        res.append(S.dp54_reference(dev, w.x0, 0.0, 1.0))
+        dev.close()
+    a, b = res
+    assert a.status == b.status == SolveStatus.Completed
+    assert (a.n_accepted, a.n_failed) == (b.n_accepted, b.n_failed)
+    assert np.array_equal(a.final_state, b.final_state)
+    O.set_threads(8)
+    q = O.dp54_reference(O.OracleSystem(w.spec), w.x0, 0.0, 1.0)
+    _same_run(a, q, 1e-9, exact_counts=False)
