@@ -574,6 +574,13 @@ EvalSpec stage_spec(const Tableau& T, int l) {
   return e;
 }
 
+}  // namespace
+// MS_CTL_SMEM=off: the controller works on Ctl in global memory (read per launch)
+bool msb::ctl_smem_enabled() {
+  const char* v = std::getenv("MS_CTL_SMEM");
+  return !(v && std::strcmp(v, "off") == 0);
+}
+namespace {
 FinArgs fin_args(ms_system* s, const Bufs& B, const Tableau& T, int mode, int k1_elided) {
   FinArgs f{};
   f.B = B;
@@ -588,6 +595,7 @@ FinArgs fin_args(ms_system* s, const Bufs& B, const Tableau& T, int mode, int k1
   f.mode = mode;
   f.k1_elided = k1_elided;
   f.write_xt = mode == FIN_STEP ? 1 : 0;
+  f.ctl_smem = ctl_smem_enabled() ? 1 : 0;
   return f;
 }
 

@@ -64,6 +64,7 @@ struct BFinArgs {
   double bt[kMaxStages];
   int bslot_[kMaxStages];
   int use_p;  // the last prep wrote P = b~1 k1 + b~2 k2 + b~3 k3 into scr1
+  int ctl_smem;  // controller on a shared-memory copy of Ctl[b] (MS_CTL_SMEM)
 };
 
 // x_tilde, weighted max-norm and the controller of one trajectory per CTA;
@@ -79,7 +80,15 @@ __global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinAr
   pdl_enter();
   const int b = blockIdx.x;
   const BatchDev& d = f.d;
-  Ctl* c = d.ctl + b;
+  Ctl* cg = d.ctl + b;
+  // the trajectory's control block: a shared-memory copy (one round trip in,
+  // one out) unless MS_CTL_SMEM=off; no other block touches Ctl[b] here
+  __shared__ __align__(16) Ctl cs;
+  if (f.ctl_smem) {
+    ctl_copy(&cs, cg);
+    __syncthreads();
+  }
+  Ctl* c = f.ctl_smem ? &cs : cg;
   const bool dead = c->done != 0;
   const bool stage_nf = c->nf_mask != 0;
   double m = 0.0;
@@ -136,9 +145,14 @@ __global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinAr
       anynf |= rnf[w];
     }
     attempt_controller(c, f.S, FIN_SOLVE, f.k1_elided, 0, dead, stage_nf, anynf != 0, e, nullptr);
-    __threadfence();
-    last = atomicAdd(d.ticket, 1u) == gridDim.x - 1;
   }
+  if (f.ctl_smem) {
+    __syncthreads();
+    ctl_copy(cg, &cs);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(d.ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   // loop condition: does any trajectory still run?
@@ -475,6 +489,7 @@ void battempt(ms_batch* m, cudaStream_t st, const BPlan& P, bool has_handle, cud
   }
   if (f.nbt != 4) throw InvalidArg("batch: finalize expects the four BS3(2) error weights");
   f.use_p = bfin_p_enabled() ? 1 : 0;
+  f.ctl_smem = ctl_smem_enabled() ? 1 : 0;
   BCK(launch_k(kb_finalize, m->B, kBFinThreads, 0, st, f, has_handle ? 1 : 0, h));
 }
 

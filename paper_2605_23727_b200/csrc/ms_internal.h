@@ -17,4 +17,6 @@ struct SysView {
 SysView sys_view(ms_system_t s);
 // the thread-local message behind ms_last_error()
 void set_last_error(const char* msg);
+// MS_CTL_SMEM: controllers run on a shared-memory copy of Ctl (default on)
+bool ctl_smem_enabled();
 }  // namespace msb

@@ -1253,8 +1253,19 @@ struct FinArgs {
   int write_xt;
   int has_handle;
   int fixed_k1;  // host-driven sharded loop: k1 stays in slot 0 (k_fsal_copy), no ping-pong
+  int ctl_smem;  // run the controller on a shared-memory copy of Ctl (MS_CTL_SMEM, default on)
   cudaGraphConditionalHandle handle;
 };
+
+// The controller's ~40 dependent field reads and writes of the control block
+// are global round trips when it runs on Ctl in place; on a shared-memory copy
+// (copied in and out by the whole block: one round trip each) they are not.
+static_assert(sizeof(Ctl) % 8 == 0, "Ctl is copied as 64-bit words");
+constexpr int kCtlWords = (int)(sizeof(Ctl) / 8);
+__device__ __forceinline__ void ctl_copy(void* dst, const void* src) {
+  for (int w = threadIdx.x; w < kCtlWords; w += blockDim.x)
+    static_cast<uint64_t*>(dst)[w] = static_cast<const uint64_t*>(src)[w];
+}
 
 constexpr int kFinThreads = 256;
 // small state vectors: one 1024-thread block does the whole reduction and the
@@ -1393,13 +1404,14 @@ __global__ void __launch_bounds__(kFinSmallThreads) k_finalize(FinArgs f) {
   if ((threadIdx.x & 31) == 0) { red[warp] = m; red_nf[warp] = nf; }
   __syncthreads();
   double e = 0.0;
-  bool any_nf;
+  bool any_nf = false;  // e and any_nf: thread 0 of the controlling block
   if (gridDim.x == 1) {
-    if (threadIdx.x != 0) return;
-    int bnf = 0;
-    for (int w = 0; w < nwarps; ++w) { e = fmax(e, red[w]); bnf |= red_nf[w]; }
-    any_nf = bnf != 0;
-    if (dead || stage_nf || any_nf) e = 0.0;
+    if (threadIdx.x == 0) {
+      int bnf = 0;
+      for (int w = 0; w < nwarps; ++w) { e = fmax(e, red[w]); bnf |= red_nf[w]; }
+      any_nf = bnf != 0;
+      if (dead || stage_nf || any_nf) e = 0.0;
+    }
   } else {
     __shared__ bool is_last;
     if (threadIdx.x == 0) {
@@ -1413,16 +1425,34 @@ __global__ void __launch_bounds__(kFinSmallThreads) k_finalize(FinArgs f) {
       is_last = (t == gridDim.x - 1);
     }
     __syncthreads();
-    if (!is_last || threadIdx.x != 0) return;
-    __threadfence();
-    c->ticket = 0;
-    any_nf = atomicAdd(&c->any_nonfinite, 0) != 0;
-    c->any_nonfinite = 0;
-    if (!(dead || stage_nf || any_nf))
-      for (int b = 0; b < (int)gridDim.x; ++b) e = fmax(e, f.B.part[b]);
+    if (!is_last) return;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      c->ticket = 0;
+      any_nf = atomicAdd(&c->any_nonfinite, 0) != 0;
+      c->any_nonfinite = 0;
+      if (!(dead || stage_nf || any_nf))
+        for (int b = 0; b < (int)gridDim.x; ++b) e = fmax(e, f.B.part[b]);
+    }
   }
-  const bool more = attempt_controller(c, f.S, f.mode, f.k1_elided, f.fixed_k1, dead, stage_nf, any_nf, e, f.B.log);
-  if (f.has_handle && f.mode == FIN_SOLVE) cudaGraphSetConditional(f.handle, more ? 1 : 0);
+  if (!f.ctl_smem) {
+    if (threadIdx.x != 0) return;
+    const bool more = attempt_controller(c, f.S, f.mode, f.k1_elided, f.fixed_k1, dead, stage_nf, any_nf, e, f.B.log);
+    if (f.has_handle && f.mode == FIN_SOLVE) cudaGraphSetConditional(f.handle, more ? 1 : 0);
+    return;
+  }
+  // no other block touches Ctl from here on; thread 0's resets above are
+  // visible to the block after the barrier
+  __shared__ __align__(16) Ctl cs;
+  __syncthreads();
+  ctl_copy(&cs, c);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const bool more = attempt_controller(&cs, f.S, f.mode, f.k1_elided, f.fixed_k1, dead, stage_nf, any_nf, e, f.B.log);
+    if (f.has_handle && f.mode == FIN_SOLVE) cudaGraphSetConditional(f.handle, more ? 1 : 0);
+  }
+  __syncthreads();
+  ctl_copy(c, &cs);
 }
 
 // StepSnapshot capture (solver.cpp:324-327): after an accepted attempt copy the
