@@ -70,7 +70,14 @@ struct BFinArgs {
 // x_tilde, weighted max-norm and the controller of one trajectory per CTA;
 // the last CTA to finish (ticket) also evaluates the loop condition, so an
 // attempt ends without a separate condition kernel
-constexpr int kBFinThreads = 256;
+#ifndef MS_BFIN_THREADS
+#define MS_BFIN_THREADS 256
+#endif
+constexpr int kBFinThreads = MS_BFIN_THREADS;
+#ifndef MS_BFIN_UNROLL
+#define MS_BFIN_UNROLL 0  // element-loop unroll (0: the compiler's choice)
+#endif
+constexpr int kBFinUnroll = MS_BFIN_UNROLL;
 // resident blocks per SM: 8 caps registers at 32 so all B = 1024 trajectory
 // blocks run in one wave (61 registers gave 4 blocks per SM, 1.7 waves)
 #ifndef MS_BFIN_MINB
@@ -107,8 +114,10 @@ __global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinAr
     const double b0 = f.bt[0], b1 = f.bt[1], b2 = f.bt[2], b3 = f.bt[3];
     const double h = c->h_att;
     const double floor_w = __ddiv_rn(c->abs_tol, c->rel_tol);
-#pragma unroll 4
     const double* __restrict__ pp = d.scr1 + o;
+#if MS_BFIN_UNROLL > 0
+#pragma unroll kBFinUnroll
+#endif
     for (int i = threadIdx.x; i < d.n; i += kBFinThreads) {
       double comb;
       if (f.use_p) {

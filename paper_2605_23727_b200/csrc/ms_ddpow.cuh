@@ -116,7 +116,14 @@ MS_HD inline bool pow_root(double x, double y, double* out) {
   for (int k = 2; k <= 8; ++k)
     if (y == msb_div(1.0, (double)k)) q = k;
   if (q == 0 || !(x > 1e-290 && x < 1e290)) return false;
-  const double r0 = pow(x, y);
+  // the libm start only has to be good to a few ulp: the Newton step squares
+  // its error; the root functions are far shorter chains than pow
+#ifndef MS_POW_ROOT_START
+#define MS_POW_ROOT_START 1  // 0: start from libm pow (A/B: tools/build_variants.py pow_libm_*)
+#endif
+  const double r0 = !MS_POW_ROOT_START ? pow(x, y)
+                    : q == 2 ? std::sqrt(x)
+                    : (q == 3 ? std::cbrt(x) : (q == 4 ? std::sqrt(std::sqrt(x)) : pow(x, y)));
   if (!(r0 > 0.0) || !isfinite(r0)) return false;
   dd p{r0, 0.0};
   for (int i = 1; i < q; ++i) p = dd_mul_d(p, r0);  // r0^q

@@ -110,6 +110,12 @@ VARIANTS = {
     "tma_m2_24k_s4": ("ms_rhs_fast.cu", {"MS_TMA_MINB": 2, "MS_TMA_KB_F32": 24576, "MS_TMA_STAGES": 4}),
     "tc_rec1": ("ms_batch.cu", {"MS_TC_PACKED": 1}),
     "fast_fadd2": ("ms_rhs_fast.cu", {"MS_FAST_FADD2": 1}),
+    "fin_t128_u4": ("ms_batch.cu", {"MS_BFIN_THREADS": 128, "MS_BFIN_UNROLL": 4}),
+    "fin_t128_u8": ("ms_batch.cu", {"MS_BFIN_THREADS": 128, "MS_BFIN_UNROLL": 8}),
+    "fin_t128": ("ms_batch.cu", {"MS_BFIN_THREADS": 128}),
+    "fin_t256_u4": ("ms_batch.cu", {"MS_BFIN_UNROLL": 4}),
+    "pow_libm_api": ("ms_api.cu", {"MS_POW_ROOT_START": 0}),
+    "pow_libm_batch": ("ms_batch.cu", {"MS_POW_ROOT_START": 0}),
     "k16_c12r2_48k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 12, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 49152}),
 }
 
