@@ -71,15 +71,18 @@ struct BFinArgs {
 // the last CTA to finish (ticket) also evaluates the loop condition, so an
 // attempt ends without a separate condition kernel
 #ifndef MS_BFIN_THREADS
-#define MS_BFIN_THREADS 256
+#define MS_BFIN_THREADS 128  // 8 x 128 threads per SM: 64 registers, unrolled loads, one wave
 #endif
 constexpr int kBFinThreads = MS_BFIN_THREADS;
 #ifndef MS_BFIN_UNROLL
-#define MS_BFIN_UNROLL 0  // element-loop unroll (0: the compiler's choice)
+#define MS_BFIN_UNROLL 8  // element-loop unroll (0: the compiler's choice)
 #endif
 constexpr int kBFinUnroll = MS_BFIN_UNROLL;
-// resident blocks per SM: 8 caps registers at 32 so all B = 1024 trajectory
-// blocks run in one wave (61 registers gave 4 blocks per SM, 1.7 waves)
+// resident blocks per SM: 8 so all B = 1024 trajectory blocks run in one wave
+// (61 registers x 256 threads gave 4 blocks per SM, 1.7 waves); 128-thread
+// blocks leave 64 registers for an unrolled element loop, where 256 x 32
+// registers spilled and kept one element's loads in flight per thread
+// (292.0 -> 287.0 ms per C5 solve, tools/gpu_bfin2.sh)
 #ifndef MS_BFIN_MINB
 #define MS_BFIN_MINB 8
 #endif
