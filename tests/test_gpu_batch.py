@@ -189,3 +189,26 @@ def test_batch_finalize_partial_sum_is_bitwise(gpu, monkeypatch, tc, pol):
     assert np.array_equal(a.n_accepted, b.n_accepted) and np.array_equal(a.n_failed, b.n_failed)
     assert np.array_equal(a.final_state, b.final_state)
     assert np.array_equal(a.t_reached, b.t_reached)
+
+
+@pytest.mark.parametrize("tc", [True, False])
+def test_batch_controller_on_shared_copy_is_bitwise(gpu, monkeypatch, tc):
+    """kb_finalize runs each trajectory's controller on a shared-memory copy of
+    Ctl[b] (MS_CTL_SMEM): ensembles with the controller in place must agree
+    bit for bit (statuses, counts, final states, t_reached)."""
+    from paper_2605_23727_b200.configs import SSS_D
+    from paper_2605_23727_b200.solver import SolverConfig
+    B, n = 37, 256
+    spec, omega, x0 = _ensemble(B, n, "bf16", seed=13)
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    dev = DeviceSystem(spec)
+    runs = []
+    for mode in ("on", "off"):
+        monkeypatch.setenv("MS_CTL_SMEM", mode)
+        runs.append(DeviceBatch(dev, omega, tensor_cores=tc).solve(x0, 0.0, 3.0, SSS_D, cfg))
+    a, b = runs
+    assert list(a.status) == list(b.status)
+    assert np.array_equal(a.n_accepted, b.n_accepted) and np.array_equal(a.n_failed, b.n_failed)
+    assert np.array_equal(a.rhs_evals, b.rhs_evals)
+    assert np.array_equal(a.final_state, b.final_state)
+    assert np.array_equal(a.t_reached, b.t_reached)

@@ -323,3 +323,54 @@ def test_folded_next_prep_dp54_is_bitwise(gpu, monkeypatch):
     O.set_threads(8)
     q = O.dp54_reference(O.OracleSystem(w.spec), w.x0, 0.0, 1.0)
     _same_run(a, q, 1e-9, exact_counts=False)
+
+
+@pytest.mark.parametrize("which", ["c1_small_block", "c2_grid_ticket", "c3_cc", "single_policy"])
+def test_controller_on_shared_copy_is_bitwise(gpu, which, monkeypatch):
+    """The finalize's controller runs on a shared-memory copy of the control
+    block (MS_CTL_SMEM, k_finalize in ms_kernels.cuh): whole solves — final
+    state, counts, tallies and every step record — must equal the solve with
+    the controller on Ctl in global memory, for the one-block finalize (dn <=
+    2048), the multi-block ticket finalize, and binary32 storage."""
+    if which == "c1_small_block":
+        w = config1_lco(n=1000)
+        w.tf = 2.0
+        pol = w.policy
+    elif which == "c3_cc":
+        w = config3_cc(n=512)
+        w.tf = 5.0
+        pol = w.policy
+    else:
+        w = config2_kuramoto(n=3000, rtol=1e-6, k_storage="f32")
+        w.tf = 4.0
+        pol = w.policy if which == "c2_grid_ticket" else policy_for(PolicyVariant.Single)
+    res = []
+    for f in ("on", "off"):
+        monkeypatch.setenv("MS_CTL_SMEM", f)
+        dev = DeviceSystem(w.spec)  # its own graph cache: the env is read while capturing
+        res.append(S.solve(dev, w.x0, w.t0, w.tf, pol, w.cfg))
+        dev.close()
+    a, b = res
+    assert a.status == b.status == SolveStatus.Completed
+    assert (a.n_accepted, a.n_failed) == (b.n_accepted, b.n_failed)
+    assert a.flops.rhs_evals == b.flops.rhs_evals
+    assert np.array_equal(a.final_state, b.final_state)
+    assert [(r.t, r.h, r.err, r.accepted) for r in a.step_log] == [(r.t, r.h, r.err, r.accepted) for r in b.step_log]
+
+
+def test_controller_on_shared_copy_limits_are_bitwise(gpu, monkeypatch):
+    """Failure statuses set by the controller's loop_check on the shared copy:
+    max_iterations and max_failed stop at the same attempt as in place."""
+    w = config2_kuramoto(n=700, rtol=1e-6, k_storage="f32")
+    for kw in ({"max_iterations": 37}, {"max_failed_steps": 3}):
+        cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False, **kw)
+        res = []
+        for f in ("on", "off"):
+            monkeypatch.setenv("MS_CTL_SMEM", f)
+            dev = DeviceSystem(w.spec)
+            res.append(S.solve(dev, w.x0, w.t0, w.tf, w.policy, cfg))
+            dev.close()
+        a, b = res
+        assert a.status == b.status != SolveStatus.Completed, kw
+        assert (a.n_accepted, a.n_failed, a.t_reached) == (b.n_accepted, b.n_failed, b.t_reached)
+        assert np.array_equal(a.final_state, b.final_state)
