@@ -101,6 +101,7 @@ VARIANTS = {
     "k16_c8r4_u1": ("ms_rhs_fast.cu", {"MS_TMA_UNROLL": 1}),
     "k16_c8r4_u2": ("ms_rhs_fast.cu", {"MS_TMA_UNROLL": 2}),
     "fin_small4k": ("ms_api.cu", {"MS_FIN_SMALL_MAX": 4096}),
+    "fin_small8k": ("ms_api.cu", {"MS_FIN_SMALL_MAX": 8192}),
     "tf_sss_c16r1_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 16, "MS_TMA_RPW_SSS": 1, "MS_TMA_KB_F32": 32768,
                                                "MS_TMA_STAGES": 6}),
     "tf_sss_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_KB_F32": 32768, "MS_TMA_STAGES": 6}),
