@@ -34,6 +34,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "Kuramoto N=32768 BS3(2) accepted steps/s"
 UNIT = "accepted_steps/s"
+DATA = "synthetic (seeded SplitMix64: omega~N(0,1), K~U(0,2), theta0~U(0,2pi))"
 
 
 def peaks():
@@ -105,17 +106,21 @@ def bytes_per_eval(n, rows, ks_bytes):
     return rows * n * ks_bytes + n * 2 * 4 + 2 * n * 8 + n * 8
 
 
-def ncu_traffic(kernel_prefix):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    kernel from the committed `ncu --set full` capture (profiles/), or None."""
+TRAFFIC_CSV = "profiles/r2_c4_sweeps_raw.csv"  # ncu --set full of one host-loop C4 attempt (tools/gpu_ncu_c4.sh)
+
+
+def ncu_traffic(kernel_prefix, path=TRAFFIC_CSV):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the first
+    launch whose name starts with `kernel_prefix` in the committed
+    `ncu --set full` capture, or None."""
     import csv
-    p = ROOT / "profiles" / "r1_k_rhs_tma_f32_raw.csv"
+    p = ROOT / path
     if not p.exists():
         return None
     rows = list(csv.reader(p.open()))
     hdr, units = rows[0], rows[1]
     for r in rows[2:]:
-        if kernel_prefix in r[hdr.index("Kernel Name")]:
+        if r[hdr.index("Kernel Name")].startswith(kernel_prefix):
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             tot = 0.0
             for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
@@ -125,28 +130,136 @@ def ncu_traffic(kernel_prefix):
     return None
 
 
-def cpu_sample(n, seed, threads, attempts=2, ks="f32"):
-    """The oracle on a bounded sample of C4: `attempts` BS3(2) attempts from
-    theta0 at the initial step (3 RHS evaluations each), OpenMP over rows."""
+def sweep_kernel(kdtype, whole):
+    """The dominant kernel of the benchmark solve (the K sweep that runs 2 of
+    the 3 stage evaluations of an attempt) and its ncu DRAM traffic."""
+    if kdtype == "f32" and os.environ.get("MS_SWEEP", "tma") == "tma":
+        nxt = 1 if whole and os.environ.get("MS_FUSE_NEXT", "on") != "off" else 0
+        name = f"void k_rhs_tma<float, float, 1, {nxt}>"
+        label = f"k_rhs_tma<f32 sum, f32 G, K f32, NEXT={nxt}> (cp.async.bulk-fed K sweep" + \
+                (", folds the next stage's prep)" if nxt else ")")
+    else:
+        ks = {"f32": 1, "f16": 2, "bf16": 3}[kdtype]
+        name = f"void k_rhs_fast<1, 1, float, float, {ks}>"
+        label = f"k_rhs_fast<Kuramoto split, f32 sum, f32 G, K {kdtype}> (register-fed K sweep)"
+    tr = ncu_traffic(name) if whole else None
+    return label, tr, (f"{TRAFFIC_CSV} ({name}, ncu --set full, one launch)" if tr else None)
+
+
+def mapped_repo_libs():
+    """Shared objects under this repo mapped into the process (evidence that
+    the reference arm runs only oracle/ code)."""
+    try:
+        maps = Path("/proc/self/maps").read_text().splitlines()
+    except OSError:
+        return None
+    return sorted({ln.split()[-1].replace(str(ROOT) + "/", "") for ln in maps
+                   if ln.endswith(".so") and str(ROOT) in ln})
+
+
+def workload_config(n, kdtype, ws):
+    """The `config` dict of BOTH arms (identical, so the driver can pair them)."""
+    return {"workload": f"C4 Kuramoto N={n} K {kdtype} (BASELINE configs[3])", "n_agents": n, "t_final": 20.0,
+            "rtol": 1e-6, "atol": 1e-9, "policy": "SSS x3 rows, binary64 storage", "k_storage": kdtype,
+            "l2": "K (4 GiB f32 / 2 GiB f16) > L2 (126 MB): no flush needed",
+            "parallelism": f"row-shard x{ws} (NCCL all-gather per stage)" if ws > 1 else "single GPU"}
+
+
+def dtype_label(kdtype):
+    return f"{kdtype} (K storage), f32 (RHS rows) / f64 (stages, error control)"
+
+
+def oracle_c4_inputs(n, seed, kdtype, rhs_mode):
+    """C4's seeded inputs drawn with the ORACLE's SplitMix64 (rng.hpp:13-52) so
+    the reference arm never maps this repo's library: omega ~ N(0,1) (stream 0),
+    theta0 ~ U(0, 2 pi) (stream 1), K ~ U(0,2) (stream 2, filled by the oracle)."""
     sys.path.insert(0, str(ROOT / "tests"))
     import _oracle as O
-    from paper_2605_23727_b200.configs import config4_kuramoto
-    w = config4_kuramoto(n=n, seed=seed, k_storage=ks)
+    from paper_2605_23727_b200.configs import SSS_D, TWO_PI
+    from paper_2605_23727_b200.solver import SolverConfig
+    from paper_2605_23727_b200.systems import SystemSpec
+    omega = O.rng_normal(seed, 0, n)
+    theta0 = O.rng_uniform(seed, 1, n, 0.0, TWO_PI)
+    spec = SystemSpec("kuramoto", n, k_storage=kdtype, rhs_mode=rhs_mode, omega=omega, k_uniform=(seed, 2, 0.0, 2.0))
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    return O, spec, theta0, cfg, SSS_D
+
+
+def cpu_prefix(n, seed, kdtype, threads, warm, timed, rhs_mode="faithful"):
+    """The reference algorithm on the host cores over a bounded PREFIX of the
+    real C4 solve: initial_step + cold k1 (untimed setup), then `warm` untimed
+    and `timed` timed attempts of solve_core's loop (solver.cpp:255-347: the
+    attempt is bs32_step = rk_step, solver.cpp:110-215; an accepted attempt
+    moves t/x/k1 (FSAL), a rejected one recomputes k1 at the next attempt,
+    :298-306), so rejections are timed where the solve takes them.
+    rhs_mode "faithful" = the reference's eval_core order, one sinf per pair
+    (systems.cpp:30-64, 141-143); "fast" = the oracle's split GEMV-2 form.
+    OpenMP over rows keeps every row's j-sum sequential (bitwise the
+    single-thread reference)."""
+    O, spec, x0, cfg, policy = oracle_c4_inputs(n, seed, kdtype, rhs_mode)
     O.set_threads(threads)
     t0 = time.perf_counter()
-    orc = O.OracleSystem(w.spec)
+    orc = O.OracleSystem(spec)
     t_gen = time.perf_counter() - t0
-    h0 = O.initial_step(orc, w.t0, w.tf, w.x0, w.cfg)
-    k1 = orc.eval_rhs(0.0, w.x0, w.policy.first_step_k1)
-    times = []
-    acc = 0
-    for _ in range(attempts):
-        t0 = time.perf_counter()
-        o = O.bs32_step(orc, 0.0, w.x0, h0, k1, w.policy, w.cfg)
-        times.append(time.perf_counter() - t0)
-        acc += int(o.accepted)
-    return {"per_attempt_s": float(np.mean(times)), "attempts": attempts, "accepted": acc,
-            "k_gen_s": t_gen, "h0": h0}
+    t0 = time.perf_counter()
+    h = O.initial_step(orc, 0.0, 20.0, x0, cfg)
+    k1 = orc.eval_rhs(0.0, x0, policy.first_step_k1)
+    t_setup = time.perf_counter() - t0
+    t, x, need_k1, tf = 0.0, x0, False, 20.0
+    rec = []
+    for a in range(warm + timed):
+        s0 = time.perf_counter()
+        ev = 3
+        if need_k1:
+            k1 = orc.eval_rhs(t, x, policy.first_step_k1)
+            need_k1, ev = False, 4
+        h_att = tf - t if t + 1.01 * h >= tf else h
+        o = O.bs32_step(orc, t, x, h_att, k1, policy, cfg)
+        dt = time.perf_counter() - s0
+        if o.accepted:
+            x, t, k1 = o.x_store, t + h_att, o.k4
+        else:
+            need_k1 = True
+        h = o.h_next
+        rec.append((dt, bool(o.accepted), ev))
+    tim = rec[warm:]
+    secs = sum(r[0] for r in tim)
+    acc = sum(r[1] for r in tim)
+    evals = sum(r[2] for r in tim)
+    return {"seconds": secs, "accepted": acc, "attempts": len(tim), "rejected": len(tim) - acc, "evals": evals,
+            "per_attempt_s": [r[0] for r in tim], "k_gen_s": t_gen, "setup_s": t_setup, "t_reached": t,
+            "threads": threads, "value": acc / secs if secs > 0 else 0.0,
+            "per_eval_s": secs / max(evals, 1)}
+
+
+def cpu_single_eval(n, seed, kdtype, threads, rhs_mode):
+    """Seconds of ONE SSS-row RHS evaluation of C4 on `threads` host threads."""
+    O, spec, x0, cfg, policy = oracle_c4_inputs(n, seed, kdtype, rhs_mode)
+    O.set_threads(threads)
+    orc = O.OracleSystem(spec)
+    from paper_2605_23727_b200.precision import SSS
+    t0 = time.perf_counter()
+    orc.eval_rhs(0.0, x0, SSS)
+    return time.perf_counter() - t0
+
+
+def oracle_counts(kdtype):
+    """The oracle's own whole-solve counts for C4 (tests/golden/solves, made by
+    tools/make_golden_solves.py; the tests check them against live runs)."""
+    p = ROOT / "tests" / "golden" / "solves" / f"c4_{kdtype}.npz"
+    if not p.exists():
+        return None
+    d = np.load(p)
+    return {"n_accepted": int(d["n_accepted"]), "n_failed": int(d["n_failed"]), "rhs_evals": int(d["rhs_evals"]),
+            "final_state": d["final_state"]}
+
+
+def project(per_eval_s, counts):
+    """Accepted steps/s of the whole solve at a measured per-evaluation time,
+    with the oracle's own evaluation count (3 + 3 accepted + 4 rejected)."""
+    if not counts:
+        return None
+    return counts["n_accepted"] / (per_eval_s * counts["rhs_evals"])
 
 
 def run_reference(args):
@@ -155,21 +268,42 @@ def run_reference(args):
         return 0
     threads = os.cpu_count() or 1
     n = args.n
-    res = []
-    sample = cpu_sample(n, args.seed, threads, attempts=args.warmup + args.steps, ks=args.kdtype)
-    per = sample["per_attempt_s"]
-    value = 1.0 / per  # every sampled attempt is accepted at h0 (checked below)
+    pre = cpu_prefix(n, args.seed, args.kdtype, threads, args.warmup, args.steps)
+    value = pre["value"]
+    counts = oracle_counts(args.kdtype) if n == 32768 else None
+    extras = {}
+    if not args.no_cpu_extras:
+        t1 = cpu_single_eval(n, args.seed, args.kdtype, 1, "faithful")
+        ts = cpu_single_eval(n, args.seed, args.kdtype, threads, "fast")
+        extras = {
+            "single_thread_faithful": {"eval_s": t1, "projected_value": project(t1, counts),
+                                       "what": "one SSS eval_core evaluation (per-pair sinf) on 1 thread; value "
+                                               "projected with the oracle's whole-solve evaluation count"},
+            "all_cores_faithful_projected": project(pre["per_eval_s"], counts),
+            "split_form_all_cores": {"eval_s": ts, "projected_value": project(ts, counts),
+                                     "what": "the oracle's split GEMV-2 form (not the reference's order), "
+                                             f"{threads} threads, one evaluation"},
+        }
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (RHS) / f64 (stages)", "data": "synthetic (seeded SplitMix64)",
-        "config": {"workload": f"C4 Kuramoto N={n} K {args.kdtype}", "n_agents": n, "t_final": 20.0,
-                   "rtol": 1e-6, "atol": 1e-9, "policy": "SSS x3, binary64 storage"},
+        "warmup": args.warmup, "ms_per_step": pre["seconds"] / max(pre["attempts"], 1) * 1e3,
+        "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None,
+        "dtype": dtype_label(args.kdtype), "data": DATA,
+        "config": workload_config(n, args.kdtype, ws),
+        "step_def": "one BS3(2) attempt of the real C4 solve prefix (after W untimed attempts)",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample['attempts']} BS3(2) attempts (3 RHS evals each) of C4 from theta0 at h0; "
-                                   f"oracle restatement, OpenMP rows over {threads} threads"},
+                         "sample": f"attempts {args.warmup + 1}..{args.warmup + args.steps} of the C4 solve "
+                                   f"({pre['accepted']} accepted, {pre['rejected']} rejected, {pre['evals']} RHS "
+                                   f"evals, t reached {pre['t_reached']:.4g}); reference eval_core order "
+                                   f"(per-pair sinf, systems.cpp:30-64) restated in oracle/, OpenMP rows over "
+                                   f"{threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "accepted_in_sample": sample["accepted"],
+        "prefix": {k: pre[k] for k in ("seconds", "accepted", "rejected", "evals", "per_eval_s", "k_gen_s",
+                                       "setup_s")},
+        "oracle_whole_solve_counts": ({k: counts[k] for k in ("n_accepted", "n_failed", "rhs_evals")}
+                                      if counts else None),
+        **extras,
+        "native_libs": mapped_repo_libs(),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -224,11 +358,14 @@ def run_ours(args):
         if ws > 1:
             torch.distributed.barrier()
         results = []
+        from paper_2605_23727_b200 import _abi as _A
+        launches0 = _A.lib().ms_launch_count()
         with ClockSampler(local) as clk:
             torch.cuda.synchronize()
             for _ in range(args.steps):
                 results.append(one())
             torch.cuda.synchronize()
+        gpu_launches = _A.lib().ms_launch_count() - launches0
     # device time of each solve: CUDA events recorded by the library on its stream
     # around the whole adaptive loop (initial step included)
     ms = float(sum(r.device_ms for r in results))
@@ -278,49 +415,62 @@ def run_ours(args):
     peak, peak_kind = peaks()
     achieved = bpe / (rhs_ms.value * 1e-3) / 1e9
     solve_gbs = launched_evals / args.steps * bpe / (ms_per_step * 1e-3) / 1e9
+    kname, traffic, traffic_src = sweep_kernel(args.kdtype, rows == n)
 
-    # accuracy: device SSS solve vs the same-tolerance all-binary64 device solve
+    # accuracy, outside the timed region: the benchmark solve
+    # vs (1) the same-tolerance all-binary64 device BS3(2) run, (2) the tight
+    # binary64 DP5(4) run at rel = abs = 1e-9 (dp54_reference, solver.cpp:472-483)
+    # on the device, and (3) the oracle's own whole solve (counts and final
+    # state from tests/golden/solves; its global error vs the same DP5(4) run)
     err = {}
     if not args.no_accuracy:
+        r0_ = e2e_res[0]
+        floor = w.cfg.abs_tol / w.cfg.rel_tol
+
+        def dev_err(ref, x=None):
+            x = r0_.final_state if x is None else x
+            d = np.abs(x - ref)
+            return {"max_abs": float(d.max()),
+                    "max_rel_weighted": float(np.max(d / np.maximum(np.abs(ref), floor))),
+                    "l2_over_sqrtN": float(np.linalg.norm(x - ref) / np.sqrt(n))}
+
         D = custom_policy((DDD, DDD, DDD), DDD, B64)
         rd = solver.solve(w.x0, w.t0, w.tf, D, w.cfg) if shard else S.solve(dev, w.x0, w.t0, w.tf, D, w.cfg)
-        r0_ = e2e_res[0]
-        diff = np.abs(r0_.final_state - rd.final_state)
-        err = {"vs": "device all-binary64 BS3(2), same rtol/atol",
-               "max_abs": float(diff.max()),
-               "max_rel_weighted": float(np.max(diff / np.maximum(np.abs(rd.final_state), w.cfg.abs_tol / w.cfg.rel_tol))),
-               "l2_over_sqrtN": float(np.linalg.norm(r0_.final_state - rd.final_state) / np.sqrt(n)),
-               "double_steps": [rd.n_accepted, rd.n_failed]}
+        err["vs_binary64_bs32_same_tol"] = {**dev_err(rd.final_state), "steps": [rd.n_accepted, rd.n_failed]}
+        if rows == n:
+            t_dp = time.perf_counter()
+            rdp = S.dp54_reference(dev, w.x0, w.t0, w.tf, S.SolverConfig(time_limits_enabled=False), log_capacity=1)
+            err["vs_dp54_1e-9"] = {**dev_err(rdp.final_state), "status": int(rdp.status),
+                                   "steps": [rdp.n_accepted, rdp.n_failed],
+                                   "wall_s": round(time.perf_counter() - t_dp, 2),
+                                   "what": "global error vs the tight binary64 DP5(4) device run (rel=abs=1e-9)"}
+            oc = oracle_counts(args.kdtype) if n == 32768 else None
+            if oc:
+                of = oc["final_state"]
+                err["oracle_vs_dp54_1e-9"] = dev_err(rdp.final_state, of)
+                err["vs_oracle"] = {
+                    "oracle_counts": [oc["n_accepted"], oc["n_failed"]],
+                    "device_counts": [r0_.n_accepted, r0_.n_failed],
+                    "accepted_within_1pct": bool(abs(r0_.n_accepted - oc["n_accepted"])
+                                                 <= max(1, 0.01 * oc["n_accepted"])),
+                    "rejected_within_1pct_of_attempts": bool(abs(r0_.n_failed - oc["n_failed"])
+                                                             <= max(1, 0.01 * (oc["n_accepted"] + oc["n_failed"]))),
+                    "final_state": dev_err(of),
+                    "source": f"tests/golden/solves/c4_{args.kdtype}.npz (the oracle's whole solve)"}
 
-    # launches per attempt: (prep + sweep [+ scan]) x 3 + finalize [+ fsal copy]; the f32
-    # TMA sweep of stages 1 and 2 also runs the next stage's prep (MS_FUSE_NEXT), 5 then
-    sweep_env = os.environ.get("MS_SWEEP", "tma")
-    folded = (not shard and args.kdtype == "f32" and os.environ.get("MS_FUSE_NEXT", "on") != "off"
-              and sweep_env not in ("ldg", "tile", "small"))
-    per_attempt = 11 if shard else (5 if folded else 7)
-    gpu_launches = sum(10 + per_attempt * (r.n_accepted + r.n_failed) for r in results)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
-        "vs_baseline": None, "dtype": "f32 (RHS, K) / f64 (stages, error control)",
-        "data": "synthetic (seeded SplitMix64: omega~N(0,1), K~U(0,2), theta0~U(0,2pi))",
-        "config": {"workload": f"C4 Kuramoto N={n} K {args.kdtype} (BASELINE configs[3])", "n_agents": n,
-                   "t_final": 20.0, "rtol": 1e-6, "atol": 1e-9, "policy": "SSS x3 rows, binary64 storage",
-                   "step": "one full adaptive solve", "l2": "K (4 GiB) > L2: no flush needed",
-                   "parallelism": f"row-shard x{ws} (NCCL all-gather per stage)" if shard else "single GPU"},
+        "vs_baseline": None, "dtype": dtype_label(args.kdtype), "data": DATA,
+        "config": workload_config(n, args.kdtype, ws),
+        "step_def": "one full adaptive solve (t in [0,20], initial_step included)",
         "accepted_steps_per_solve": results[0].n_accepted, "rejected_per_solve": results[0].n_failed,
         "rhs_evals_per_solve": results[0].flops.rhs_evals,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
                      "frac_nominal_8TBps": achieved / 8000.0,  # both denominators
-                     "traffic": (ncu_traffic("k_rhs_tma<float, float, 1>")
-                                 if args.kdtype == "f32" and rows == n and os.environ.get("MS_SWEEP", "tma") != "ldg"
-                                 else None),
-                     "traffic_source": "profiles/r1_k_rhs_tma_f32_raw.csv (ncu --set full, one launch)",
-                     "peak_kind": peak_kind,
-                     "kernel": ("k_rhs_tma<f32, f32, K f32> (cp.async.bulk-fed K sweep)" if args.kdtype == "f32"
-                                and os.environ.get("MS_SWEEP", "tma") != "ldg"
-                                else f"k_rhs_fast<Kuramoto split, f32, f32, K {args.kdtype}>"),
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind, "kernel": kname,
                      "bytes_per_launch": bpe, "launch_ms": rhs_ms.value, "prep_ms": prep_ms.value,
                      "solve_effective_GBps": solve_gbs},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,
@@ -329,11 +479,13 @@ def run_ours(args):
         "accuracy": err,
     }
     if rank == 0 and not args.no_cpu_baseline and ws == 1:
-        cs = cpu_sample(args.cpu_n or n, args.seed, os.cpu_count() or 1, attempts=1, ks=args.kdtype)
-        line["cpu_baseline"] = {"value": 1.0 / cs["per_attempt_s"], "unit": UNIT, "cores": os.cpu_count() or 1,
-                                "kind": "port",
-                                "sample": f"1 BS3(2) attempt (3 RHS evals) of C4 N={args.cpu_n or n} from theta0 at h0, "
-                                          "oracle restatement, OpenMP rows"}
+        thr = os.cpu_count() or 1
+        cs = cpu_prefix(args.cpu_n or n, args.seed, args.kdtype, thr, 0, args.cpu_attempts)
+        line["cpu_baseline"] = {"value": cs["value"], "unit": UNIT, "cores": thr, "kind": "port",
+                                "sample": f"the first {cs['attempts']} attempts of the C4 solve (N={args.cpu_n or n}: "
+                                          f"{cs['accepted']} accepted, {cs['evals']} RHS evals, {cs['seconds']:.1f} s) "
+                                          "in the reference eval_core order (per-pair sinf, systems.cpp:30-64) "
+                                          f"restated in oracle/, OpenMP rows over {thr} threads"}
     line["clocks"] = clk.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -354,6 +506,8 @@ def main():
     ap.add_argument("--kdtype", default="f32", choices=["f32", "f16", "bf16"])
     ap.add_argument("--cpu-n", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-attempts", type=int, default=3, help="attempts timed by the GPU arm's cpu_baseline leg")
+    ap.add_argument("--no-cpu-extras", action="store_true", help="reference arm: skip the 1-thread/split extras")
     ap.add_argument("--no-accuracy", action="store_true")
     ap.add_argument("--shard", action="store_true", help="use the row-sharded loop even on 1 GPU")
     ap.add_argument("--check-every", type=int, default=8)

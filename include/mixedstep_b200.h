@@ -229,6 +229,11 @@ const char* ms_last_error(void);
 int ms_abi_sizes(int64_t out[8]);
 /* device count visible to the library (0 without a GPU; never an error) */
 int ms_device_count(void);
+/* number of this library's kernels that have run on the current device since
+ * the library was loaded (every kernel counts itself once, CUDA-graph replays
+ * included); synchronizes the device; -1 on a CUDA error or without a GPU.
+ * Bench/driver evidence, no reference counterpart. */
+int64_t ms_launch_count(void);
 void ms_default_config(ms_solver_config* cfg);
 /* policy_for, precision.cpp:22-42 */
 int ms_policy_for(int variant, ms_policy* out);

@@ -106,6 +106,7 @@ SIGNATURES = [
     ("ms_last_error", C.c_char_p, []),
     ("ms_abi_sizes", C.c_int, [C.POINTER(C.c_int64)]),
     ("ms_device_count", C.c_int, []),
+    ("ms_launch_count", C.c_int64, []),
     ("ms_default_config", None, [C.POINTER(SolverConfigC)]),
     ("ms_policy_for", C.c_int, [C.c_int, C.POINTER(Policy)]),
     ("ms_policy_lowest_format", C.c_int, [C.POINTER(Policy)]),

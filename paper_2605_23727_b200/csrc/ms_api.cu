@@ -194,6 +194,7 @@ template <> __device__ __forceinline__ __nv_bfloat16 to_k<MS_K_BF16>(double v) {
 template <int KS>
 __global__ void k_fill_uniform(typename KElem<KS>::T* K, int n, int row0, int rows, int64_t ld, uint64_t state0,
                                double lo, double hi) {
+  msb::count_launch();
   const int64_t total = (int64_t)rows * n;
   const double span = __dsub_rn(hi, lo);
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
@@ -206,6 +207,7 @@ __global__ void k_fill_uniform(typename KElem<KS>::T* K, int n, int row0, int ro
 
 template <int KS, class SRC>
 __global__ void k_convert_rows(typename KElem<KS>::T* K, const SRC* src, int n, int rows, int64_t ld) {
+  msb::count_launch();
   const int64_t total = (int64_t)rows * n;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = q / n, j = q % n;
@@ -215,6 +217,7 @@ __global__ void k_convert_rows(typename KElem<KS>::T* K, const SRC* src, int n, 
 
 template <int KS>
 __global__ void k_get_rows(const typename KElem<KS>::T* K, double* dst, int n, int rows, int64_t ld) {
+  msb::count_launch();
   const int64_t total = (int64_t)rows * n;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = q / n, j = q % n;
@@ -224,6 +227,7 @@ __global__ void k_get_rows(const typename KElem<KS>::T* K, double* dst, int n, i
 
 __global__ void k_estimate_error(int64_t n, const double* a, const double* b, const double* c, double ab, double rel,
                                  double* out) {
+  msb::count_launch();
   // estimate_error, solver.cpp:399-411 (max is order-independent)
   __shared__ double red[32];
   const double floor_w = __ddiv_rn(ab, rel);
@@ -244,6 +248,7 @@ __global__ void k_estimate_error(int64_t n, const double* a, const double* b, co
 
 __global__ void k_adjust_step(double h, double err, double rel, double safety, double fmin, double fmax_,
                               double ex, double* out) {
+  msb::count_launch();
   *out = d_adjust_step(h, err, rel, safety, fmin, fmax_, ex);
 }
 
@@ -1187,6 +1192,7 @@ struct LaneCtls {
 
 // loop condition over the lanes (the WHILE node of the variants graph)
 __global__ void k_lanes_cond(LaneCtls L, int nl, int* flag, int has_handle, cudaGraphConditionalHandle h) {
+  msb::count_launch();
   int any = 0;
   for (int v = 0; v < nl; ++v) any |= L.c[v]->done == 0;
   *flag = any;
@@ -1526,6 +1532,20 @@ int ms_abi_sizes(int64_t out[8]) {
   out[6] = sizeof(ms_step_outcome);
   out[7] = sizeof(ms_exchange);
   return MS_OK;
+}
+
+int64_t ms_launch_count(void) {
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, msb::g_ms_launches, sizeof(v)) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  v += launches_tu_fast() + launches_tu_faithful() + launches_tu_multi() + launches_tu_batch();
+  return static_cast<int64_t>(v);
 }
 
 int ms_device_count(void) {

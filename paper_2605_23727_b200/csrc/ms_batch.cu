@@ -19,6 +19,10 @@
 
 using namespace msb;
 
+namespace msb {
+MS_DEFINE_LAUNCH_READER(launches_tu_batch)
+}  // namespace msb
+
 namespace {
 
 struct CudaError : std::runtime_error {
@@ -87,6 +91,7 @@ constexpr int kBFinUnroll = MS_BFIN_UNROLL;
 #define MS_BFIN_MINB 8
 #endif
 __global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinArgs f, int has_handle, cudaGraphConditionalHandle h) {
+  msb::count_launch();
   pdl_enter();
   const int b = blockIdx.x;
   const BatchDev& d = f.d;
@@ -180,11 +185,13 @@ __global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinAr
 }
 
 __global__ void kb_stamp(Ctl* ctl, int B) {
+  msb::count_launch();
   const uint64_t t = globaltimer_ns();
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) ctl[b].t_start_ns = t;
 }
 
 __global__ void kb_loop_head(Ctl* ctl, int B) {
+  msb::count_launch();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   Ctl* c = ctl + b;
@@ -202,6 +209,7 @@ __global__ void kb_loop_head(Ctl* ctl, int B) {
 // initial_step (solver.cpp:420-451) per trajectory: terms in parallel, the
 // sums by one thread in ascending order (the oracle's order)
 __global__ void __launch_bounds__(256) kb_init_a(BatchDev d) {
+  msb::count_launch();
   const int b = blockIdx.x;
   Ctl* c = d.ctl + b;
   if (c->done) return;
@@ -246,6 +254,7 @@ __global__ void __launch_bounds__(256) kb_init_a(BatchDev d) {
 }
 
 __global__ void __launch_bounds__(256) kb_init_b(BatchDev d, double exponent) {
+  msb::count_launch();
   const int b = blockIdx.x;
   Ctl* c = d.ctl + b;
   if (c->done) return;

@@ -174,6 +174,7 @@ __device__ __forceinline__ void bprep_elem(const BPrepArgs& p, int b, int i, Ctl
 // every trajectory: grid (ceil(n/256), B)
 template <class FS, class GS>
 __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
+  msb::count_launch();
   pdl_enter();
   const int b = blockIdx.y;
   const BatchDev& d = p.d;
@@ -202,6 +203,7 @@ __global__ void __launch_bounds__(256) kb_prep(BPrepArgs p) {
 constexpr int kPrepTcElems = MS_PREP_TC_ELEMS;
 template <int OPKS, int NT, bool LAST>
 __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
+  msb::count_launch();
   pdl_enter();
   const int b = blockIdx.y;
   const BatchDev& d = p.d;
@@ -335,6 +337,7 @@ __device__ __forceinline__ void b_epilogue(const BRhsArgs& a, int i, int b, SS A
 constexpr int kBT_I = 64, kBT_B = 32, kBT_J = 32;
 template <class SS, class GS, int KS>
 __global__ void __launch_bounds__(256) kb_rhs_cc(BRhsArgs a) {
+  msb::count_launch();
   pdl_enter();
   const BatchDev& d = a.d;
   __shared__ GS Ks[kBT_I][kBT_J + 1];

@@ -104,6 +104,25 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// ---- launch accounting ---------------------------------------------------------
+// Every kernel of the library starts with count_launch(): the first thread of
+// block (0,0,0) adds one to a per-translation-unit device counter, so
+// ms_launch_count() reports how many of this library's kernels actually ran
+// (CUDA-graph replays and early-exiting kernels included) — a count, not a
+// formula. One counter per TU (no relocatable device code); each .cu defines a
+// host reader with MS_DEFINE_LAUNCH_READER.
+static __device__ unsigned long long g_ms_launches;
+__device__ __forceinline__ void count_launch() {
+  if ((blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x | threadIdx.y | threadIdx.z) == 0)
+    atomicAdd(&g_ms_launches, 1ull);
+}
+#define MS_DEFINE_LAUNCH_READER(fn)                                                        \
+  unsigned long long fn() {                                                                \
+    unsigned long long v = 0;                                                              \
+    if (cudaMemcpyFromSymbol(&v, msb::g_ms_launches, sizeof(v)) != cudaSuccess) return 0;  \
+    return v;                                                                              \
+  }
+
 // ---- coupling storage --------------------------------------------------------
 struct KScalar {};  // no matrix: G uses RN_S(coupling_k)
 template <int KS> struct KElem;

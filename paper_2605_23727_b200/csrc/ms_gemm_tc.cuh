@@ -175,6 +175,7 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
 
 __global__ void __launch_bounds__(kTcThreads, MS_TC_MINB)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs t) {
+  msb::count_launch();
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   // 1024-byte alignment for SWIZZLE_128B tiles
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -348,6 +349,7 @@ __device__ __forceinline__ void tma2_load(uint32_t dst, const CUtensorMap* tm, u
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MINB)
     k_tc_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs t) {
+  msb::count_launch();
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));

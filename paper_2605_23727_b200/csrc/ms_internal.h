@@ -19,4 +19,9 @@ SysView sys_view(ms_system_t s);
 void set_last_error(const char* msg);
 // MS_CTL_SMEM: controllers run on a shared-memory copy of Ctl (default on)
 bool ctl_smem_enabled();
+// per-translation-unit kernel launch counters (ms_common.cuh count_launch)
+unsigned long long launches_tu_fast();
+unsigned long long launches_tu_faithful();
+unsigned long long launches_tu_multi();
+unsigned long long launches_tu_batch();
 }  // namespace msb

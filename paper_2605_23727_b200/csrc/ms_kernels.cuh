@@ -292,6 +292,7 @@ __device__ __forceinline__ bool prep_agent(const PrepArgs& p, const PrepCtx& c, 
 
 template <int MODEL, class FS, class GS>
 __global__ void __launch_bounds__(256) k_prep(PrepArgs p) {
+  msb::count_launch();
   pdl_enter();
   Ctl* ctl = p.B.ctl;
   if (stage_skip(ctl, p.l, p.gate)) return;
@@ -529,6 +530,7 @@ __device__ __forceinline__ void sweep_step(const uint4 (&kv)[R], int nr, const G
 // (not on the row partition), so sharded runs are bitwise identical.
 template <int MODEL, bool SPLIT, class SS, class GS, int KS>
 __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsArgs a) {
+  msb::count_launch();
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   sweep_count(a);
@@ -741,6 +743,7 @@ constexpr size_t kFusedMaxSmem = 96 * 1024;
 // unrolled loop.
 template <int MODEL, bool SPLIT, class FS, class SS, class GS, int KS, bool PREPPED = false>
 __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(PrepArgs p, RhsArgs a) {
+  msb::count_launch();
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -999,6 +1002,7 @@ __device__ __forceinline__ void tma_col_step(const unsigned char* sk, const GS* 
 // k_prep + sweep; host side: launch_attempt (fuse_next_ok in ms_rhs_fast.cu).
 template <class SS, class GS, int KS, bool NEXT = false>
 __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs a, PrepArgs pn) {
+  msb::count_launch();
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   sweep_count(a);
@@ -1162,6 +1166,7 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
 // j including j = i, acc = acc + mw * (SS)G_ij, G in GS with RN_GS(K_ij).
 template <int MODEL, class SS, class GS, int KS>
 __global__ void __launch_bounds__(128) k_rhs_faithful(RhsArgs a) {
+  msb::count_launch();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   sweep_count(a);
   const int r = a.row0 + blockIdx.x * blockDim.x + threadIdx.x;
@@ -1366,6 +1371,7 @@ __device__ inline double seq_sum(const double* v, int64_t n) {
 
 #ifdef MS_DEFINE_STEP_KERNELS
 __global__ void __launch_bounds__(kFinSmallThreads) k_finalize(FinArgs f) {
+  msb::count_launch();
   pdl_enter();
   Ctl* c = f.B.ctl;
   const bool dead = c->done != 0;
@@ -1460,6 +1466,7 @@ __global__ void __launch_bounds__(kFinSmallThreads) k_finalize(FinArgs f) {
 // state, written once after initialisation with row0 = 1).
 __global__ void __launch_bounds__(256) k_snapshot(Bufs B, double* snap, double* snap_h, int64_t cap, int64_t dn,
                                                   int row0) {
+  msb::count_launch();
   pdl_enter();
   const Ctl* c = B.ctl;
   if (!row0 && !c->snap_pending) return;
@@ -1495,6 +1502,7 @@ __device__ __forceinline__ double hermite(double th, double h, double xn, double
 }
 
 __global__ void __launch_bounds__(256) k_dense(Bufs B, int S, double* y, int64_t dn, int row0, int64_t row0_count) {
+  msb::count_launch();
   pdl_enter();
   const Ctl* c = B.ctl;
   int64_t lo, hi;
@@ -1525,6 +1533,7 @@ __global__ void __launch_bounds__(256) k_dense(Bufs B, int S, double* y, int64_t
 // parallel; each of the three sums is then added by one thread in ascending
 // order (the oracle's fixed order).
 __global__ void __launch_bounds__(1024) k_init_a(InitArgs a) {
+  msb::count_launch();
   pdl_enter();
   Ctl* c = a.B.ctl;
   if (c->done) return;
@@ -1570,6 +1579,7 @@ __global__ void __launch_bounds__(1024) k_init_a(InitArgs a) {
 }
 
 __global__ void __launch_bounds__(1024) k_init_b(InitArgs a) {
+  msb::count_launch();
   pdl_enter();
   Ctl* c = a.B.ctl;
   if (c->done) return;
@@ -1621,6 +1631,7 @@ __global__ void __launch_bounds__(1024) k_init_b(InitArgs a) {
 
 // after the cold k1 (solver.cpp:263-269) and before the first attempt
 __global__ void k_loop_head(Ctl* c) {
+  msb::count_launch();
   pdl_enter();
   if (c->done) return;
   if (c->nf_mask & 1) {
@@ -1634,12 +1645,14 @@ __global__ void k_loop_head(Ctl* c) {
 }
 
 __global__ void k_stamp_start(Ctl* c) {
+  msb::count_launch();
   pdl_enter();
   c->t_start_ns = globaltimer_ns();
 }
 
 // sharded loop: finiteness of a gathered stage vector, identical on every rank
 __global__ void k_nf_scan(Ctl* c, const double* v, int64_t n, int l) {
+  msb::count_launch();
   bool nf = false;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     nf |= !isfinite(v[e]);
@@ -1648,6 +1661,7 @@ __global__ void k_nf_scan(Ctl* c, const double* v, int64_t n, int l) {
 
 // sharded loop: FSAL k1 <- k_last on an accepted attempt (slot 0 stays k1)
 __global__ void k_fsal_copy(const Ctl* c, double* k1, const double* klast, int64_t n) {
+  msb::count_launch();
   if (!c->accepted) return;  // set by this attempt's k_finalize (stale only once done)
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     k1[e] = klast[e];

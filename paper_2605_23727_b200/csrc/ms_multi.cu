@@ -122,4 +122,6 @@ void launch_rhs_multi(const MultiArgs& m, int ns, int nds, int ndd, int ks, cons
   }
 }
 
+MS_DEFINE_LAUNCH_READER(launches_tu_multi)
+
 }  // namespace msb

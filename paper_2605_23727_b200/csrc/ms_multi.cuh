@@ -195,6 +195,7 @@ __device__ __forceinline__ void multi_tile(const unsigned char* sk, int warp, in
 template <int KS, int NS, int NDS, int NDD>
 __global__ void __launch_bounds__(kMultiThreads, 1)
     k_rhs_multi(const __grid_constant__ CUtensorMap tmK, MultiArgs a) {
+  msb::count_launch();
   constexpr int NL = NS + NDS + NDD;
   static_assert(NL >= 1 && NL <= kMaxLanes, "lane count");
   using G = MultiGeom<KS, NL>;

@@ -50,4 +50,6 @@ void launch_rhs_faithful(const RhsLaunch& L, const RhsArgs& a) {
   }
 }
 
+MS_DEFINE_LAUNCH_READER(launches_tu_faithful)
+
 }  // namespace msb

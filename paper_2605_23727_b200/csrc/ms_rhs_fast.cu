@@ -266,4 +266,6 @@ void launch_rhs_fast(const RhsLaunch& L, const RhsArgs& a) {
   }
 }
 
+MS_DEFINE_LAUNCH_READER(launches_tu_fast)
+
 }  // namespace msb

@@ -24,12 +24,18 @@ def _run(args, timeout=900):
 
 
 def test_reference_arm_contract():
-    d = _run(["--impl", "reference", "--n", "512", "--steps", "1", "--warmup", "0"])
+    d = _run(["--impl", "reference", "--n", "512", "--steps", "2", "--warmup", "1"])
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
     assert d["higher_is_better"] is True and d["value"] > 0 and d["unit"] == d["e2e"]["unit"]
     cb = d["cpu_baseline"]
     assert {"value", "unit", "cores", "kind", "sample"} <= set(cb) and cb["kind"] == "port" and cb["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    # the reference arm runs only the oracle (no library of this repo mapped),
+    # times attempts of the real solve prefix, and names the same config as ours
+    assert d["native_libs"] == ["oracle/liborc.so"], d["native_libs"]
+    assert d["prefix"]["evals"] >= 3 * d["steps"]
+    import bench
+    assert d["config"] == bench.workload_config(512, "f32", 1)
 
 
 @pytest.mark.gpu
@@ -42,3 +48,7 @@ def test_our_arm_contract(gpu):
     assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["config"]["workload"]
+    import bench
+    assert d["config"] == bench.workload_config(4096, "f32", 1)
+    # the launch count is the library's own device counter, not a formula
+    assert d["gpu_launches"] >= 3 * d["accepted_steps_per_solve"]

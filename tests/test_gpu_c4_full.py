@@ -94,20 +94,5 @@ def test_c4_device_k_rows_match_generator(gpu):
         assert np.array_equal(part.get_k(), ref)
         part.close()
 
-
-def test_c4_whole_solve_benchmark_policy(c4):
-    """The whole benchmark solve (SSS rows, t in [0, 20]) on the device and in
-    the oracle (OpenMP over rows, bitwise its sequential order; a few minutes):
-    the BASELINE.md §2 gate -- counts within 1 %, final state within 1e-5
-    weighted, else global error vs a tight DP5(4) run no worse than the
-    oracle's."""
-    import time
-    from _gates import gate
-    w, dev, orc = c4
-    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg)
-    t = time.perf_counter()
-    o = O.solve(orc, w.x0, w.t0, w.tf, w.policy, w.cfg)
-    print(f"oracle whole C4 solve: {time.perf_counter() - t:.1f} s on {os.cpu_count()} threads; "
-          f"device {r.device_ms:.1f} ms")
-    assert r.status == o.status == S.SolveStatus.Completed
-    gate(r, o, w.cfg, dev, w)
+# The whole benchmark solve against the oracle's whole solve: tests/test_gpu_golden_solves.py
+# (fixture c4_f32; also c4_f16 and c4_mixed2).

@@ -1,0 +1,123 @@
+"""Whole solves at BASELINE.json's stated configs, device against the oracle's
+whole solves committed under tests/golden/solves/ (tools/make_golden_solves.py;
+tests/test_golden_solves.py checks that the fixtures reproduce and match these
+inputs). The reference code pinned: the adaptive loop solver.cpp:226-347, the
+policies precision.cpp:22-42, eval_core systems.cpp:30-189.
+
+Gate (tests/_gates.py): accepted counts within 1 %, rejected
+within 1 % of the attempts, final state within 1e-5 (weighted like Eq. 7,
+floor ab/rel) of the oracle's; where two noise-driven step sequences end
+further apart than that, the device's global error against the tight binary64
+DP5(4) run (rel = abs = 1e-9) must be no larger than the oracle's
+(x1.5 + 1e-7).
+
+fp16 K (the tolerance the north star asks to state): the oracle rounds K to
+f16 exactly as the device stores it, so the device is held to the same gate.
+"""
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+import golden_cases as G
+from _gates import gate
+from paper_2605_23727_b200 import solver as S
+from paper_2605_23727_b200.systems import DeviceSystem
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+SINGLE = [k for k, c in G.CASES.items() if not c.get("batch")]
+
+
+def _fixture(name):
+    p = G.OUT / f"{name}.npz"
+    if not p.exists():
+        pytest.fail(f"missing golden fixture {p} (tools/make_golden_solves.py {name})")
+    return G.load(name)
+
+
+def _as_result(d):
+    return SimpleNamespace(status=S.SolveStatus(int(d["status"])), n_accepted=int(d["n_accepted"]),
+                           n_failed=int(d["n_failed"]), final_state=d["final_state"], t_reached=float(d["t_reached"]))
+
+
+@pytest.mark.parametrize("name", SINGLE)
+def test_whole_solve_vs_oracle_fixture(gpu, name):
+    case = G.CASES[name]
+    w = case["build"]()
+    d = _fixture(name)
+    assert G.input_hash(w) == d["meta"]["inputs"], "fixture made from other inputs: regenerate it"
+    dev = DeviceSystem(w.spec)
+    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg, log_capacity=1)
+    o = _as_result(d)
+    assert o.status == S.SolveStatus.Completed
+    assert r.t_reached == o.t_reached
+    # the evaluation budget of the reference loop (solver.cpp:255-306)
+    assert r.flops.rhs_evals == 3 + 3 * r.n_accepted + 4 * r.n_failed
+    gate(r, o, w.cfg, dev, w)
+    dev.close()
+
+
+def test_c4_mixed2_step_for_step(gpu):
+    """Mixed2 rows (binary64 sums, binary32 G) at C4: the device retraces the
+    oracle's step sequence. Each estimate differs from the oracle's only by the
+    sinf/cosf ulps of G (device: binary64 sincos rounded once; oracle: glibc),
+    so step sizes agree to a relative 1e-6 and accept/reject decisions agree
+    except where an estimate lands within that noise of rel_tol."""
+    name = "c4_mixed2"
+    w = G.CASES[name]["build"]()
+    d = _fixture(name)
+    assert G.input_hash(w) == d["meta"]["inputs"]
+    dev = DeviceSystem(w.spec)
+    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg)
+    lt, lh, la = d["log_t"], d["log_h"], d["log_acc"].astype(bool)
+    m = min(len(r.step_log), lt.size)
+    ra = np.array([s.accepted for s in r.step_log[:m]])
+    rh = np.array([s.h for s in r.step_log[:m]])
+    same = ra == la[:m]
+    first_split = int(np.argmin(same)) if not same.all() else m
+    print(f"C4 Mixed2: device {r.n_accepted}/{r.n_failed}, oracle {int(d['n_accepted'])}/{int(d['n_failed'])}; "
+          f"identical accept/reject sequence for the first {first_split} of {m} attempts")
+    # before the first differing decision the step sizes agree to the noise
+    assert np.all(np.abs(rh[:first_split] - lh[:first_split]) <= 1e-6 * lh[:first_split])
+    assert first_split >= min(m, 50)
+    gate(r, _as_result(d), w.cfg, dev, w)
+    dev.close()
+
+
+def test_c5_full_ensemble_vs_oracle(gpu):
+    """C5 at its stated size (B = 1024, N = 2048, t in [0, 20], K bf16,
+    tensor-core contraction): every trajectory's counts against the oracle's
+    per-trajectory solves with the same operand rounding (hi + lo bf16), the
+    ensemble totals within 1 %, and 16 sampled trajectories' final states."""
+    from paper_2605_23727_b200.batch import DeviceBatch
+    name = "c5_bf16"
+    w = G.CASES[name]["build"]()
+    d = _fixture(name)
+    assert G.input_hash(w) == d["meta"]["inputs"]
+    dev = DeviceSystem(w.spec)
+    bat = DeviceBatch(dev, w.omega, tensor_cores=True)
+    res = bat.solve(w.x0, w.t0, w.tf, w.policy, w.cfg)
+    assert np.all(res.status == 0) and np.all(d["status"] == 0)
+    assert np.array_equal(res.t_reached, d["t_reached"])
+    acc, rej = res.n_accepted.astype(np.int64), res.n_failed.astype(np.int64)
+    oacc, orej = d["n_accepted"], d["n_failed"]
+    att = oacc + orej
+    print(f"C5 ensemble: device {acc.sum()}/{rej.sum()}, oracle {oacc.sum()}/{orej.sum()}; per-trajectory max "
+          f"|d acc| {np.max(np.abs(acc - oacc))}, max |d rej| {np.max(np.abs(rej - orej))}")
+    assert abs(acc.sum() - oacc.sum()) <= 0.01 * oacc.sum()
+    assert abs(rej.sum() - orej.sum()) <= 0.01 * att.sum()
+    # per trajectory: near-threshold decisions flip on ulp-level differences
+    assert np.all(np.abs(acc - oacc) <= np.maximum(2, 0.03 * oacc))
+    assert np.all(np.abs(rej - orej) <= np.maximum(4, 0.05 * att))
+    assert np.array_equal(res.rhs_evals, 3 + 3 * acc + 4 * rej)
+    floor = w.cfg.abs_tol / w.cfg.rel_tol
+    worst = 0.0
+    for k, b in enumerate(d["sample"]):
+        of = d["final_states"][k]
+        rel = float(np.max(np.abs(res.final_state[b] - of) / np.maximum(np.abs(of), floor)))
+        worst = max(worst, rel)
+        assert rel <= 1e-5, (int(b), rel)
+    print(f"C5 sampled final states: worst weighted deviation {worst:.3e}")
+    bat.close()
+    dev.close()
