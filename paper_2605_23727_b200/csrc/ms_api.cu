@@ -215,6 +215,20 @@ __global__ void k_convert_rows(typename KElem<KS>::T* K, const SRC* src, int n, 
   }
 }
 
+// any nonzero |K| below kPkMinK (a product could then be subnormal, where the
+// packed FTZ multiply of the split sweeps would flush it)
+template <int KS>
+__global__ void k_scan_tiny(const typename KElem<KS>::T* K, int n, int rows, int64_t ld, int* flag) {
+  msb::count_launch();
+  const int64_t total = (int64_t)rows * n;
+  bool tiny = false;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const float v = fabsf(k2f(K[(q / n) * ld + q % n]));
+    tiny |= v != 0.f && v < kPkMinK;
+  }
+  if (__any_sync(0xffffffffu, tiny) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 template <int KS>
 __global__ void k_get_rows(const typename KElem<KS>::T* K, double* dst, int n, int rows, int64_t ld) {
   msb::count_launch();
@@ -275,6 +289,7 @@ struct ms_system {
   int n = 0, d = 0, cs = 0, ld = 0;
   int row0 = 0, row1 = 0;
   int ks = MS_K_SCALAR, rhs_mode = MS_RHS_FAST;
+  int k_tiny = 0;     // some nonzero |K| < 2^-80: the packed FTZ sweep path is off (ms_common.cuh mac2)
   int dev = 0, sms = kNumSMsDefault;
   cudaStream_t stream = nullptr;
   void* K = nullptr;
@@ -466,6 +481,11 @@ bool launch_prep(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e
   return launch_prep(s, st, prep_args(s, B, e, sp), sp);
 }
 
+bool env_is(const char* name, const char* value) {
+  const char* v = std::getenv(name);
+  return v && std::strcmp(v, value) == 0;
+}
+
 // K beyond ~3/4 of the 126 MB L2 cannot stay resident between evaluations:
 // the sweeps stream it with an evict-first policy
 int k_stream_of(const ms_system* s) {
@@ -496,6 +516,7 @@ RhsArgs rhs_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_
   a.coupling_k = s->md.coupling_k;
   a.ws32 = (is32(sp.f_prec) && is32(sp.sum_prec)) ? 1 : 0;
   a.k_stream = k_stream_of(s);
+  a.pk = env_is("MS_SWEEP_PK", "off") ? 0 : 1;
   return a;
 }
 
@@ -802,6 +823,7 @@ void init_ctl(ms_system* s, Ctl& c, const ms_solver_config& cfg, double t0, doub
   c.max_failed = cfg.max_failed_steps;
   c.log_capacity = log_cap;
   c.store32 = P.storage == MS_BINARY32 ? 1 : 0;
+  c.pk_off = s->k_tiny;
   c.time_limits = cfg.time_limits_enabled ? 1 : 0;
   c.record_log = cfg.record_step_log ? 1 : 0;
   c.snap_on = P.snaps ? 1 : 0;
@@ -1516,6 +1538,24 @@ msb::SysView msb::sys_view(ms_system_t s) {
   return v;
 }
 
+namespace {
+void scan_k_tiny(ms_system* s) {
+  int* flag = nullptr;
+  CK(cudaMalloc(&flag, sizeof(int)));
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), s->stream));
+  const int rows = s->row1 - s->row0, grid = 4 * s->sms;
+  if (s->ks == MS_K_F32) k_scan_tiny<MS_K_F32><<<grid, 256, 0, s->stream>>>((const float*)s->K, s->n, rows, s->ld, flag);
+  else if (s->ks == MS_K_F16) k_scan_tiny<MS_K_F16><<<grid, 256, 0, s->stream>>>((const __half*)s->K, s->n, rows, s->ld, flag);
+  else k_scan_tiny<MS_K_BF16><<<grid, 256, 0, s->stream>>>((const __nv_bfloat16*)s->K, s->n, rows, s->ld, flag);
+  CK(cudaGetLastError());
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  CK(cudaFree(flag));
+  s->k_tiny = h;
+}
+}  // namespace
+
 // =====================================================================================
 extern "C" {
 
@@ -1716,11 +1756,14 @@ int ms_system_create(const ms_system_desc* d, ms_system_t* out) {
         }
         CK(cudaFree(stage));
       }
+      CK(cudaDeviceSynchronize());
+      scan_k_tiny(s.get());
     }
     CK(cudaDeviceSynchronize());
     *out = s.release();
   });
 }
+
 
 int ms_system_destroy(ms_system_t s) {
   if (!s) return MS_OK;
@@ -1755,7 +1798,7 @@ int ms_system_fill_k_uniform(ms_system_t s, uint64_t seed, uint64_t stream, doub
     else if (s->ks == MS_K_F16) k_fill_uniform<MS_K_F16><<<grid, 256, 0, s->stream>>>((__half*)s->K, s->n, s->row0, rows, s->ld, state0, lo, hi);
     else k_fill_uniform<MS_K_BF16><<<grid, 256, 0, s->stream>>>((__nv_bfloat16*)s->K, s->n, s->row0, rows, s->ld, state0, lo, hi);
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(s->stream));
+    scan_k_tiny(s);
   });
 }
 
@@ -1797,6 +1840,7 @@ int ms_eval_rhs(ms_system_t s, double t, const double* x, ms_stage_prec sp, doub
     ensure_workspace(s, 1);
     Ctl& c = *s->ctl_host;
     std::memset(&c, 0, sizeof(Ctl));
+    c.pk_off = s->k_tiny;
     const int64_t dn = s->dn();
     CK(cudaMemcpyAsync(s->B.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(s->B.xb[0], x, sizeof(double) * dn, cudaMemcpyHostToDevice, s->stream));
@@ -1819,6 +1863,7 @@ int ms_profile_rhs(ms_system_t s, const double* x, ms_stage_prec sp, int iters, 
     ensure_workspace(s, 1);
     Ctl& c = *s->ctl_host;
     std::memset(&c, 0, sizeof(Ctl));
+    c.pk_off = s->k_tiny;
     cudaStream_t st = s->stream;
     CK(cudaMemcpyAsync(s->B.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(s->B.xb[0], x, sizeof(double) * s->dn(), cudaMemcpyHostToDevice, st));

@@ -90,6 +90,49 @@ template <class S, bool PACK = true> __device__ __forceinline__ void add2(S& a, 
   b = add<S>(b, y);
 }
 
+// ---- packed products for the split Kuramoto sweeps ---------------------------
+// {A, B} += {RN32(s k), RN32(c k)} for a packed accumulator AB = {A, B} and a
+// packed column pair sc = {s_j, c_j}: one FMUL2 (K broadcast) and one FADD2
+// instead of two FMUL and two FADD. The multiply carries .ftz: ptxas contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under -fmad=false (one rounding
+// less), but not a flush-to-zero multiply into a non-flushing add. The .ftz
+// changes nothing while no operand or product is subnormal: |K| >= 2^-80 for
+// every nonzero K (checked when K is created, ms_system::k_tiny) and
+// |s|, |c| >= 2^-46 for every nonzero s, c (checked by every prep, sticky in
+// Ctl::pk_off) bound every nonzero product by 2^-126 from below. Otherwise the
+// sweeps take the unflushed path (two FMUL, one FADD2), the same arithmetic.
+constexpr float kPkMinK = 0x1p-80f;
+constexpr float kPkMinSC = 0x1p-46f;
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t pk2u(uint32_t a, uint32_t b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ void unpk2(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+template <bool FTZ>
+__device__ __forceinline__ void mac2(uint64_t& ab, uint64_t sc, float k) {
+  uint64_t p;
+  if constexpr (FTZ) {
+    asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(p) : "l"(sc), "l"(pk2(k, k)));
+  } else {
+    float s, c;
+    unpk2(sc, s, c);
+    p = pk2(__fmul_rn(s, k), __fmul_rn(c, k));
+  }
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(ab) : "l"(p));
+}
+// sticky Ctl::pk_off when a column value is nonzero and below 2^-46
+__device__ __forceinline__ bool sc_tiny(float s, float c) {
+  return (s != 0.f && fabsf(s) < kPkMinSC) || (c != 0.f && fabsf(c) < kPkMinSC);
+}
+
 // RN into S of a double
 template <class S> __device__ __forceinline__ S cvt(double x);
 template <> __device__ __forceinline__ float cvt<float>(double x) { return __double2float_rn(x); }
@@ -164,7 +207,7 @@ struct Ctl {
   uint32_t ticket;        // last-block-done counter (finalize / init)
   int32_t snap_on;        // record StepSnapshots (solver.cpp:324-327)
   int32_t snap_pending;   // this attempt was accepted: k_snapshot copies x
-  int32_t _pad;
+  int32_t pk_off;         // packed FMUL2.FTZ sweep disabled: K has tiny entries, or a prep saw a tiny s/c
   double snap_hv;         // h of the accepted attempt (h_att before loop_check moves on)
   // dense output (D6 extension): sorted output times, the next unfilled one,
   // and the range [dense_lo, dense_hi) the accepted attempt covers

@@ -15,6 +15,7 @@
 //               272-342, 399-418), last-block-done over a grid reduction
 //   init_a/b    initial_step norms (solver.cpp:420-451)
 #pragma once
+#include <type_traits>
 
 #include "ms_common.cuh"
 #include "ms_ddpow.cuh"
@@ -97,6 +98,9 @@ struct RhsArgs {
   int count;
   // K larger than L2 can hold across evaluations: stream it evict-first
   int k_stream;
+  // packed FMUL2.FTZ products allowed (MS_SWEEP_PK != off; the device flag
+  // Ctl::pk_off can still veto them)
+  int pk;
 };
 
 __device__ __forceinline__ void sweep_count(const RhsArgs& a) {
@@ -281,8 +285,10 @@ __device__ __forceinline__ bool prep_agent(const PrepArgs& p, const PrepCtx& c, 
   if (p.split) {
     GS sv, cv;
     dsincos(xg, &sv, &cv);
-    gin[i] = sv;
-    gin[p.ld + i] = cv;
+    gin[2 * i] = sv;  // split column data: interleaved (s_j, c_j) pairs
+    gin[2 * i + 1] = cv;
+    if constexpr (sizeof(GS) == 4)
+      if (sc_tiny(sv, cv)) c.ctl->pk_off = 1;
   } else {
     gin[i] = xg;
   }
@@ -313,8 +319,12 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs p) {
   if (MODEL >= 0) {
     GS* gin = reinterpret_cast<GS*>(p.B.gin);
     for (int j = p.md.n + blockIdx.x * blockDim.x + threadIdx.x; j < p.ld; j += gridDim.x * blockDim.x) {
-      gin[j] = GS(0);
-      if (p.split) gin[p.ld + j] = GS(0);
+      if (p.split) {
+        gin[2 * j] = GS(0);
+        gin[2 * j + 1] = GS(0);
+      } else {
+        gin[j] = GS(0);
+      }
     }
   }
   if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(&ctl->nf_mask, 1 << p.l);
@@ -478,6 +488,11 @@ template <> struct KVec<MS_K_SCALAR> {
 #define MS_FAST_FADD2 0      // packed FADD2 accumulation in the register sweep: measured slower (f16 K)
 #endif
 constexpr bool kFastFadd2 = MS_FAST_FADD2;
+// packed (FMUL2.FTZ + FADD2, ms_common.cuh mac2) products in the binary32
+// split sweeps; 0 = two scalar FMUL per K element
+#ifndef MS_SWEEP_PK
+#define MS_SWEEP_PK 1
+#endif
 constexpr int kFastThreads = MS_FAST_THREADS;
 constexpr int kFastMinBlocks = MS_FAST_MINB;
 constexpr int kFastWarps = kFastThreads / 32;
@@ -561,9 +576,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
     const int cc = chunk_cols(c);
     const uint32_t bytes = (uint32_t)(cc * sizeof(GS));
     mbar_expect_tx(&full[st], bytes * NCOL);
-    for (int t = 0; t < NCOL; ++t)
-      bulk_g2s(stage_buf + (size_t)(st * NCOL + t) * kChunkCols, gin + (size_t)t * ld + (size_t)c * kChunkCols,
-               bytes, &full[st]);
+    // split: the (s_j, c_j) pairs of the chunk are one contiguous run
+    bulk_g2s(stage_buf + (size_t)st * NCOL * kChunkCols, gin + (size_t)NCOL * c * kChunkCols, bytes * NCOL,
+             &full[st]);
   };
 
   if (threadIdx.x == 0) {
@@ -578,6 +593,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
   if (threadIdx.x == 0)
     for (int q = 0; q < min(kStagesNS, Q); ++q) issue(q);
 
+  constexpr bool kPk = SPLIT && sizeof(SS) == 4 && sizeof(GS) == 4 && KS != MS_K_SCALAR && MS_SWEEP_PK;
+  const bool use_pk = kPk && a.pk && a.ctl->pk_off == 0;
   const SS mw = cvt<SS>(a.mw);
   const GS kscal = cvt<GS>(a.coupling_k);
   using KT = typename KElem<KS == MS_K_SCALAR ? MS_K_F32 : KS>::T;
@@ -606,20 +623,60 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
     SS A[R], B[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) { A[k] = SS(0); B[k] = SS(0); }
+    uint64_t AB[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) AB[k] = 0ull;
 
     for (int c = 0; c < nchunks; ++c, ++q) {
       const int st = q % kStagesNS;
       const int cc = chunk_cols(c);
       mbar_wait(&full[st], (q / kStagesNS) & 1);
-      const GS* sv = stage_buf + (size_t)(st * NCOL) * kChunkCols;
-      const GS* cv = sv + kChunkCols;
+      const GS* sv = stage_buf + (size_t)(st * NCOL) * kChunkCols;  // split: (s, c) pairs
 #ifndef MS_PREFETCH
 #define MS_PREFETCH 0
 #endif
       // fp64 accumulation (R = 4) gains from software pipelining, fp32 (R = 8)
       // from more rows in flight (tools/tune_rhs.py, profiles/r1_tune_rhs.txt)
       constexpr bool kPrefetch = MS_PREFETCH || (sizeof(SS) == 8 || sizeof(GS) == 8);
-      if (nr > 0 && kPrefetch && KS != MS_K_SCALAR) {
+      if (kPk && use_pk) {
+        // binary32 split rows, packed products: the lane's (s, c) pairs are
+        // read straight from the interleaved chunk, one FMUL2 + FADD2 per element
+        if (nr > 0) {
+          // row pointers of this chunk (lane offset included); a row past the
+          // CTA's range re-reads row rows[0] (valid memory), its sums are never written
+          const uint4* kp[R];
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            kp[k] = reinterpret_cast<const uint4*>(Kbase + (size_t)((k < nr ? rows[k] : rows[0]) - a.row0) * ld +
+                                                   c * kChunkCols + lane * VEC);
+          const uint4* sp = reinterpret_cast<const uint4*>(sv) + lane * (VEC / 2);
+          auto step = [&](int it) {
+            uint64_t pr[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC / 2; ++v) {
+              const uint4 qv = sp[it * 16 * VEC + v];
+              pr[2 * v] = pk2u(qv.x, qv.y);
+              pr[2 * v + 1] = pk2u(qv.z, qv.w);
+            }
+            uint4 kv[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) kv[k] = ldg_stream(kp[k] + it * 32, kpol);
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              float kf[VEC];
+              KVec<KS>::unpack(kv[k], kf);
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) mac2<true>(AB[k], pr[v], kf[v]);
+            }
+          };
+          if (cc == kChunkCols) {
+#pragma unroll 4
+            for (int it = 0; it < kChunkCols / COLS_IT; ++it) step(it);
+          } else {
+            for (int it = 0; lane * VEC + it * COLS_IT < cc; ++it) step(it);
+          }
+        }
+      } else if (nr > 0 && kPrefetch && KS != MS_K_SCALAR) {
         // software-pipelined: the next step's K vectors are in flight while
         // the current ones are consumed
         const int c0 = c * kChunkCols;
@@ -637,8 +694,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
           GS s_loc[VEC], c_loc[VEC];
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
-            s_loc[v] = sv[col + v];
-            if (SPLIT) c_loc[v] = cv[col + v];
+            s_loc[v] = sv[NCOL * (col + v)];
+            if (SPLIT) c_loc[v] = sv[NCOL * (col + v) + 1];
           }
           sweep_step<MODEL, SPLIT, SS, GS, KS, R, VEC>(kv, nr, s_loc, c_loc, xi, pref, A, B);
 #pragma unroll
@@ -650,8 +707,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
           GS s_loc[VEC], c_loc[VEC];
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
-            s_loc[v] = sv[col + v];
-            if (SPLIT) c_loc[v] = cv[col + v];
+            s_loc[v] = sv[NCOL * (col + v)];
+            if (SPLIT) c_loc[v] = sv[NCOL * (col + v) + 1];
           }
           if constexpr (KS == MS_K_SCALAR) {
 #pragma unroll
@@ -688,6 +745,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
         __syncwarp();
       }
     }
+    if (kPk && use_pk) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        float a0, b0;
+        unpk2(AB[k], a0, b0);
+        A[k] = a0;
+        B[k] = b0;
+      }
+    }
     // warp-shuffle reduction of every row, then lane k writes row k
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -703,7 +769,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
         const int r = rows[k];
         SS coup;
         if (SPLIT) {
-          const SS si = (SS)gin[r], ci = (SS)gin[ld + r];
+          const SS si = (SS)gin[2 * r], ci = (SS)gin[2 * r + 1];
           coup = mul<SS>(mw, sub<SS>(mul<SS>(ci, A[k]), mul<SS>(si, B[k])));
         } else {
           coup = mul<SS>(mw, A[k]);
@@ -766,8 +832,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
   for (int j = threadIdx.x; j < ld; j += blockDim.x) {
     if (PREPPED) {
       const GS* g = reinterpret_cast<const GS*>(a.gin);
-      colv[j] = j < n ? g[j] : GS(0);
-      if (SPLIT) colv[ld + j] = j < n ? g[ld + j] : GS(0);
+      if (SPLIT) {
+        colv[j] = j < n ? g[2 * j] : GS(0);
+        colv[ld + j] = j < n ? g[2 * j + 1] : GS(0);
+      } else {
+        colv[j] = j < n ? g[j] : GS(0);
+      }
     } else if (j < n) {
       const GS xg = cvt<GS>(prep_arg(p, c, (int64_t)j * d, false));
       if (SPLIT) {
@@ -866,7 +936,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
         const int r = rows[k];
         SS coup;
         if (SPLIT) {
-          const SS si = (SS)gin[r], ci = (SS)gin[ld + r];
+          const SS si = (SS)gin[2 * r], ci = (SS)gin[2 * r + 1];
           coup = mul<SS>(mw, sub<SS>(mul<SS>(ci, A[k]), mul<SS>(si, B[k])));
         } else {
           coup = mul<SS>(mw, A[k]);
@@ -969,15 +1039,15 @@ struct TmaGeom {
 // staged tile against each of the warp's rows (A += K s, B += K c; ascending
 // columns per lane, as in k_rhs_fast).
 template <class SS, class GS, int KS, int RPW, int TC, bool CHECK>
-__device__ __forceinline__ void tma_col_step(const unsigned char* sk, const GS* sv, const GS* cv, int col,
+__device__ __forceinline__ void tma_col_step(const unsigned char* sk, const GS* sc, int col,
                                              const int (&rows)[RPW], int nr, SS (&A)[RPW], SS (&B)[RPW]) {
   using KT = typename KElem<KS>::T;
   constexpr int VEC = KVec<KS>::N;
   GS s_loc[VEC], c_loc[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    s_loc[v] = sv[col + v];
-    c_loc[v] = cv[col + v];
+    s_loc[v] = sc[2 * (col + v)];
+    c_loc[v] = sc[2 * (col + v) + 1];
   }
 #pragma unroll
   for (int k = 0; k < RPW; ++k) {
@@ -990,6 +1060,36 @@ __device__ __forceinline__ void tma_col_step(const unsigned char* sk, const GS* 
         const GS kg = (GS)kf[v];
         add2<SS>(A[k], B[k], (SS)mul<GS>(kg, s_loc[v]), (SS)mul<GS>(kg, c_loc[v]));
       }
+    }
+  }
+}
+
+// The same warp step for binary32 sums and columns with packed accumulators
+// AB[k] = {A_k, B_k}: the lane's (s, c) pairs come straight from the
+// interleaved staged columns (LDS.128 = two pairs), one FMUL2 + one FADD2 per
+// K element (mac2). Bit-identical to tma_col_step (same products, same sums,
+// same order).
+template <int KS, int RPW, int TC, bool CHECK>
+__device__ __forceinline__ void tma_col_step_pk(const unsigned char* sk, const float* sc, int col,
+                                                const int (&rows)[RPW], int nr, uint64_t (&AB)[RPW]) {
+  using KT = typename KElem<KS>::T;
+  constexpr int VEC = KVec<KS>::N;
+  uint64_t pr[VEC];
+  const uint4* sp = reinterpret_cast<const uint4*>(sc + 2 * col);
+#pragma unroll
+  for (int v = 0; v < VEC / 2; ++v) {
+    const uint4 q = sp[v];
+    pr[2 * v] = pk2u(q.x, q.y);
+    pr[2 * v + 1] = pk2u(q.z, q.w);
+  }
+#pragma unroll
+  for (int k = 0; k < RPW; ++k) {
+    if (!CHECK || k < nr) {
+      const uint4 kv = *reinterpret_cast<const uint4*>(sk + ((size_t)rows[k] * TC + col) * sizeof(KT));
+      float kf[VEC];
+      KVec<KS>::unpack(kv, kf);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) mac2<true>(AB[k], pr[v], kf[v]);
     }
   }
 }
@@ -1057,12 +1157,11 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
       GS* ss = reinterpret_cast<GS*>(sk + G::KBYTES);
       if (lane == 0) {
         mbar_expect_tx(&full[st], kbytes * nr + 2 * sbytes);
+        // the tile's (s_j, c_j) pairs: one contiguous run of the interleaved column data
 #if MS_TMA_KHINT
-        bulk_g2s_hint(ss, gin + c0, sbytes, &full[st], pol_sc);
-        bulk_g2s_hint(ss + G::TC, gin + (size_t)ld + c0, sbytes, &full[st], pol_sc);
+        bulk_g2s_hint(ss, gin + 2 * (size_t)c0, 2 * sbytes, &full[st], pol_sc);
 #else
-        bulk_g2s(ss, gin + c0, sbytes, &full[st]);
-        bulk_g2s(ss + G::TC, gin + (size_t)ld + c0, sbytes, &full[st]);
+        bulk_g2s(ss, gin + 2 * (size_t)c0, 2 * sbytes, &full[st]);
 #endif
       }
       if (MS_TMA_LANES) {
@@ -1085,6 +1184,8 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
   }
 
   // consumers: warp w owns rows w, w + CONS, ... of every group
+  constexpr bool kPk = sizeof(SS) == 4 && sizeof(GS) == 4 && MS_SWEEP_PK;
+  const bool use_pk = kPk && a.pk && a.ctl->pk_off == 0;
   const SS mw = cvt<SS>(a.mw);
   double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
   bool nonfinite = false;
@@ -1102,25 +1203,46 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
     SS A[G::RPW], B[G::RPW];
 #pragma unroll
     for (int k = 0; k < G::RPW; ++k) { A[k] = SS(0); B[k] = SS(0); }
+    uint64_t AB[G::RPW];
+#pragma unroll
+    for (int k = 0; k < G::RPW; ++k) AB[k] = 0ull;
     for (int t = 0; t < ntiles; ++t, ++q) {
       const int st = q % G::NS;
       const int cc = min(G::TC, ld - t * G::TC);
       mbar_wait(&full[st], (q / G::NS) & 1);
       const unsigned char* sk = smem + (size_t)st * G::STAGE_BYTES;
-      const GS* sv = reinterpret_cast<const GS*>(sk + G::KBYTES);
-      const GS* cv = sv + G::TC;
-      if (nr == G::RPW && cc == G::TC) {
+      const GS* sc = reinterpret_cast<const GS*>(sk + G::KBYTES);  // (s, c) pairs
+      if (kPk && use_pk) {
+        const float* scf = reinterpret_cast<const float*>(sc);
+        if (nr == G::RPW && cc == G::TC) {
+#pragma unroll kTmaUnroll
+          for (int it = 0; it < G::TC / COLS_IT; ++it)
+            tma_col_step_pk<KS, G::RPW, G::TC, false>(sk, scf, lane * VEC + it * COLS_IT, rows, nr, AB);
+        } else if (nr > 0) {
+          for (int col = lane * VEC; col < cc; col += COLS_IT)
+            tma_col_step_pk<KS, G::RPW, G::TC, true>(sk, scf, col, rows, nr, AB);
+        }
+      } else if (nr == G::RPW && cc == G::TC) {
         // full tile, every row valid: a fixed trip count the compiler unrolls,
         // so the shared-memory loads of later column steps are issued ahead
 #pragma unroll kTmaUnroll
         for (int it = 0; it < G::TC / COLS_IT; ++it)
-          tma_col_step<SS, GS, KS, G::RPW, G::TC, false>(sk, sv, cv, lane * VEC + it * COLS_IT, rows, nr, A, B);
+          tma_col_step<SS, GS, KS, G::RPW, G::TC, false>(sk, sc, lane * VEC + it * COLS_IT, rows, nr, A, B);
       } else if (nr > 0) {
         for (int col = lane * VEC; col < cc; col += COLS_IT)
-          tma_col_step<SS, GS, KS, G::RPW, G::TC, true>(sk, sv, cv, col, rows, nr, A, B);
+          tma_col_step<SS, GS, KS, G::RPW, G::TC, true>(sk, sc, col, rows, nr, A, B);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    if (kPk && use_pk) {
+#pragma unroll
+      for (int k = 0; k < G::RPW; ++k) {
+        float a0, b0;
+        unpk2(AB[k], a0, b0);
+        A[k] = a0;
+        B[k] = b0;
+      }
     }
 #pragma unroll
     for (int k = 0; k < G::RPW; ++k) {
@@ -1134,7 +1256,7 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
     for (int k = 0; k < G::RPW; ++k) {
       if (lane == k && k < nr) {
         const int r = r0 + rows[k];
-        const SS si = (SS)gin[r], ci = (SS)gin[ld + r];
+        const SS si = (SS)gin[2 * r], ci = (SS)gin[2 * r + 1];
         const SS coup = mul<SS>(mw, sub<SS>(mul<SS>(ci, A[k]), mul<SS>(si, B[k])));
         const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
         out[(int64_t)r * a.d + a.cs] = o;
@@ -1154,8 +1276,8 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
     if (blockIdx.x == 0) {  // the padding columns of the target buffer (k_prep does the same)
       GS* g = reinterpret_cast<GS*>(pn.B.gin);
       for (int j = pn.md.n + (int)threadIdx.x; j < pn.ld; j += G::CONS * 32) {
-        g[j] = GS(0);
-        g[pn.ld + j] = GS(0);
+        g[2 * j] = GS(0);
+        g[2 * j + 1] = GS(0);
       }
     }
   }

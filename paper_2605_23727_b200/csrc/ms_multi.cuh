@@ -151,8 +151,8 @@ __device__ __forceinline__ void multi_tile(const unsigned char* sk, int warp, in
     float s0[VEC], c0[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
-      s0[e] = p[col + e];
-      c0[e] = p[TC + col + e];
+      s0[e] = p[2 * (col + e)];
+      c0[e] = p[2 * (col + e) + 1];
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -176,8 +176,8 @@ __device__ __forceinline__ void multi_tile(const unsigned char* sk, int warp, in
     double s0[VEC], c0[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
-      s0[e] = p[col + e];
-      c0[e] = p[TC + col + e];
+      s0[e] = p[2 * (col + e)];
+      c0[e] = p[2 * (col + e) + 1];
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -262,8 +262,8 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
           const uint32_t es = v >= NS + NDS ? 8u : 4u;
           const unsigned char* gp = reinterpret_cast<const unsigned char*>(a.lane[v].gin);
           unsigned char* dst = sk + G::KTILE + (size_t)v * G::LANEB;
-          bulk_g2s(dst, gp + (size_t)t * TC * es, (uint32_t)cc * es, &full[st]);
-          bulk_g2s(dst + (size_t)TC * es, gp + ((size_t)ld + (size_t)t * TC) * es, (uint32_t)cc * es, &full[st]);
+          // the lane's (s_j, c_j) pairs of the tile: one run of the interleaved column data
+          bulk_g2s(dst, gp + (size_t)2 * t * TC * es, 2u * (uint32_t)cc * es, &full[st]);
         }
         if (++st == G::NS) {
           st = 0;
@@ -342,17 +342,17 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
         const LaneArgs& L = a.lane[v];
         double coup;
         if (v < NS) {
-          const float si = reinterpret_cast<const float*>(L.gin)[r], ci = reinterpret_cast<const float*>(L.gin)[ld + r];
+          const float si = reinterpret_cast<const float*>(L.gin)[2 * r], ci = reinterpret_cast<const float*>(L.gin)[2 * r + 1];
           const float mwf = __double2float_rn(a.mw);
           coup = (double)__fmul_rn(mwf, __fsub_rn(__fmul_rn(ci, AS[v][k][0]), __fmul_rn(si, AS[v][k][1])));
         } else {
           double si, ci;
           if (v < NS + NDS) {
-            si = (double)reinterpret_cast<const float*>(L.gin)[r];
-            ci = (double)reinterpret_cast<const float*>(L.gin)[ld + r];
+            si = (double)reinterpret_cast<const float*>(L.gin)[2 * r];
+            ci = (double)reinterpret_cast<const float*>(L.gin)[2 * r + 1];
           } else {
-            si = reinterpret_cast<const double*>(L.gin)[r];
-            ci = reinterpret_cast<const double*>(L.gin)[ld + r];
+            si = reinterpret_cast<const double*>(L.gin)[2 * r];
+            ci = reinterpret_cast<const double*>(L.gin)[2 * r + 1];
           }
           const int w = NS > 0 ? (v - NS) : v;
           coup = __dmul_rn(a.mw, __dsub_rn(__dmul_rn(ci, AD[w][k][0]), __dmul_rn(si, AD[w][k][1])));

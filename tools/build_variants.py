@@ -118,6 +118,18 @@ VARIANTS = {
     "pow_libm_api": ("ms_api.cu", {"MS_POW_ROOT_START": 0}),
     "pow_libm_batch": ("ms_batch.cu", {"MS_POW_ROOT_START": 0}),
     "k16_c12r2_48k": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 12, "MS_TMA_RPW_K16": 2, "MS_TMA_KB_K16": 49152}),
+    # round 2, packed FMUL2.FTZ products: register sweep rows per warp, 16-bit K TMA geometry
+    "fr4": ("ms_rhs_fast.cu", {"MS_FAST_R": 4}),
+    "fr12": ("ms_rhs_fast.cu", {"MS_FAST_R": 12}),
+    "fr16": ("ms_rhs_fast.cu", {"MS_FAST_R": 16}),
+    "fr8_t256": ("ms_rhs_fast.cu", {"MS_FAST_THREADS": 256, "MS_FAST_MINB": 2}),
+    "pk_c16r2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 16, "MS_TMA_RPW_K16": 2}),
+    "pk_c8r2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 8, "MS_TMA_RPW_K16": 2}),
+    "pk_c4r8": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 4, "MS_TMA_RPW_K16": 8}),
+    "pk_c8r8": ("ms_rhs_fast.cu", {"MS_TMA_CONS_K16": 8, "MS_TMA_RPW_K16": 8}),
+    "pk_c8r4_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_KB_K16": 32768, "MS_TMA_STAGES": 6}),
+    "pk_sss_c4r4": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 4, "MS_TMA_RPW_SSS": 4}),
+    "pk_sss_c4r2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 4, "MS_TMA_RPW_SSS": 2}),
 }
 
 
