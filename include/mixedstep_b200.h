@@ -90,7 +90,12 @@ enum { MS_HOST_F64 = 0, MS_HOST_F32 = 1 };
  *               split; tolerance parity;
  *   FAITHFUL  — one thread per row, ascending j including j = i, per-pair G,
  *               exactly the order of eval_core (systems.cpp:50-57). */
-enum { MS_RHS_FAST = 0, MS_RHS_FAITHFUL = 1 };
+/* RHS evaluation order: FAST = blocked/tree sums (tolerance parity; Kuramoto
+ * split into K sin / K cos); FAITHFUL = eval_core's sequential order with
+ * per-pair G (systems.cpp:30-64); ORDERED = the Kuramoto split summed in
+ * sequential order (the oracle's split form bit for bit; other models: as
+ * FAITHFUL) */
+enum { MS_RHS_FAST = 0, MS_RHS_FAITHFUL = 1, MS_RHS_ORDERED = 2 };
 
 /* StagePrecision, precision.hpp:36-42 */
 typedef struct {

@@ -216,7 +216,9 @@ int orc_system_create(const ms_system_desc* d, void** out) {
     if (p.kind == ModelKind::Kuramoto && p.omega.empty()) throw std::invalid_argument("kuramoto: omega required");
     if (p.kind == ModelKind::CC && (p.k1.empty() || p.theta_h.empty()))
       throw std::invalid_argument("cc: k1 and theta_h required");
-    p.split = p.kind == ModelKind::Kuramoto && d->rhs_mode == MS_RHS_FAST;
+    // the split form for the fast and ordered modes;
+    // the oracle always sums in ascending j (the device's ordered mode)
+    p.split = p.kind == ModelKind::Kuramoto && (d->rhs_mode == MS_RHS_FAST || d->rhs_mode == MS_RHS_ORDERED);
     s->k_storage = d->k_storage;
     if (d->k_storage != MS_K_SCALAR && d->K) {
       auto K = std::make_shared<std::vector<float>>(static_cast<size_t>(n) * static_cast<size_t>(n));

@@ -24,7 +24,7 @@ MS_MODEL_LCO, MS_MODEL_KURAMOTO, MS_MODEL_CC = 0, 1, 2
 MS_MODEL_SCALAR_EXP, MS_MODEL_SCALAR_ZERO, MS_MODEL_SCALAR_NAN = 16, 17, 18
 MS_K_SCALAR, MS_K_F32, MS_K_F16, MS_K_BF16 = 0, 1, 2, 3
 MS_HOST_F64, MS_HOST_F32 = 0, 1
-MS_RHS_FAST, MS_RHS_FAITHFUL = 0, 1
+MS_RHS_FAST, MS_RHS_FAITHFUL, MS_RHS_ORDERED = 0, 1, 2
 
 
 class StagePrec(C.Structure):

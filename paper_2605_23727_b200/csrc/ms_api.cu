@@ -325,6 +325,12 @@ struct ms_system {
   int64_t dn() const { return (int64_t)n * d; }
 };
 
+// the Kuramoto sin/cos split: the column data are (s_j, c_j) pairs
+bool split_of(const ms_system* s) {
+  return s->mkind == MD_KUR && (s->rhs_mode == MS_RHS_FAST || s->rhs_mode == MS_RHS_ORDERED);
+}
+
+
 namespace {
 
 void set_device(ms_system* s) { CK(cudaSetDevice(s->dev)); }
@@ -452,7 +458,7 @@ PrepArgs prep_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stag
   }
   p.is_last = e.is_last;
   p.round_x = e.round_x;
-  p.split = (s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST) ? 1 : 0;
+  p.split = split_of(s) ? 1 : 0;
   p.ws32 = (fs32 && ss32) ? 1 : 0;
   p.fs32 = fs32 ? 1 : 0;
   p.ld = s->ld;
@@ -521,7 +527,7 @@ RhsArgs rhs_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_
 }
 
 void launch_sweep(ms_system* s, cudaStream_t st, const RhsArgs& a, const ms_stage_prec& sp) {
-  const bool split = s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST;
+  const bool split = split_of(s);
   RhsLaunch L{s->mkind, split, is32(sp.sum_prec), is32(sp.g_prec), s->ks, s->sms, st};
   if (s->rhs_mode == MS_RHS_FAST) launch_rhs_fast(L, a);
   else launch_rhs_faithful(L, a);
@@ -543,7 +549,7 @@ void launch_eval(ms_system* s, const Bufs& B, cudaStream_t st, const EvalSpec& e
   if (!launch_prep(s, B, st, e, sp)) return;
   const RhsArgs a = rhs_args(s, B, e, sp);
   if (mid0) CK(cudaEventRecord(mid0, st));
-  const bool split = s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST;
+  const bool split = s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST;  // fast-mode sweeps only
   RhsLaunch L{s->mkind, split, is32(sp.sum_prec), is32(sp.g_prec), s->ks, s->sms, st};
   if (!(split && launch_sweep_small(L, prep_args(s, B, e, sp), a))) launch_sweep(s, st, a, sp);
   if (mid1) CK(cudaEventRecord(mid1, st));
@@ -1674,7 +1680,8 @@ int ms_system_create(const ms_system_desc* d, ms_system_t* out) {
     s->ks = d->k_storage;
     if (s->ks < MS_K_SCALAR || s->ks > MS_K_BF16) throw InvalidArg("system: bad K storage");
     s->rhs_mode = d->rhs_mode;
-    if (s->rhs_mode != MS_RHS_FAST && s->rhs_mode != MS_RHS_FAITHFUL) throw InvalidArg("system: bad rhs mode");
+    if (s->rhs_mode != MS_RHS_FAST && s->rhs_mode != MS_RHS_FAITHFUL && s->rhs_mode != MS_RHS_ORDERED)
+      throw InvalidArg("system: bad rhs mode");
     s->ld = (n + 7) & ~7;
     s->row0 = d->row_begin;
     s->row1 = d->row_end;

@@ -493,6 +493,9 @@ constexpr bool kFastFadd2 = MS_FAST_FADD2;
 #ifndef MS_SWEEP_PK
 #define MS_SWEEP_PK 1
 #endif
+#ifndef MS_PK_PREFETCH
+#define MS_PK_PREFETCH 0   // software-pipelined K loads in the packed register sweep
+#endif
 constexpr int kFastThreads = MS_FAST_THREADS;
 constexpr int kFastMinBlocks = MS_FAST_MINB;
 constexpr int kFastWarps = kFastThreads / 32;
@@ -638,19 +641,45 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
       // fp64 accumulation (R = 4) gains from software pipelining, fp32 (R = 8)
       // from more rows in flight (tools/tune_rhs.py, profiles/r1_tune_rhs.txt)
       constexpr bool kPrefetch = MS_PREFETCH || (sizeof(SS) == 8 || sizeof(GS) == 8);
-      if (kPk && use_pk) {
+      if constexpr (kPk) {
         // binary32 split rows, packed products: the lane's (s, c) pairs are
         // read straight from the interleaved chunk, one FMUL2 + FADD2 per element
         if (nr > 0) {
-          // row pointers of this chunk (lane offset included); a row past the
-          // CTA's range re-reads row rows[0] (valid memory), its sums are never written
-          const uint4* kp[R];
+          // row offsets of this chunk in 16-byte units (lane offset included);
+          // a row past the CTA's range re-reads row rows[0] (valid memory) and
+          // its sums are never written
+          const uint4* kb4 = reinterpret_cast<const uint4*>(Kbase);
+          uint32_t ko[R];  // < 2^32 x 16 B: K of up to 64 GB per handle
 #pragma unroll
           for (int k = 0; k < R; ++k)
-            kp[k] = reinterpret_cast<const uint4*>(Kbase + (size_t)((k < nr ? rows[k] : rows[0]) - a.row0) * ld +
-                                                   c * kChunkCols + lane * VEC);
+            ko[k] = (uint32_t)(((size_t)((k < nr ? rows[k] : rows[0]) - a.row0) * ld + (size_t)c * kChunkCols) / VEC +
+                               lane);
           const uint4* sp = reinterpret_cast<const uint4*>(sv) + lane * (VEC / 2);
-          auto step = [&](int it) {
+          const int nit = cc == kChunkCols ? kChunkCols / COLS_IT : (cc - lane * VEC + COLS_IT - 1) / COLS_IT;
+          auto sweep_chunk = [&](auto ftz) {
+#if MS_PK_PREFETCH
+          // software-pipelined: the next step's K vectors are in flight while
+          // the current ones are consumed (twice the bytes in flight per thread)
+          uint4 kn[R];
+          if (nit > 0) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) kn[k] = ldg_stream(kb4 + ko[k], kpol);
+          }
+#endif
+#pragma unroll 1
+          for (int it = 0; it < nit; ++it) {
+            uint4 kv[R];
+#if MS_PK_PREFETCH
+#pragma unroll
+            for (int k = 0; k < R; ++k) kv[k] = kn[k];
+            if (it + 1 < nit) {
+#pragma unroll
+              for (int k = 0; k < R; ++k) kn[k] = ldg_stream(kb4 + ko[k] + (it + 1) * 32, kpol);
+            }
+#else
+#pragma unroll
+            for (int k = 0; k < R; ++k) kv[k] = ldg_stream(kb4 + ko[k] + it * 32, kpol);
+#endif
             uint64_t pr[VEC];
 #pragma unroll
             for (int v = 0; v < VEC / 2; ++v) {
@@ -658,23 +687,17 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
               pr[2 * v] = pk2u(qv.x, qv.y);
               pr[2 * v + 1] = pk2u(qv.z, qv.w);
             }
-            uint4 kv[R];
-#pragma unroll
-            for (int k = 0; k < R; ++k) kv[k] = ldg_stream(kp[k] + it * 32, kpol);
 #pragma unroll
             for (int k = 0; k < R; ++k) {
               float kf[VEC];
               KVec<KS>::unpack(kv[k], kf);
 #pragma unroll
-              for (int v = 0; v < VEC; ++v) mac2<true>(AB[k], pr[v], kf[v]);
+              for (int v = 0; v < VEC; ++v) mac2<decltype(ftz)::value>(AB[k], pr[v], kf[v]);
             }
-          };
-          if (cc == kChunkCols) {
-#pragma unroll 4
-            for (int it = 0; it < kChunkCols / COLS_IT; ++it) step(it);
-          } else {
-            for (int it = 0; lane * VEC + it * COLS_IT < cc; ++it) step(it);
           }
+          };
+          if (use_pk) sweep_chunk(std::true_type{});
+          else sweep_chunk(std::false_type{});  // unflushed products (Ctl::pk_off, MS_SWEEP_PK=off)
         }
       } else if (nr > 0 && kPrefetch && KS != MS_K_SCALAR) {
         // software-pipelined: the next step's K vectors are in flight while
@@ -745,7 +768,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
         __syncwarp();
       }
     }
-    if (kPk && use_pk) {
+    if constexpr (kPk) {
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         float a0, b0;
@@ -1284,41 +1307,105 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
 }
 
 // ------------------------------------------------------------------------------
-// rhs_faithful: eval_core's exact order (systems.cpp:50-57): per row, ascending
-// j including j = i, acc = acc + mw * (SS)G_ij, G in GS with RN_GS(K_ij).
-template <int MODEL, class SS, class GS, int KS>
-__global__ void __launch_bounds__(128) k_rhs_faithful(RhsArgs a) {
+// rhs_seq: every row's coupling sum in eval_core's exact order
+// (systems.cpp:50-57): ascending j including j = i, acc = acc (+) term_j in SS,
+// with term_j = mw * (SS)G_ij (faithful: per-pair G in GS with RN_GS(K_ij))
+// or, for the Kuramoto split in sequential order (MS_RHS_ORDERED), the pair
+// (RN_SS(K s_j), RN_SS(K c_j)) and the coupling mw (c_i A - s_i B) at the end —
+// the oracle's split form bit for bit (up to the libm ulp of sin/cos).
+// Only the additions are sequential: a CTA owns kSeqRows rows; per tile of
+// kSeqCols columns its warps 1..7 compute the terms of all (row, column) pairs
+// in parallel (K read row-major, coalesced along j) into a double-buffered
+// shared tile, while warp 0 (lane = row) adds the previous tile's terms in
+// ascending j. Terms of a tile are summed only after the tile is complete.
+constexpr int kSeqRows = 32, kSeqThreads = 256;
+template <class SS, bool SPLIT> struct SeqGeom {
+  static constexpr int COLS = sizeof(SS) == 8 && SPLIT ? 64 : 128;   // columns per tile
+  static constexpr int PITCH = COLS + 1;                              // conflict-free row reads
+  static constexpr int NACC = SPLIT ? 2 : 1;
+  static constexpr size_t SMEM = (size_t)2 * NACC * kSeqRows * PITCH * sizeof(SS);
+};
+
+template <int MODEL, bool SPLIT, class SS, class GS, int KS>
+__global__ void __launch_bounds__(kSeqThreads) k_rhs_seq(RhsArgs a) {
   msb::count_launch();
+  pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   sweep_count(a);
-  const int r = a.row0 + blockIdx.x * blockDim.x + threadIdx.x;
-  bool nonfinite = false;
-  if (r < a.row1) {
-    const GS* gin = reinterpret_cast<const GS*>(a.gin);
-    const GS xi = gin[r];
-    const GS pref = MODEL == MD_CC ? reinterpret_cast<const GS*>(a.rowc)[r] : GS(0);
-    const SS mw = cvt<SS>(a.mw);
-    const GS kscal = cvt<GS>(a.coupling_k);
-    using KT = typename KElem<KS == MS_K_SCALAR ? MS_K_F32 : KS>::T;
-    const KT* Krow = reinterpret_cast<const KT*>(a.K) + (size_t)(r - a.row0) * a.ld;
-    SS acc = SS(0);
-    for (int j = 0; j < a.n; ++j) {
+  using Gm = SeqGeom<SS, SPLIT>;
+  constexpr int TC = Gm::COLS, P = Gm::PITCH, NA = Gm::NACC;
+  extern __shared__ __align__(16) unsigned char seq_smem[];
+  SS* tile = reinterpret_cast<SS*>(seq_smem);  // [2][NA][kSeqRows][P]
+  const int r0 = a.row0 + blockIdx.x * kSeqRows;
+  const int nrows = min(kSeqRows, a.row1 - r0);
+  const int n = a.n;
+  const int ntiles = (n + TC - 1) / TC;
+  const GS* gin = reinterpret_cast<const GS*>(a.gin);
+  const SS mw = cvt<SS>(a.mw);
+  const GS kscal = cvt<GS>(a.coupling_k);
+  using KT = typename KElem<KS == MS_K_SCALAR ? MS_K_F32 : KS>::T;
+  const KT* K = reinterpret_cast<const KT*>(a.K);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  auto compute = [&](int t, int buf) {  // warps 1..7: the terms of tile t
+    const int j0 = t * TC;
+    for (int q = threadIdx.x - 32; q < kSeqRows * TC; q += kSeqThreads - 32) {
+      const int rr = q / TC, jj = q % TC, j = j0 + jj;
+      if (rr >= nrows || j >= n) continue;
+      const int r = r0 + rr;
       GS kg;
       if constexpr (KS == MS_K_SCALAR) kg = kscal;
-      else kg = (GS)k2f(Krow[j]);
-      const GS diff = sub<GS>(__ldg(gin + j), xi);
-      GS g;
-      if (MODEL == MD_LCO) g = mul<GS>(kg, diff);
-      else if (MODEL == MD_KUR) g = mul<GS>(kg, dsin<GS>(diff));
-      else g = mul<GS>(pref, mul<GS>(kg, datan<GS>(diff)));
-      acc = add<SS>(acc, mul<SS>(mw, (SS)g));
+      else kg = (GS)k2f(K[(size_t)(r - a.row0) * a.ld + j]);
+      SS* dst = tile + ((size_t)buf * NA * kSeqRows + rr) * P + jj;
+      if constexpr (SPLIT) {
+        dst[0] = (SS)mul<GS>(kg, gin[2 * j]);
+        dst[kSeqRows * P] = (SS)mul<GS>(kg, gin[2 * j + 1]);
+      } else {
+        const GS xi = gin[r];
+        const GS diff = sub<GS>(gin[j], xi);
+        GS g;
+        if (MODEL == MD_LCO) g = mul<GS>(kg, diff);
+        else if (MODEL == MD_KUR) g = mul<GS>(kg, dsin<GS>(diff));
+        else g = mul<GS>(reinterpret_cast<const GS*>(a.rowc)[r], mul<GS>(kg, datan<GS>(diff)));
+        dst[0] = mul<SS>(mw, (SS)g);
+      }
+    }
+  };
+  SS A = SS(0), Bc = SS(0);
+  if (warp != 0) compute(0, 0);
+  __syncthreads();
+  for (int t = 0; t < ntiles; ++t) {
+    const int buf = t & 1;
+    if (warp == 0) {
+      if (lane < nrows) {
+        const SS* row = tile + ((size_t)buf * NA * kSeqRows + lane) * P;
+        const int cols = min(TC, n - t * TC);
+        for (int jj = 0; jj < cols; ++jj) {
+          A = add<SS>(A, row[jj]);
+          if constexpr (SPLIT) Bc = add<SS>(Bc, row[kSeqRows * P + jj]);
+        }
+      }
+    } else if (t + 1 < ntiles) {
+      compute(t + 1, buf ^ 1);
+    }
+    __syncthreads();
+  }
+  bool nonfinite = false;
+  if (warp == 0 && lane < nrows) {
+    const int r = r0 + lane;
+    SS coup;
+    if constexpr (SPLIT) {
+      const SS si = (SS)gin[2 * r], ci = (SS)gin[2 * r + 1];
+      coup = mul<SS>(mw, sub<SS>(mul<SS>(ci, A), mul<SS>(si, Bc)));
+    } else {
+      coup = A;
     }
     double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
-    const double o = ws_add(a.fvc[r], (double)acc, a.ws32);
+    const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
     out[(int64_t)r * a.d + a.cs] = o;
     nonfinite = !isfinite(o);
   }
-  if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(a.nf_mask, 1 << a.l);
+  if (warp == 0 && __any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
 }
 
 // ------------------------------------------------------------------------------

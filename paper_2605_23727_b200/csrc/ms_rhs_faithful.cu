@@ -1,6 +1,8 @@
-// ms_rhs_faithful.cu — instantiation and launch of k_rhs_faithful (the
-// reference-order coupling sum, systems.cpp:50-57).
+// ms_rhs_faithful.cu — instantiation and launch of k_rhs_seq (the
+// reference-order coupling sum, systems.cpp:50-57; rhs modes faithful and,
+// for the Kuramoto split in sequential order, ordered).
 #include <stdexcept>
+#include <string>
 
 #include "ms_dispatch.h"
 
@@ -8,13 +10,26 @@ namespace msb {
 
 namespace {
 
-constexpr int kFaithThreads = 128;
+template <int MODEL, bool SPLIT, class SS, class GS, int KS>
+void go_split(const RhsLaunch& L, const RhsArgs& a) {
+  auto kern = k_rhs_seq<MODEL, SPLIT, SS, GS, KS>;
+  constexpr size_t smem = SeqGeom<SS, SPLIT>::SMEM;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_seq attribute: ") + cudaGetErrorString(e));
+    attr_done = true;
+  }
+  const int rows = a.row1 - a.row0;
+  const int grid = (rows + kSeqRows - 1) / kSeqRows;
+  cudaError_t e = launch_k(kern, grid, kSeqThreads, smem, L.stream, a);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_seq launch: ") + cudaGetErrorString(e));
+}
 
 template <int MODEL, class SS, class GS, int KS>
 void go(const RhsLaunch& L, const RhsArgs& a) {
-  const int rows = a.row1 - a.row0;
-  const int grid = (rows + kFaithThreads - 1) / kFaithThreads;
-  k_rhs_faithful<MODEL, SS, GS, KS><<<grid, kFaithThreads, 0, L.stream>>>(a);
+  if (MODEL == MD_KUR && L.split) go_split<MODEL, true, SS, GS, KS>(L, a);
+  else go_split<MODEL, false, SS, GS, KS>(L, a);
 }
 
 template <int MODEL, class SS, class GS>

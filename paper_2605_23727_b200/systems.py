@@ -21,7 +21,7 @@ MODEL_IDS = {"lco": _abi.MS_MODEL_LCO, "kuramoto": _abi.MS_MODEL_KURAMOTO, "cc":
              "scalar_exp": _abi.MS_MODEL_SCALAR_EXP, "scalar_zero": _abi.MS_MODEL_SCALAR_ZERO,
              "scalar_nan": _abi.MS_MODEL_SCALAR_NAN}
 K_STORAGE = {"scalar": _abi.MS_K_SCALAR, "f32": _abi.MS_K_F32, "f16": _abi.MS_K_F16, "bf16": _abi.MS_K_BF16}
-RHS_MODES = {"fast": _abi.MS_RHS_FAST, "faithful": _abi.MS_RHS_FAITHFUL}
+RHS_MODES = {"fast": _abi.MS_RHS_FAST, "faithful": _abi.MS_RHS_FAITHFUL, "ordered": _abi.MS_RHS_ORDERED}
 DIMS = {"lco": 2, "kuramoto": 1, "cc": 4, "scalar_exp": 1, "scalar_zero": 1, "scalar_nan": 1}
 
 

@@ -40,9 +40,13 @@ CASES = {
     "c2_rtol1e-6_f32": {"build": lambda: config2_kuramoto(rtol=1e-6), "what": "C2 N=4096 t[0,50] rtol 1e-6 K f32"},
     "c2_rtol1e-6_f16": {"build": lambda: config2_kuramoto(rtol=1e-6, k_storage="f16"),
                         "what": "C2 N=4096 t[0,50] rtol 1e-6 K f16"},
-    "c2_rtol1e-8_f32": {"build": lambda: config2_kuramoto(rtol=1e-8), "what": "C2 N=4096 t[0,50] rtol 1e-8 K f32"},
+    # rtol 1e-8 under binary32 rows is noise-driven: the rounding noise of the
+    # RHS sums (~1e-7 relative) exceeds the tolerance, so the step sequence
+    # follows the summation order's noise (tests/test_gpu_golden_solves.py)
+    "c2_rtol1e-8_f32": {"build": lambda: config2_kuramoto(rtol=1e-8), "what": "C2 N=4096 t[0,50] rtol 1e-8 K f32",
+                        "noise": True},
     "c2_rtol1e-8_f16": {"build": lambda: config2_kuramoto(rtol=1e-8, k_storage="f16"),
-                        "what": "C2 N=4096 t[0,50] rtol 1e-8 K f16"},
+                        "what": "C2 N=4096 t[0,50] rtol 1e-8 K f16", "noise": True},
     "c3_full": {"build": _c3_full, "what": "C3 CC N=2048 t[0,240] rtol 1e-6 K f32", "log": False},
     "c4_f32": {"build": lambda: config4_kuramoto(), "what": "C4 N=32768 t[0,20] rtol 1e-6 SSS rows, K f32"},
     "c4_f16": {"build": lambda: config4_kuramoto(k_storage="f16"),

@@ -13,6 +13,16 @@ DP5(4) run (rel = abs = 1e-9) must be no larger than the oracle's
 
 fp16 K (the tolerance the north star asks to state): the oracle rounds K to
 f16 exactly as the device stores it, so the device is held to the same gate.
+
+Noise-driven cases (C2 at rtol 1e-8 with binary32 rows): the binary32
+rounding noise of the coupling sums (~1e-7 relative) is larger than the
+tolerance, so the controller's accept/reject sequence follows that noise and
+its statistics depend on the SUMMATION ORDER (the oracle sums each row
+sequentially, the fast sweeps in a blocked warp tree whose error is smaller:
+fewer rejections). There the counts gate runs the device in the ordered mode
+(MS_RHS_ORDERED: the same split, summed in ascending j like the oracle), and
+the fast mode is held to accuracy: its global error against the tight
+binary64 DP5(4) run no larger than the oracle's (x1.5 + 1e-7).
 """
 from types import SimpleNamespace
 
@@ -47,14 +57,36 @@ def test_whole_solve_vs_oracle_fixture(gpu, name):
     w = case["build"]()
     d = _fixture(name)
     assert G.input_hash(w) == d["meta"]["inputs"], "fixture made from other inputs: regenerate it"
-    dev = DeviceSystem(w.spec)
-    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg, log_capacity=1)
     o = _as_result(d)
     assert o.status == S.SolveStatus.Completed
+    if case.get("noise"):
+        w.spec.rhs_mode = "ordered"  # the oracle's summation order
+    dev = DeviceSystem(w.spec)
+    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg, log_capacity=1)
     assert r.t_reached == o.t_reached
     # the evaluation budget of the reference loop (solver.cpp:255-306)
     assert r.flops.rhs_evals == 3 + 3 * r.n_accepted + 4 * r.n_failed
     gate(r, o, w.cfg, dev, w)
+    dev.close()
+
+
+@pytest.mark.parametrize("name", [k for k in SINGLE if G.CASES[k].get("noise")])
+def test_noise_driven_fast_mode_accuracy(gpu, name):
+    """The fast sweeps in a noise-driven configuration: the global error
+    against the tight binary64 DP5(4) run is no larger than the oracle's
+    (the counts are reported, not gated: they follow the summation noise)."""
+    w = G.CASES[name]["build"]()
+    d = _fixture(name)
+    dev = DeviceSystem(w.spec)
+    r = S.solve(dev, w.x0, w.t0, w.tf, w.policy, w.cfg, log_capacity=1)
+    ref = S.dp54_reference(dev, w.x0, w.t0, w.tf, S.SolverConfig(time_limits_enabled=False), log_capacity=1)
+    assert r.status == ref.status == S.SolveStatus.Completed
+    floor = w.cfg.abs_tol / w.cfg.rel_tol
+    wrel = lambda a, b: float(np.max(np.abs(a - b) / np.maximum(np.abs(b), floor)))  # noqa: E731
+    e_dev, e_orc = wrel(r.final_state, ref.final_state), wrel(d["final_state"], ref.final_state)
+    print(f"{name} fast mode: counts {r.n_accepted}/{r.n_failed} (oracle {int(d['n_accepted'])}/"
+          f"{int(d['n_failed'])}); global error vs DP5(4) device {e_dev:.3e}, oracle {e_orc:.3e}")
+    assert e_dev <= 1.5 * e_orc + 1e-7
     dev.close()
 
 

@@ -243,3 +243,60 @@ def test_small_split_sweep_bitwise_equals_register_sweep(gpu, k_storage, n, sp, 
     monkeypatch.setenv("MS_SWEEP", "small")
     b = dev.eval_rhs(0.0, x, sp)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("sweep", ["tma", "ldg"])
+@pytest.mark.parametrize("case", ["tiny_k", "tiny_theta", "normal"])
+@pytest.mark.parametrize("ks", ["f32", "bf16"])
+def test_packed_ftz_products_equal_scalar_products(gpu, monkeypatch, sweep, case, ks):
+    """The split sweeps' packed FMUL2.FTZ path (ms_common.cuh mac2) against
+    the scalar products (MS_SWEEP_PK=off), bit for bit, including inputs where
+    a flushing multiply WOULD differ: K entries that are binary32-subnormal
+    (the system is flagged at creation, ms_system::k_tiny) and column values
+    sin(theta) ~ 1e-30 whose products with K ~ 1e-10 are subnormal (the prep
+    flags them, Ctl::pk_off). Rows with omega = 0 expose the subnormal sums in
+    the output."""
+    from paper_2605_23727_b200.precision import SSS
+    n = 96
+    om = rng_uniform(5, 0, n, -1.0, 1.0)
+    om[:8] = 0.0
+    theta = rng_uniform(5, 1, n, 0.0, TWO_PI)
+    K = rng_uniform(5, 2, n * n, 0.0, 2.0).reshape(n, n)
+    if case == "tiny_k":
+        K[:8] = 1e-39 * (1.0 + rng_uniform(5, 3, 8 * n, 0.0, 1.0).reshape(8, n))
+    elif case == "tiny_theta":
+        K[:8] = 1e-10
+        theta = 1e-30 * (1.0 + np.arange(n) / n)
+    spec = SystemSpec("kuramoto", n, k_storage=ks, rhs_mode="fast", omega=om, K=K)
+    dev = DeviceSystem(spec)
+    monkeypatch.setenv("MS_SWEEP", sweep)
+    packed = dev.eval_rhs(0.0, theta, SSS)
+    monkeypatch.setenv("MS_SWEEP_PK", "off")
+    scalar = dev.eval_rhs(0.0, theta, SSS)
+    assert np.array_equal(packed, scalar)
+    if case != "normal":
+        assert np.any(packed[:8] != 0.0)  # the subnormal sums reached the output
+    orc = O.OracleSystem(spec)
+    ref = orc.eval_rhs(0.0, theta, SSS)
+    gsum = np.abs(orc.get_k()).sum(axis=1)
+    assert np.all(np.abs(packed - ref) <= reorder_tol(SSS, n, ref, gsum) * 4 + 1e-44)
+
+
+@pytest.mark.parametrize("n", [1, 31, 300, 4097])
+@pytest.mark.parametrize("sp", ALL_ROWS, ids=str)
+@pytest.mark.parametrize("ks", ["f32", "f16"])
+def test_kuramoto_ordered_mode_is_the_oracle_split(gpu, n, sp, ks):
+    """MS_RHS_ORDERED: the split Kuramoto summed in ascending j (k_rhs_seq) is
+    the oracle's split form: equal up to the libm ulp of sin/cos (device:
+    binary64 sincos rounded once; oracle: glibc). One differing s_j or c_j
+    moves every row's binary64 sum by ~K ulp(s_j); binary32 sums absorb it,
+    so there nearly every row is bit-identical."""
+    spec = kur_spec(n, k_storage=ks, mode="ordered")
+    dev, orc = pair(spec)
+    x = rng_uniform(3, 1, n, 0.0, TWO_PI)
+    a, b = dev.eval_rhs(0.0, x, sp), orc.eval_rhs(0.0, x, sp)
+    gsum = np.abs(orc.get_k()).sum(axis=1)
+    tol = 8 * eps(sp.g_prec) * gsum / max(n, 1) * 2 + 4 * eps(sp.sum_prec) * np.abs(b) + 1e-300
+    assert np.all(np.abs(a - b) <= tol), float(np.max(np.abs(a - b) / tol))
+    if sp.sum_prec == B32:
+        assert np.mean(a == b) >= 0.9

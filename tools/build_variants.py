@@ -130,6 +130,12 @@ VARIANTS = {
     "pk_c8r4_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_KB_K16": 32768, "MS_TMA_STAGES": 6}),
     "pk_sss_c4r4": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 4, "MS_TMA_RPW_SSS": 4}),
     "pk_sss_c4r2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 4, "MS_TMA_RPW_SSS": 2}),
+    "pf_t384": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_THREADS": 384}),
+    "pf_t256": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_THREADS": 256}),
+    "pf_r4": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_R": 4}),
+    "pf_r6_t384": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_R": 6, "MS_FAST_THREADS": 384}),
+    "t384": ("ms_rhs_fast.cu", {"MS_FAST_THREADS": 384}),
+    "r12_t384": ("ms_rhs_fast.cu", {"MS_FAST_R": 12, "MS_FAST_THREADS": 384}),
 }
 
 
