@@ -106,10 +106,11 @@ def bytes_per_eval(n, rows, ks_bytes):
     return rows * n * ks_bytes + n * 2 * 4 + 2 * n * 8 + n * 8
 
 
-TRAFFIC_CSV = "profiles/r2_c4_sweeps_raw.csv"  # ncu --set full of one host-loop C4 attempt (tools/gpu_ncu_c4.sh)
+# ncu --set full of the K sweeps of one host-loop C4 attempt (tools/gpu_ncu_c4.sh <kdtype>)
+TRAFFIC_CSV = "profiles/r2_c4_sweeps_{ks}_raw.csv"
 
 
-def ncu_traffic(kernel_prefix, path=TRAFFIC_CSV):
+def ncu_traffic(kernel_prefix, path):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the first
     launch whose name starts with `kernel_prefix` in the committed
     `ncu --set full` capture, or None."""
@@ -142,8 +143,9 @@ def sweep_kernel(kdtype, whole):
         ks = {"f32": 1, "f16": 2, "bf16": 3}[kdtype]
         name = f"void k_rhs_fast<1, 1, float, float, {ks}>"
         label = f"k_rhs_fast<Kuramoto split, f32 sum, f32 G, K {kdtype}> (register-fed K sweep)"
-    tr = ncu_traffic(name) if whole else None
-    return label, tr, (f"{TRAFFIC_CSV} ({name}, ncu --set full, one launch)" if tr else None)
+    path = TRAFFIC_CSV.format(ks=kdtype)
+    tr = ncu_traffic(name, path) if whole else None
+    return label, tr, (f"{path} ({name}, ncu --set full, one launch)" if tr else None)
 
 
 def mapped_repo_libs():

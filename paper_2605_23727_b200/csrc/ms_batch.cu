@@ -69,6 +69,7 @@ struct BFinArgs {
   int bslot_[kMaxStages];
   int use_p;  // the last prep wrote P = b~1 k1 + b~2 k2 + b~3 k3 into scr1
   int ctl_smem;  // controller on a shared-memory copy of Ctl[b] (MS_CTL_SMEM)
+  int err_epi;   // the last contraction's epilogue formed the error (d.errb / d.nfe): read and clear it
 };
 
 // x_tilde, weighted max-norm and the controller of one trajectory per CTA;
@@ -108,7 +109,16 @@ __global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinAr
   const bool stage_nf = c->nf_mask != 0;
   double m = 0.0;
   bool nf = false;
-  if (!dead && !stage_nf) {
+  if (f.err_epi) {
+    if (threadIdx.x == 0) {
+      if (!dead && !stage_nf) {
+        m = __longlong_as_double((long long)d.errb[b]);
+        nf = d.nfe[b] != 0;
+      }
+      d.errb[b] = 0ull;
+      d.nfe[b] = 0;
+    }
+  } else if (!dead && !stage_nf) {
     const int ix = c->ix;
     const int64_t o = (int64_t)b * d.n;
     const double* __restrict__ x = d.xb[ix] + o;
@@ -353,6 +363,15 @@ bool bfin_p_enabled() {
   return !(v && std::strcmp(v, "off") == 0);
 }
 
+// MS_BFIN_EPI=on: the last contraction's epilogue forms the error (read per
+// launch; graphs capture it once). Off by default: measured +35 us in that
+// contraction's epilogue (four more latency-bound loads per element on 8 warps
+// per SM) against -8 us in the finalize (profiles/r2_c5_epi_ab.txt)
+bool bfin_epi_enabled() {
+  const char* v = std::getenv("MS_BFIN_EPI");
+  return v && std::strcmp(v, "on") == 0;
+}
+
 template <class FS>
 void launch_bprep(ms_batch* m, cudaStream_t st, const BPrepArgs& p, bool gs32) {
   dim3 grid((m->d.n + 255) / 256, m->B);
@@ -397,7 +416,7 @@ void launch_brhs_cc(ms_batch* m, cudaStream_t st, const BRhsArgs& a) {
 }
 
 void beval(ms_batch* m, cudaStream_t st, const BEval& e, const ms_stage_prec& sp, cudaEvent_t mid0 = nullptr,
-           cudaEvent_t mid1 = nullptr) {
+           cudaEvent_t mid1 = nullptr, bool fin = false) {
   const bool fs32 = is32(sp.f_prec), ss32 = is32(sp.sum_prec), gs32 = is32(sp.g_prec);
   const bool use_tc = m->tc && is_sss(sp);
   BPrepArgs p{};
@@ -438,6 +457,11 @@ void beval(ms_batch* m, cudaStream_t st, const BEval& e, const ms_stage_prec& sp
   a.out_slot = e.out_slot;
   a.ws32 = p.ws32;
   a.fs32 = p.fs32;
+  if (fin) {
+    if (!(use_tc && p.write_p)) throw InvalidArg("batch: the folded error estimate needs the tensor-core path and P");
+    a.fin = 1;
+    a.bt_last = kBT.bt[3];
+  }
   if (mid0) BCK(cudaEventRecord(mid0, st));
   if (use_tc) {
     launch_tc_gemm(m->gemm, a, st);
@@ -498,8 +522,11 @@ void battempt(ms_batch* m, cudaStream_t st, const BPlan& P, bool has_handle, cud
     e.out_slot = SLOT_K1;
     beval(m, st, e, P.k1_row);
   }
-  for (int l = 1; l < 4; ++l) beval(m, st, bstage(l), P.rows[l - 1]);
+  // the error estimate in the last contraction's epilogue (MS_BFIN_EPI=off: in the finalize)
+  const bool epi = MS_TC_FIN && bfin_epi_enabled() && m->tc && is_sss(P.rows[2]) && bfin_p_enabled();
+  for (int l = 1; l < 4; ++l) beval(m, st, bstage(l), P.rows[l - 1], nullptr, nullptr, epi && l == 3);
   BFinArgs f{};
+  f.err_epi = epi ? 1 : 0;
   f.d = m->d;
   f.S = 4;
   f.k1_elided = P.k1_elided;
@@ -606,7 +633,8 @@ int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t
     const size_t vec = al(sizeof(double) * bn);
     size_t total = vec /*omega*/ + 2 * vec + (kMaxStages + 1) * vec + 3 * vec /*xn, scr0, scr1*/ +
                    2 * vec /*sc*/ + al(sizeof(uint16_t) * 4 * (size_t)batch * ld) /*op*/ + vec /*fvc*/ + 2 * vec /*rec*/ +
-                   al(sizeof(Ctl) * batch) + al(sizeof(int));
+                   al(sizeof(Ctl) * batch) + al(sizeof(int)) + al(sizeof(unsigned long long) * batch) +
+                   al(sizeof(int) * batch);
     char* base = nullptr;
     BCK(cudaMalloc(&base, total));
     BCK(cudaMemset(base, 0, total));
@@ -637,6 +665,8 @@ int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t
     d.ctl = reinterpret_cast<Ctl*>(take(sizeof(Ctl) * batch));
     d.flag = reinterpret_cast<int*>(take(2 * sizeof(int)));
     d.ticket = reinterpret_cast<unsigned*>(d.flag + 1);
+    d.errb = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * batch));
+    d.nfe = reinterpret_cast<int*>(take(sizeof(int) * batch));
     d.mw = 1.0 / n;
     BCK(cudaMemcpy(m->omega, omega, sizeof(double) * bn, cudaMemcpyHostToDevice));
     {  // the records' F: RN32(omega), F of a binary32 row (systems.cpp:136-139; the

@@ -31,6 +31,12 @@ struct BatchDev {
   void* rec;                      // tensor-core epilogue records TcRec [B][n]; F written once at creation
   Ctl* ctl;                       // [B]
   int* flag;                      // [1] any trajectory still running (host loop / conditional)
+  // error estimate folded into the last stage's contraction epilogue (MS_BFIN_EPI):
+  // per trajectory the bit pattern of the weighted max-norm so far (non-negative
+  // doubles order like their bits) and a non-finite flag; kb_finalize reads and
+  // clears them
+  unsigned long long* errb;       // [B]
+  int* nfe;                       // [B]
   unsigned* ticket;               // [1] finalize last-block counter (reset by the last block)
   double mw;                      // 1/N
 };
@@ -312,6 +318,11 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
 struct BRhsArgs {
   BatchDev d;
   int S, l, gate, out_slot, ws32, fs32;
+  // last stage with MS_BFIN_EPI: the epilogue also forms x_tilde = x + h (P + b~4 k4)
+  // (P = b~1 k1 + b~2 k2 + b~3 k3 from the last prep) and the weighted error of
+  // solver.cpp:399-411 per element, reduced into d.errb / d.nfe
+  int fin;
+  double bt_last;
 };
 
 // coupling epilogue of one (row i, trajectory b): k = (double)(RN_WS(omega) +

@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -36,6 +37,17 @@
 
 namespace msb {
 
+// the error estimate folded into the last contraction's epilogue (MS_BFIN_EPI):
+// compiled out unless MS_TC_FIN=1 (measured slower, ms_batch.cu bfin_epi_enabled)
+#ifndef MS_TC_FIN
+#define MS_TC_FIN 0
+#endif
+#ifndef MS_TC_REC128
+#define MS_TC_REC128 0   // 128-bit loads of the epilogue records: measured 57 vs 39 us per contraction
+#endif
+#ifndef MS_TC_STCG
+#define MS_TC_STCG 0     // st.global.cg for the k stores (else a generic store)
+#endif
 #ifndef MS_TC_STAGES
 #define MS_TC_STAGES 2   // 2 x 48 KB: two CTAs per SM, one's epilogue overlaps the other's MMA
 #endif
@@ -120,8 +132,31 @@ __device__ __forceinline__ void tc_ld32(uint32_t addr, uint32_t (&r)[32]) {
 // of the next 8 trajectories are issued before the current 8 are finished.
 // The first 8 trajectories' records are loaded while the MMAs still run (the
 // epilogue warps are idle until tmem_full), then the accumulators are awaited.
+// per-trajectory inputs of the folded error estimate (TcArgs::a.fin)
+struct TcFin {
+  const double* x;   // x_n
+  const double* xs;  // x_store (finite check)
+  const double* xn;  // x_next (x_store unless binary32 storage)
+  const double* p;   // P = b~1 k1 + b~2 k2 + b~3 k3
+  double h, fw;      // h of the attempt, weight floor ab / rel
+};
+
+__device__ __forceinline__ void tc_fin_setup(const TcArgs& t, int b, TcFin& f) {
+  const BatchDev& d = t.a.d;
+  const Ctl* c = d.ctl + b;
+  const int64_t o = (int64_t)b * d.n;
+  const int ix = c->ix;
+  f.x = d.xb[ix] + o;
+  f.xs = d.xb[ix ^ 1] + o;
+  f.xn = c->store32 ? d.xn + o : f.xs;
+  f.p = d.scr1 + o;
+  f.h = c->h_att;
+  f.fw = __ddiv_rn(c->abs_tol, c->rel_tol);
+}
+
 __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr, int i, int tb0, int c_beg, int c_end,
-                                            const int* skip, double* const* outp, uint64_t* tmem_full) {
+                                            const int* skip, double* const* outp, uint64_t* tmem_full,
+                                            const TcFin* fin = nullptr) {
   const BatchDev& d = t.a.d;
   const float mw = (float)d.mw;
   const float2* sc2 = reinterpret_cast<const float2*>(d.sc);
@@ -136,7 +171,16 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
 #if MS_TC_PACKED == 1
         v[q] = reinterpret_cast<const TcRec*>(d.sc)[e];
 #elif MS_TC_PACKED == 2
+#if MS_TC_REC128
+        // one 128-bit load per record (the struct copy compiles to two LDG.64)
+        const double2 raw = __ldg(reinterpret_cast<const double2*>(d.rec) + e);
+        const unsigned long long sc_bits = (unsigned long long)__double_as_longlong(raw.x);
+        v[q].s = __uint_as_float((unsigned)(sc_bits & 0xffffffffull));
+        v[q].c = __uint_as_float((unsigned)(sc_bits >> 32));
+        v[q].f = raw.y;
+#else
         v[q] = reinterpret_cast<const TcRec*>(d.rec)[e];
+#endif
 #else
         const float2 p = sc2[e];
         v[q].s = p.x;
@@ -153,6 +197,9 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
   for (int c0 = c_beg; c0 < c_end; c0 += 32) {
     uint32_t r[32];
     tc_ld32(lane_addr + (uint32_t)c0, r);
+#if MS_TC_FIN
+    double rk[8];
+#endif
     TcRec nxt[8];
     if (c0 + 32 < c_end) load(c0 + 32, nxt);
     if (row_ok) {
@@ -164,10 +211,47 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
         const float Bv = __fadd_rn(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
         const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(cur[q].c, A), __fmul_rn(cur[q].s, Bv)));
         const double o = ws_add(cur[q].f, (double)coup, t.a.ws32);
+#if MS_TC_STCG
+        __stcg(outp[tq] + i, o);  // a global store (the pointer comes through shared memory)
+#else
         outp[tq][i] = o;
+#endif
         if (!isfinite(o)) atomicOr(&d.ctl[tb0 + tq].nf_mask, 1 << t.a.l);
+#if MS_TC_FIN
+        if (fin) rk[q] = o;
+#endif
       }
     }
+#if MS_TC_FIN
+    if (fin) {
+      // the finalize's element loop for these 8 trajectories (kb_finalize order
+      // and arithmetic; max and or are order-free, so the result is bitwise)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int tq = (c0 >> 2) + q;
+        if (skip[tq]) continue;  // uniform over the warp
+        double m = 0.0;
+        bool nf = false;
+        if (row_ok) {
+          const TcFin& fr = fin[tq];
+          const double comb = __dadd_rn(fr.p[i], __dmul_rn(t.a.bt_last, rk[q]));
+          const double xi = fr.x[i];
+          const double xt = __dadd_rn(xi, __dmul_rn(fr.h, comb));
+          const double xn = fr.xn[i];
+          nf = !isfinite(xn) || !isfinite(xt) || !isfinite(fr.xs[i]);
+          const double w = fmax(fmax(fabs(xi), fabs(xn)), fr.fw);
+          m = fmax(0.0, __ddiv_rn(fabs(__dsub_rn(xn, xt)), w));
+        }
+#pragma unroll
+        for (int sft = 16; sft >= 1; sft >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, sft));
+        nf = __any_sync(0xffffffffu, nf);
+        if ((threadIdx.x & 31) == 0) {
+          atomicMax(d.errb + tb0 + tq, (unsigned long long)__double_as_longlong(m));
+          if (nf) atomicOr(d.nfe + tb0 + tq, 1);
+        }
+      }
+    }
+#endif
 #pragma unroll
     for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
   }
@@ -187,6 +271,11 @@ __global__ void __launch_bounds__(kTcThreads, MS_TC_MINB)
 
   __shared__ int tc_skip[kTcBN / 4];
   __shared__ double* tc_out[kTcBN / 4];
+#if MS_TC_FIN
+  __shared__ TcFin tc_fin[kTcBN / 4];
+#else
+  constexpr TcFin* tc_fin = nullptr;
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * kTcBM, n0 = blockIdx.y * kTcBN;
   const int nkb = (t.n + kTcBK - 1) / kTcBK;
@@ -275,12 +364,16 @@ __global__ void __launch_bounds__(kTcThreads, MS_TC_MINB)
       }
       tc_skip[et] = skip;
       tc_out[et] = outp;
+#if MS_TC_FIN
+      if (t.a.fin && !skip) tc_fin_setup(t, b, tc_fin[et]);
+#endif
     }
     asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpiWarps) : "memory");
     const int i = m0 + q4 * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
     constexpr int kCols = kTcBN * 4 / kTcEpiWarps;  // columns per epilogue warp
-    tc_epilogue(t, lane_addr, i, tb0, half * kCols, (half + 1) * kCols, tc_skip, tc_out, tmem_full);
+    tc_epilogue(t, lane_addr, i, tb0, half * kCols, (half + 1) * kCols, tc_skip, tc_out, tmem_full,
+                t.a.fin ? tc_fin : nullptr);
   }
   tc_fence_before();
   __syncthreads();
@@ -360,6 +453,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
 
   __shared__ int tc_skip[kT2BN / 4];
   __shared__ double* tc_out[kT2BN / 4];
+#if MS_TC_FIN
+  __shared__ TcFin tc_fin[kT2BN / 4];
+#else
+  constexpr TcFin* tc_fin = nullptr;
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int m0 = (blockIdx.x >> 1) * (2 * kT2BM) + (int)rank * kT2BM;  // this CTA's rows
@@ -456,13 +554,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
       }
       tc_skip[et] = skip;
       tc_out[et] = outp;
+#if MS_TC_FIN
+      if (t.a.fin && !skip) tc_fin_setup(t, b, tc_fin[et]);
+#endif
     }
     asm volatile("bar.sync 1, %0;" ::"r"(32 * kT2EpiWarps) : "memory");
     const int i = m0 + q4 * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
     constexpr int kCols = kT2BN / (kT2EpiWarps / 4);  // columns per epilogue warp
 #ifndef MS_T2_NOEPI
-    tc_epilogue(t, lane_addr, i, tb0, part * kCols, (part + 1) * kCols, tc_skip, tc_out, tmem_full);
+    tc_epilogue(t, lane_addr, i, tb0, part * kCols, (part + 1) * kCols, tc_skip, tc_out, tmem_full,
+                t.a.fin ? tc_fin : nullptr);
 #else
     tc_wait(tmem_full, 0);
     tc_fence_after();
@@ -518,6 +620,7 @@ inline void tc_gemm_setup(TcGemm& g, const BatchDev& d, int sms) {
   if (g.pair) {
     g.grid_m = 2 * ((d.n + 2 * kT2BM - 1) / (2 * kT2BM));
     g.grid_n = (4 * d.B + kT2BN - 1) / kT2BN;
+    if (const char* gn = std::getenv("MS_T2_GRIDN")) g.grid_n = std::max(1, std::min(g.grid_n, std::atoi(gn)));  // tuning only
     cudaError_t e = cudaFuncSetAttribute(k_tc_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT2Smem);
     if (e != cudaSuccess) throw std::runtime_error(std::string("tc gemm2 smem attribute: ") + cudaGetErrorString(e));
   } else {

@@ -130,6 +130,11 @@ VARIANTS = {
     "pk_c8r4_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_KB_K16": 32768, "MS_TMA_STAGES": 6}),
     "pk_sss_c4r4": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 4, "MS_TMA_RPW_SSS": 4}),
     "pk_sss_c4r2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 4, "MS_TMA_RPW_SSS": 2}),
+    "tcv_base": ("ms_batch.cu", {}),
+    "tcv_rec64": ("ms_batch.cu", {"MS_TC_REC128": 0}),
+    "tcv_stcg": ("ms_batch.cu", {"MS_TC_STCG": 1}),
+    "tcv_fin": ("ms_batch.cu", {"MS_TC_FIN": 1}),
+    "tcv_noepi": ("ms_batch.cu", {"MS_T2_NOEPI": 1}),
     "pf_t384": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_THREADS": 384}),
     "pf_t256": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_THREADS": 256}),
     "pf_r4": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_R": 4}),
