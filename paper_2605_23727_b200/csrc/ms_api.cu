@@ -244,12 +244,16 @@ __global__ void k_estimate_error(int64_t n, const double* a, const double* b, co
   msb::count_launch();
   // estimate_error, solver.cpp:399-411 (max is order-independent)
   __shared__ double red[32];
+  // the max without a division per element (QuotMax, bitwise the per-element
+  // fmax of the rounded quotients: also the unit-level test of the device
+  // finalizes' reduction, tests/test_gpu_solver.py)
   const double floor_w = __ddiv_rn(ab, rel);
-  double m = 0.0;
+  QuotMax qm;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const double w = fmax(fmax(fabs(a[i]), fabs(b[i])), floor_w);
-    m = fmax(m, __ddiv_rn(fabs(__dsub_rn(b[i], c[i])), w));
+    qm.add(fabs(__dsub_rn(b[i], c[i])), w);
   }
+  double m = qm.value();
   for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();

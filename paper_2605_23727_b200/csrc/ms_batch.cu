@@ -70,6 +70,7 @@ struct BFinArgs {
   int use_p;  // the last prep wrote P = b~1 k1 + b~2 k2 + b~3 k3 into scr1
   int ctl_smem;  // controller on a shared-memory copy of Ctl[b] (MS_CTL_SMEM)
   int err_epi;   // the last contraction's epilogue formed the error (d.errb / d.nfe): read and clear it
+  int quot;      // the error norm's max without a division per element (QuotMax; MS_BFIN_QUOT=off: per element)
 };
 
 // x_tilde, weighted max-norm and the controller of one trajectory per CTA;
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinAr
     const double h = c->h_att;
     const double floor_w = __ddiv_rn(c->abs_tol, c->rel_tol);
     const double* __restrict__ pp = d.scr1 + o;
+    QuotMax qm;
 #if MS_BFIN_UNROLL > 0
 #pragma unroll kBFinUnroll
 #endif
@@ -151,8 +153,10 @@ __global__ void __launch_bounds__(kBFinThreads, MS_BFIN_MINB) kb_finalize(BFinAr
       const double xn = xnx[i];
       nf |= !isfinite(xn) || !isfinite(xt) || !isfinite(xst[i]);
       const double w = fmax(fmax(fabs(xi), fabs(xn)), floor_w);
-      m = fmax(m, __ddiv_rn(fabs(__dsub_rn(xn, xt)), w));
+      if (f.quot) qm.add(fabs(__dsub_rn(xn, xt)), w);
+      else m = fmax(m, __ddiv_rn(fabs(__dsub_rn(xn, xt)), w));
     }
+    if (f.quot) m = qm.value();
   }
   __shared__ double red[kBFinThreads / 32];
   __shared__ int rnf[kBFinThreads / 32];
@@ -538,6 +542,10 @@ void battempt(ms_batch* m, cudaStream_t st, const BPlan& P, bool has_handle, cud
   if (f.nbt != 4) throw InvalidArg("batch: finalize expects the four BS3(2) error weights");
   f.use_p = bfin_p_enabled() ? 1 : 0;
   f.ctl_smem = ctl_smem_enabled() ? 1 : 0;
+  {
+    const char* v = std::getenv("MS_BFIN_QUOT");  // read per launch (graphs capture it once)
+    f.quot = (v && std::strcmp(v, "off") == 0) ? 0 : 1;
+  }
   BCK(launch_k(kb_finalize, m->B, kBFinThreads, 0, st, f, has_handle ? 1 : 0, h));
 }
 

@@ -1492,6 +1492,35 @@ constexpr int64_t kFinSmallMax = MS_FIN_SMALL_MAX;  // measured: C1 (2048) -3 %,
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000ll); }
 
+// Running max of RN(a_i / w_i) (the weighted error norm, solver.cpp:403-408)
+// without a division per element: rounding is monotone, so the max of the
+// rounded quotients is RN of the largest exact quotient. Candidates are
+// compared exactly, a1 w2 vs a2 w1 as (RN product, FMA remainder) pairs, and
+// one division per thread remains (value()). Elements whose quotient is not a
+// regular one (w == 0, a not finite, factors outside [1e-140, 1e140]) take
+// the division directly, combined with fmax as before (NaN
+// ignored) — the result is bitwise the per-element fmax(m, RN(a / w)).
+struct QuotMax {
+  double ab = 0.0, wb = 1.0;  // best regular candidate (quotient 0 to start)
+  double ms = 0.0;            // fmax over the irregular elements
+  __device__ __forceinline__ void add(double a, double w) {
+    // both factors in [1e-140, 1e140]: every product is a normal double whose
+    // FMA remainder is exact
+    if (a >= 1e-140 && a <= 1e140 && w >= 1e-140 && w <= 1e140) {
+      const double p = __dmul_rn(a, wb), q = __dmul_rn(ab, w);
+      bool gt = p > q;
+      if (p == q) gt = __fma_rn(a, wb, -p) > __fma_rn(ab, w, -q);
+      if (gt) {
+        ab = a;
+        wb = w;
+      }
+    } else if (!(a == 0.0 && w > 0.0)) {  // a zero quotient changes nothing
+      ms = fmax(ms, __ddiv_rn(a, w));
+    }
+  }
+  __device__ __forceinline__ double value() const { return fmax(ms, __ddiv_rn(ab, wb)); }
+};
+
 // The controller of one attempt (rk_step tail, solver.cpp:158-162, 201-214, and
 // the solve_core bookkeeping, :298-342), run by one thread once the weighted
 // max-norm err_max of the attempt is known. Returns whether the loop goes on.

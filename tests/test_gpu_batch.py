@@ -238,3 +238,29 @@ def test_batch_error_in_epilogue_is_bitwise(gpu, monkeypatch, pol):
     assert np.array_equal(a.rhs_evals, b.rhs_evals)
     assert np.array_equal(a.final_state, b.final_state)
     assert np.array_equal(a.t_reached, b.t_reached)
+
+
+@pytest.mark.parametrize("tc", [True, False])
+@pytest.mark.parametrize("pol", ["SSS_D", "Single", "Mixed2"])
+def test_batch_finalize_max_without_division_is_bitwise(gpu, monkeypatch, tc, pol):
+    """kb_finalize's weighted max-norm (solver.cpp:403-408) as RN of the largest
+    exact quotient (ms_kernels.cuh QuotMax: candidates compared as product +
+    FMA remainder, one division per thread) against a division per element
+    (MS_BFIN_QUOT=off): identical ensembles, bit for bit."""
+    from paper_2605_23727_b200.configs import SSS_D
+    from paper_2605_23727_b200.precision import PolicyVariant, policy_for
+    from paper_2605_23727_b200.solver import SolverConfig
+    B, n = 48, 320
+    spec, omega, x0 = _ensemble(B, n, "bf16", seed=15)
+    policy = SSS_D if pol == "SSS_D" else policy_for(getattr(PolicyVariant, pol))
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    dev = DeviceSystem(spec)
+    runs = []
+    for mode in ("on", "off"):
+        monkeypatch.setenv("MS_BFIN_QUOT", mode)
+        runs.append(DeviceBatch(dev, omega, tensor_cores=tc).solve(x0, 0.0, 3.0, policy, cfg))
+    a, b = runs
+    assert list(a.status) == list(b.status)
+    assert np.array_equal(a.n_accepted, b.n_accepted) and np.array_equal(a.n_failed, b.n_failed)
+    assert np.array_equal(a.final_state, b.final_state)
+    assert np.array_equal(a.t_reached, b.t_reached)

@@ -298,5 +298,5 @@ def test_kuramoto_ordered_mode_is_the_oracle_split(gpu, n, sp, ks):
     gsum = np.abs(orc.get_k()).sum(axis=1)
     tol = 8 * eps(sp.g_prec) * gsum / max(n, 1) * 2 + 4 * eps(sp.sum_prec) * np.abs(b) + 1e-300
     assert np.all(np.abs(a - b) <= tol), float(np.max(np.abs(a - b) / tol))
-    if sp.sum_prec == B32:
+    if sp.sum_prec == B32 and sp.f_prec == B32:  # binary32 output absorbs the ulp
         assert np.mean(a == b) >= 0.9

@@ -374,3 +374,39 @@ def test_controller_on_shared_copy_limits_are_bitwise(gpu, monkeypatch):
         assert a.status == b.status != SolveStatus.Completed, kw
         assert (a.n_accepted, a.n_failed, a.t_reached) == (b.n_accepted, b.n_failed, b.t_reached)
         assert np.array_equal(a.final_state, b.final_state)
+
+
+def test_estimate_error_max_without_division_is_exact(gpu):
+    """The device max-norm takes RN of the largest exact quotient instead of a
+    division per element (ms_kernels.cuh QuotMax: candidates compared as
+    product + FMA remainder). Against the oracle's per-element division, bit
+    for bit, on inputs built to defeat it: quotients that tie or differ in the
+    last bit, several magnitudes, zero denominators (ab = 0), tiny and huge
+    values, and non-finite entries."""
+    rng = np.random.default_rng(7)
+    for trial in range(60):
+        n = int(rng.integers(1, 5000))
+        a = rng.uniform(-5, 5, n) * 10.0 ** rng.integers(-3, 4, n)
+        b = a * (1 + rng.uniform(-1e-3, 1e-3, n))
+        q = 10.0 ** rng.uniform(-12, -2)
+        # near-ties: |b - c| / w == q (1 + k ulp) for a few k
+        w = np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-9 / 1e-6)
+        k = rng.integers(-3, 4, n)
+        c = b - w * q * (1 + k * 2.0 ** -52)
+        if trial % 5 == 1:
+            c[rng.integers(0, n)] = b[0] + 1e-200
+        if trial % 5 == 2:
+            a[: n // 2] = 1e-160
+            b[: n // 2] = 1e-160
+            c[: n // 2] = 3e-161
+        if trial % 5 == 3 and n > 2:
+            a[1], b[1], c[1] = 1e200, 1e200 * (1 + 1e-9), 1e200
+        ab = 0.0 if trial % 7 == 0 else 1e-9
+        if trial % 11 == 0:
+            a[0] = b[0] = 0.0
+            c[0] = 1e-30
+        if trial % 13 == 0 and n > 3:
+            c[3] = np.nan
+        for args in ((a, b, c, ab, 1e-6),):
+            d, o = S.estimate_error(*args), O.estimate_error(*args)
+            assert (np.isnan(d) and np.isnan(o)) or d == o, (trial, d, o)

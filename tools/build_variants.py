@@ -130,6 +130,12 @@ VARIANTS = {
     "pk_c8r4_32k_s6": ("ms_rhs_fast.cu", {"MS_TMA_KB_K16": 32768, "MS_TMA_STAGES": 6}),
     "pk_sss_c4r4": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 4, "MS_TMA_RPW_SSS": 4}),
     "pk_sss_c4r2": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 4, "MS_TMA_RPW_SSS": 2}),
+    "f32_nopk": ("ms_rhs_fast.cu", {"MS_SWEEP_PK": 0}),
+    "f32_pk_u2": ("ms_rhs_fast.cu", {"MS_TMA_UNROLL": 2}),
+    "f32_pk_u8": ("ms_rhs_fast.cu", {"MS_TMA_UNROLL": 8}),
+    "f32_pk_c16r1": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 16, "MS_TMA_RPW_SSS": 1}),
+    "f32_pk_c8r4": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 8, "MS_TMA_RPW_SSS": 4}),
+    "f32_pk_s3": ("ms_rhs_fast.cu", {"MS_TMA_STAGES": 3}),
     "tcv_base": ("ms_batch.cu", {}),
     "tcv_rec64": ("ms_batch.cu", {"MS_TC_REC128": 0}),
     "tcv_stcg": ("ms_batch.cu", {"MS_TC_STCG": 1}),

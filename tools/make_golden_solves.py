@@ -50,32 +50,52 @@ def run_single(name, case):
     print(f"{name}: {o.status.name} {o.n_accepted}/{o.n_failed} evals {o.flops.rhs_evals} in {dt:.1f} s", flush=True)
 
 
-def run_batch(name, case):
-    """Every trajectory of the ensemble through the oracle (per-trajectory
-    omega, shared K, the tensor-core operand rounding); counts for all of them,
-    final states for the sampled ones."""
+def _batch_worker(args):
+    """One process, one oracle thread: a contiguous block of trajectories."""
+    name, b0, b1 = args
+    case = CASES[name]
+    O.set_threads(1)
     w = case["build"]()
     orc = O.OracleSystem(w.spec)
     orc.set_op_round(case["op_round"])
+    out = []
+    for b in range(b0, b1):
+        orc.set_omega(w.omega[b])
+        o = O.solve(orc, w.x0[b], w.t0, w.tf, w.policy, w.cfg, cap=1, snapshot_capacity=0)
+        fs = o.final_state if b in case["sample"] else None
+        out.append((b, o.n_accepted, o.n_failed, o.flops.rhs_evals, int(o.status), o.t_reached, fs))
+    return out
+
+
+def run_batch(name, case):
+    """Every trajectory of the ensemble through the oracle (per-trajectory
+    omega, shared K, the tensor-core operand rounding); counts for all of them,
+    final states for the sampled ones. Trajectories are independent solves
+    (the reference's campaign model, harness.cpp:449-456): one single-threaded
+    oracle process per core."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    w = case["build"]()
     B = w.omega.shape[0]
     sample = np.array(case["sample"], dtype=np.int64)
     acc, rej, evals, status, tr = (np.zeros(B, np.int64), np.zeros(B, np.int64), np.zeros(B, np.int64),
                                    np.zeros(B, np.int32), np.zeros(B))
     finals = np.zeros((sample.size, w.x0.shape[1]))
     t = time.perf_counter()
-    for b in range(B):
-        orc.set_omega(w.omega[b])
-        o = O.solve(orc, w.x0[b], w.t0, w.tf, w.policy, w.cfg, cap=1, snapshot_capacity=0)
-        acc[b], rej[b], evals[b], status[b], tr[b] = o.n_accepted, o.n_failed, o.flops.rhs_evals, int(o.status), \
-            o.t_reached
-        hit = np.nonzero(sample == b)[0]
-        if hit.size:
-            finals[hit[0]] = o.final_state
-        if b % 64 == 63:
-            print(f"  {name}: {b + 1}/{B} trajectories, {time.perf_counter() - t:.0f} s", flush=True)
+    nproc = os.cpu_count() or 1
+    blocks = [(name, B * k // (4 * nproc), B * (k + 1) // (4 * nproc)) for k in range(4 * nproc)]
+    done = 0
+    with ProcessPoolExecutor(nproc, mp_context=mp.get_context("spawn")) as ex:
+        for part in ex.map(_batch_worker, blocks):
+            for b, a_, r_, e_, s_, t_, fs in part:
+                acc[b], rej[b], evals[b], status[b], tr[b] = a_, r_, e_, s_, t_
+                if fs is not None:
+                    finals[int(np.nonzero(sample == b)[0][0])] = fs
+            done += len(part)
+            print(f"  {name}: {done}/{B} trajectories, {time.perf_counter() - t:.0f} s", flush=True)
     dt = time.perf_counter() - t
     meta = {"case": name, "what": case["what"], "oracle_src": oracle_source_hash(), "inputs": input_hash(w),
-            "oracle_s": dt, "threads": O.lib().orc_get_threads(), "t0": w.t0, "tf": w.tf}
+            "oracle_s": dt, "threads": nproc, "t0": w.t0, "tf": w.tf}
     np.savez_compressed(OUT / f"{name}.npz", sample=sample, final_states=finals, n_accepted=acc, n_failed=rej,
                         rhs_evals=evals, status=status, t_reached=tr, meta=json.dumps(meta))
     print(f"{name}: {int(acc.sum())}/{int(rej.sum())} over {B} trajectories in {dt:.1f} s", flush=True)
