@@ -496,11 +496,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
         if (kb >= kT2Stages) tc_wait(&empty[st], ((kb / kT2Stages) & 1) ^ 1);
         const uint32_t sa = smem_u32(smem + (size_t)st * kT2StageBytes);
         const uint32_t sb = sa + kT2ABytes;
-        if (rank == 0) mbar_expect_tx(&full[st], 2 * kT2StageBytes);
+#ifndef MS_T2_EXP_NB
+#define MS_T2_EXP_NB kT2NMma  // timing experiments only: operand halves loaded per k-block (results wrong if fewer)
+#endif
+        if (rank == 0) mbar_expect_tx(&full[st], 2 * (kT2ABytes + MS_T2_EXP_NB * (kT2Half * kTcBK * 2)));
         const uint32_t bar = map_to_rank(smem_u32(&full[st]), 0);
         tma2_load(sa, &tmA, bar, kb * kTcBK, m0);
 #pragma unroll
-        for (int hf = 0; hf < kT2NMma; ++hf)
+        for (int hf = 0; hf < MS_T2_EXP_NB; ++hf)
           tma2_load(sb + hf * (kT2Half * kTcBK * 2), &tmB, bar, kb * kTcBK, n0 + hf * 2 * kT2Half + (int)rank * kT2Half);
       }
     }
@@ -516,8 +519,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
         for (int k = 0; k < kTcBK / 16; ++k) {
           const uint64_t adesc = umma_smem_desc(sa + k * 32);
           const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+#ifndef MS_T2_EXP_NMMA
+#define MS_T2_EXP_NMMA kT2NMma  // timing experiments only: MMAs issued per k-step
+#endif
 #pragma unroll
-          for (int hf = 0; hf < kT2NMma; ++hf) {
+          for (int hf = 0; hf < MS_T2_EXP_NMMA; ++hf) {
             const uint64_t bdesc = umma_smem_desc(sb + hf * (kT2Half * kTcBK * 2) + k * 32);
             asm volatile(
                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"

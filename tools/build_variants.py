@@ -136,6 +136,10 @@ VARIANTS = {
     "f32_pk_c16r1": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 16, "MS_TMA_RPW_SSS": 1}),
     "f32_pk_c8r4": ("ms_rhs_fast.cu", {"MS_TMA_CONS_SSS": 8, "MS_TMA_RPW_SSS": 4}),
     "f32_pk_s3": ("ms_rhs_fast.cu", {"MS_TMA_STAGES": 3}),
+    "tcx_halfb": ("ms_batch.cu", {"MS_T2_NOEPI": 1, "MS_T2_EXP_NB": 1}),
+    "tcx_nob": ("ms_batch.cu", {"MS_T2_NOEPI": 1, "MS_T2_EXP_NB": 0}),
+    "tcx_1mma": ("ms_batch.cu", {"MS_T2_NOEPI": 1, "MS_T2_EXP_NMMA": 1}),
+    "tcx_0mma": ("ms_batch.cu", {"MS_T2_NOEPI": 1, "MS_T2_EXP_NMMA": 0}),
     "tcv_base": ("ms_batch.cu", {}),
     "tcv_rec64": ("ms_batch.cu", {"MS_TC_REC128": 0}),
     "tcv_stcg": ("ms_batch.cu", {"MS_TC_STCG": 1}),
