@@ -78,6 +78,12 @@ struct TcArgs {
   BRhsArgs a;
   int n, ncol;  // rows of K, GEMM columns (4B: s_hi, s_lo, c_hi, c_lo per trajectory)
   uint32_t idesc;
+  // MS_TC_PDL=early: release the dependent launch (the next stage's prep / the
+  // finalize) once this CTA's mainloop is done, so its blocks are scheduled while
+  // the epilogue runs (they still wait for this grid in griddepcontrol.wait).
+  // Measured slower (whole C5 solve 292 vs 282 ms: the waiting blocks crowd the
+  // epilogue), so the default releases at exit
+  int pdl_early;
 };
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -193,6 +199,7 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
   load(c_beg, cur);
   tc_wait(tmem_full, 0);
   tc_fence_after();
+  if (t.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #pragma unroll 1
   for (int c0 = c_beg; c0 < c_end; c0 += 32) {
     uint32_t r[32];
@@ -507,6 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
           tma2_load(sb + hf * (kT2Half * kTcBK * 2), &tmB, bar, kb * kTcBK, n0 + hf * 2 * kT2Half + (int)rank * kT2Half);
       }
     }
+    if (t.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {  // MMA issuer: the leader only
       for (int kb = 0; kb < nkb; ++kb) {
@@ -543,6 +551,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
           "h"((uint16_t)3)
           : "memory");
     }
+    if (t.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else {  // epilogue: TMEM lane quarter warp%4, column part (warp-2)/4
     const int q4 = warp & 3;
     const int part = (warp - 2) >> 2;
@@ -654,6 +663,10 @@ inline void launch_tc_gemm(const TcGemm& g, const BRhsArgs& a, cudaStream_t st) 
   t.n = a.d.n;
   t.ncol = 4 * a.d.B;
   dim3 grid(g.grid_m, g.grid_n);
+  {
+    const char* v = std::getenv("MS_TC_PDL");  // read per launch (graphs capture it once)
+    t.pdl_early = (v && std::string(v) == "early") ? 1 : 0;
+  }
   if (g.pair) {
     t.idesc = tc_idesc(a.d.ks, 2 * kT2BM);
     cudaError_t e = launch_k(k_tc_gemm2, grid, kT2Threads, kT2Smem, st, g.tmA, g.tmB2, t);

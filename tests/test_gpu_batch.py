@@ -214,32 +214,6 @@ def test_batch_controller_on_shared_copy_is_bitwise(gpu, monkeypatch, tc):
     assert np.array_equal(a.t_reached, b.t_reached)
 
 
-@pytest.mark.parametrize("pol", ["SSS_D", "Single"])
-def test_batch_error_in_epilogue_is_bitwise(gpu, monkeypatch, pol):
-    """The last stage's contraction epilogue forms x_tilde and the weighted
-    error (MS_BFIN_EPI, ms_gemm_tc.cuh tc_epilogue) instead of the finalize's
-    element loop: the per-trajectory max and the non-finite flag are
-    order-free, so ensembles with and without it agree bit for bit."""
-    from paper_2605_23727_b200.configs import SSS_D
-    from paper_2605_23727_b200.precision import PolicyVariant, policy_for
-    from paper_2605_23727_b200.solver import SolverConfig
-    B, n = 300, 384
-    spec, omega, x0 = _ensemble(B, n, "bf16", seed=14)
-    policy = SSS_D if pol == "SSS_D" else policy_for(PolicyVariant.Single)
-    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
-    dev = DeviceSystem(spec)
-    runs = []
-    for mode in ("on", "off"):
-        monkeypatch.setenv("MS_BFIN_EPI", mode)
-        runs.append(DeviceBatch(dev, omega, tensor_cores=True).solve(x0, 0.0, 3.0, policy, cfg))
-    a, b = runs
-    assert list(a.status) == list(b.status)
-    assert np.array_equal(a.n_accepted, b.n_accepted) and np.array_equal(a.n_failed, b.n_failed)
-    assert np.array_equal(a.rhs_evals, b.rhs_evals)
-    assert np.array_equal(a.final_state, b.final_state)
-    assert np.array_equal(a.t_reached, b.t_reached)
-
-
 @pytest.mark.parametrize("tc", [True, False])
 @pytest.mark.parametrize("pol", ["SSS_D", "Single", "Mixed2"])
 def test_batch_finalize_max_without_division_is_bitwise(gpu, monkeypatch, tc, pol):
