@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
 #endif
   const double h = row.h;
   const int i0 = blockIdx.x * kPrepTcElems * blockDim.x + threadIdx.x;
+  MS_CHECK(b < d.B, "batch prep: trajectory index");
   double xv[kPrepTcElems], kv[kPrepTcElems][NT];
 #if MS_TC_PACKED == 1
   double wv[kPrepTcElems];

@@ -10,6 +10,7 @@
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "../../include/mixedstep_b200.h"
 
@@ -145,6 +146,35 @@ template <> __device__ __forceinline__ double cvt<double>(double x) { return x; 
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---- checked builds ------------------------------------------------------------
+// -DMS_CHECKS=1 (tools/build_checked.py) compiles bounds and alignment checks into
+// the kernels' memory movement: a failed check prints its site and traps, so a
+// bad access ends the kernel with an error instead of corrupting memory. The
+// pool runs no compute-sanitizer (profiles/r2_sanitizer_closed.txt); the checked
+// build run over the GPU tests stands in for memcheck.
+#ifndef MS_CHECKS
+#define MS_CHECKS 0
+#endif
+#if MS_CHECKS
+#define MS_CHECK(cond, what)                                                                               \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("MS_CHECK failed: %s (%s:%d) block (%d,%d) thread %d\n", what, __FILE__, __LINE__, blockIdx.x, \
+             blockIdx.y, threadIdx.x);                                                                     \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define MS_CHECK(cond, what) \
+  do {                       \
+  } while (0)
+#endif
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+  uint32_t v;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
 }
 
 // ---- launch accounting ---------------------------------------------------------

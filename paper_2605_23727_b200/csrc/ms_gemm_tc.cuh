@@ -217,6 +217,7 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
         const float A = __fadd_rn(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]));
         const float Bv = __fadd_rn(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
         const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(cur[q].c, A), __fmul_rn(cur[q].s, Bv)));
+        MS_CHECK(i < d.n && tb0 + tq < d.B, "contraction epilogue: element outside the ensemble");
         const double o = ws_add(cur[q].f, (double)coup, t.a.ws32);
 #if MS_TC_STCG
         __stcg(outp[tq] + i, o);  // a global store (the pointer comes through shared memory)

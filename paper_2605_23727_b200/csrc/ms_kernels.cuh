@@ -285,6 +285,7 @@ __device__ __forceinline__ bool prep_agent(const PrepArgs& p, const PrepCtx& c, 
   if (p.split) {
     GS sv, cv;
     dsincos(xg, &sv, &cv);
+    MS_CHECK(i >= 0 && 2 * i + 1 < 2 * p.ld, "prep: column data index");
     gin[2 * i] = sv;  // split column data: interleaved (s_j, c_j) pairs
     gin[2 * i + 1] = cv;
     if constexpr (sizeof(GS) == 4)
@@ -376,7 +377,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (mbar_try(bar, parity)) return;
   mbar_wait_slow(bar, parity);
 }
+// dst inside this CTA's dynamic shared memory, 16-byte granularity (checked builds)
+__device__ __forceinline__ void check_bulk(const void* dst, const void* src, uint32_t bytes) {
+#if MS_CHECKS
+  extern __shared__ unsigned char ms_dyn_smem[];
+  const uint32_t base = smem_u32(ms_dyn_smem), d = smem_u32(dst);
+  MS_CHECK(d >= base && d + bytes <= base + dyn_smem_bytes(), "bulk copy outside dynamic shared memory");
+  MS_CHECK((d & 15u) == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (bytes & 15u) == 0,
+           "bulk copy alignment");
+#else
+  (void)dst; (void)src; (void)bytes;
+#endif
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  check_bulk(dst, src, bytes);
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
@@ -386,6 +400,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // the same copy with an L2 eviction-priority policy (createpolicy)
 __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                               uint64_t pol) {
+  check_bulk(dst, src, bytes);
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           smem_u32(dst)),
@@ -656,6 +671,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
                                lane);
           const uint4* sp = reinterpret_cast<const uint4*>(sv) + lane * (VEC / 2);
           const int nit = cc == kChunkCols ? kChunkCols / COLS_IT : (cc - lane * VEC + COLS_IT - 1) / COLS_IT;
+#if MS_CHECKS
+          for (int k = 0; k < R; ++k)
+            MS_CHECK(nit <= 0 || ((size_t)ko[k] + (size_t)(nit - 1) * 32 + 1) * VEC <= (size_t)(a.row1 - a.row0) * ld,
+                     "register sweep: K load past the handle's rows");
+          MS_CHECK(nit <= 0 || (lane * (VEC / 2) + (nit - 1) * 16 * VEC + VEC / 2) * 16 <=
+                                   (int)(NCOL * kChunkCols * sizeof(GS)), "register sweep: column pair past the chunk");
+#endif
           auto sweep_chunk = [&](auto ftz) {
 #if MS_PK_PREFETCH
           // software-pipelined: the next step's K vectors are in flight while
@@ -797,6 +819,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
         } else {
           coup = mul<SS>(mw, A[k]);
         }
+        MS_CHECK(r >= a.row0 && r < a.row1, "register sweep: output row outside the handle");
         const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
         out[(int64_t)r * a.d + a.cs] = o;
         nonfinite |= !isfinite(o);
@@ -1176,6 +1199,8 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
       const int cc = min(G::TC, ld - c0);
       const uint32_t kbytes = (uint32_t)(cc * sizeof(KT));
       const uint32_t sbytes = (uint32_t)(cc * sizeof(GS));
+      MS_CHECK(r0 >= a.row0 && r0 + nr <= a.row1 && c0 + cc <= ld && nr <= G::RG && cc <= G::TC,
+               "TMA sweep: tile outside the handle");
       unsigned char* sk = smem + (size_t)st * G::STAGE_BYTES;
       GS* ss = reinterpret_cast<GS*>(sk + G::KBYTES);
       if (lane == 0) {
@@ -1279,6 +1304,7 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
     for (int k = 0; k < G::RPW; ++k) {
       if (lane == k && k < nr) {
         const int r = r0 + rows[k];
+        MS_CHECK(r >= a.row0 && r < a.row1, "TMA sweep: output row outside the handle");
         const SS si = (SS)gin[2 * r], ci = (SS)gin[2 * r + 1];
         const SS coup = mul<SS>(mw, sub<SS>(mul<SS>(ci, A[k]), mul<SS>(si, B[k])));
         const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
@@ -1354,9 +1380,11 @@ __global__ void __launch_bounds__(kSeqThreads) k_rhs_seq(RhsArgs a) {
       if (rr >= nrows || j >= n) continue;
       const int r = r0 + rr;
       GS kg;
+      MS_CHECK(r >= a.row0 && r < a.row1 && j < a.n && j <= a.ld, "seq sweep: K index");
       if constexpr (KS == MS_K_SCALAR) kg = kscal;
       else kg = (GS)k2f(K[(size_t)(r - a.row0) * a.ld + j]);
       SS* dst = tile + ((size_t)buf * NA * kSeqRows + rr) * P + jj;
+      MS_CHECK((size_t)((dst - tile) + (NA - 1) * kSeqRows * P + 1) * sizeof(SS) <= Gm::SMEM, "seq sweep: tile index");
       if constexpr (SPLIT) {
         dst[0] = (SS)mul<GS>(kg, gin[2 * j]);
         dst[kSeqRows * P] = (SS)mul<GS>(kg, gin[2 * j + 1]);
