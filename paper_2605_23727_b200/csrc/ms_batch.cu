@@ -679,9 +679,15 @@ int ms_batch_create(ms_system_t sys, int32_t batch, const double* omega, int32_t
     BCK(cudaMemcpy(m->omega, omega, sizeof(double) * bn, cudaMemcpyHostToDevice));
     {  // the records' F: RN32(omega), F of a binary32 row (systems.cpp:136-139; the
        // host cast rounds to nearest); the tensor-core path runs binary32 rows only
+#if MS_TC_PACKED == 3
+      std::vector<float> r(bn);
+      for (size_t e = 0; e < bn; ++e) r[e] = (float)omega[e];
+      BCK(cudaMemcpy(d.rec, r.data(), sizeof(float) * bn, cudaMemcpyHostToDevice));
+#else
       std::vector<TcRec> r(bn);
       for (size_t e = 0; e < bn; ++e) r[e] = TcRec{0.f, 0.f, (double)(float)omega[e]};
       BCK(cudaMemcpy(d.rec, r.data(), sizeof(TcRec) * bn, cudaMemcpyHostToDevice));
+#endif
     }
     BCK(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
     BCK(cudaEventCreate(&m->ev0));

@@ -28,7 +28,7 @@ struct BatchDev {
   void* sc;                       // GS-typed s (first B*n) and c (next B*n)
   void* op;                       // GEMM operand [B][4][ld] in K's 16-bit format: s_hi, s_lo, c_hi, c_lo
   double* fvc;                    // F (omega in FS) [B][n]
-  void* rec;                      // tensor-core epilogue records TcRec [B][n]; F written once at creation
+  void* rec;                      // tensor-core epilogue F: TcRec [B][n] records, or RN32(omega) floats (MS_TC_PACKED 3); written at creation
   Ctl* ctl;                       // [B]
   int* flag;                      // [1] any trajectory still running (host loop / conditional)
   // error estimate folded into the last stage's contraction epilogue (MS_BFIN_EPI):
@@ -74,6 +74,11 @@ __device__ __forceinline__ double b_fval(const BatchDev& d, int64_t e, int fs32)
 //    pairs + a separate F array instead measured 21 vs 26 us per prep but a
 //    64 vs 41 us contraction.)
 // 1: the prep writes whole {s, c, F} records every stage; 0: (s, c) pairs + omega
+// 3: (s, c) pairs in `sc` (written by the prep) and F = RN32(omega) as a binary32
+//    array in `rec` (written once at creation): 12 B per element, both arrays
+//    copied into shared memory by the contraction's bulk copies (MS_T2_SREC).
+//    Measured: prep 20.9 vs 23.0 us, contraction 47.3 vs 38.9 us
+//    (profiles/r2_c5_srec.txt), so the default stays 2
 #define MS_TC_PACKED 2
 #endif
 struct __align__(16) TcRec {
@@ -248,6 +253,8 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
 #if MS_TC_PACKED == 1
   TcRec* rec = reinterpret_cast<TcRec*>(d.sc) + (int64_t)b * d.n;
   const double* om = d.omega + (int64_t)b * d.n;
+#elif MS_TC_PACKED == 3
+  float2* rec = reinterpret_cast<float2*>(d.sc) + (int64_t)b * d.n;
 #else
   TcRec* rec = reinterpret_cast<TcRec*>(d.rec) + (int64_t)b * d.n;
 #endif
@@ -305,6 +312,8 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
     r.c = cv;
     r.f = (double)__double2float_rn(wv[u]);  // b_fval, fs32
     rec[i] = r;
+#elif MS_TC_PACKED == 3
+    rec[i] = make_float2(sv, cv);  // F was written at creation
 #else
     *reinterpret_cast<float2*>(rec + i) = make_float2(sv, cv);  // F was written at creation
 #endif

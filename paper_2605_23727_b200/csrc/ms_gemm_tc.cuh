@@ -187,6 +187,11 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
 #else
         v[q] = reinterpret_cast<const TcRec*>(d.rec)[e];
 #endif
+#elif MS_TC_PACKED == 3
+        const float2 p = sc2[e];
+        v[q].s = p.x;
+        v[q].c = p.y;
+        v[q].f = (double)reinterpret_cast<const float*>(d.rec)[e];
 #else
         const float2 p = sc2[e];
         v[q].s = p.x;
@@ -407,8 +412,18 @@ __global__ void __launch_bounds__(kTcThreads, MS_TC_MINB)
 #ifndef MS_T2_BN
 #define MS_T2_BN 512     // GEMM columns per pair tile: 512 (two N256 MMAs, all of TMEM) or 256
 #endif
+// MS_T2_SREC: the epilogue reads its {s, c, F} records from shared memory,
+// staged by bulk copies (two 32 KB slots prefetched while the MMAs run, the
+// rest into the drained operand ring), instead of per-thread global loads
+#ifndef MS_T2_SREC
+#define MS_T2_SREC 1
+#endif
 #ifndef MS_T2_STAGES
+#if MS_T2_SREC
+#define MS_T2_STAGES 3   // leaves room for the two prefetched record slots
+#else
 #define MS_T2_STAGES 4
+#endif
 #endif
 #ifndef MS_T2_MINB
 #define MS_T2_MINB 1
@@ -426,7 +441,29 @@ constexpr int kT2ABytes = kT2BM * kTcBK * 2;               // 16 KB
 constexpr int kT2BBytes = kT2NMma * kT2Half * kTcBK * 2;   // 16 KB per N256 MMA
 constexpr int kT2StageBytes = kT2ABytes + kT2BBytes;
 constexpr int kT2Threads = 64 + 32 * kT2EpiWarps;
-constexpr size_t kT2Smem = 1024 + (size_t)kT2Stages * kT2StageBytes + 256;
+// record staging (MS_T2_SREC): slot g holds the records of epilogue group g of
+// both column parts (trajectories 8g..8g+7 and 64+8g..64+8g+7 of the pair tile)
+// for this CTA's 128 rows: 16 x 128 x 16 B = 32 KB, laid out [part*8+q][row]
+#if MS_TC_PACKED == 3
+// (s, c) pairs and F in separate arrays: per trajectory a 128 x 8 B (s, c) block
+// and a 128 x 4 B F block, each copied as the 16-byte-aligned run covering it
+// (+16 B slack: ragged N leaves the source unaligned)
+constexpr int kT2ScStride = kT2BM * 8 + 16, kT2FStride = kT2BM * 4 + 16;
+constexpr int kT2SlotBytes = 16 * (kT2ScStride + kT2FStride);
+constexpr int kT2SpareSlots = 3;
+#else
+constexpr int kT2ScStride = kT2BM * 16, kT2FStride = 0;  // whole 16-byte {s, c, F} records
+constexpr int kT2SlotBytes = 16 * kT2BM * 16;
+constexpr int kT2SpareSlots = 2;
+#endif
+constexpr int kT2NSlot = 8;
+constexpr int kT2Spare = MS_T2_SREC ? kT2SpareSlots : 0;  // slots prefetched at kernel start
+constexpr int kT2RingSlots = (kT2Stages * kT2StageBytes) / kT2SlotBytes;
+constexpr int kT2RingUse = kT2RingSlots < kT2NSlot - kT2Spare ? kT2RingSlots : kT2NSlot - kT2Spare;
+static_assert(!MS_T2_SREC || (kT2BN == 512 && kT2EpiWarps == 8 && !MS_TC_FIN), "record staging layout");
+static_assert(!MS_T2_SREC || kT2Spare + kT2RingUse + kT2Spare >= kT2NSlot, "record slots: each spare reused once");
+static_assert(!MS_T2_SREC || kT2NSlot - kT2Spare - kT2RingUse <= 2, "record slots: at most two spares refilled");
+constexpr size_t kT2Smem = 1024 + (size_t)kT2Stages * kT2StageBytes + (size_t)kT2Spare * kT2SlotBytes + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -441,11 +478,96 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t ran
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// end-of-kernel pair barrier without release semantics: it only orders the two
+// CTAs' TMEM use before the collective dealloc; a .release arrive compiles to
+// MEMBAR.ALL.GPU, which makes every CTA wait for its k stores to drain first
+#ifndef MS_T2_END_RELAXED
+#define MS_T2_END_RELAXED 1
+#endif
+__device__ __forceinline__ void cluster_sync_end() {
+#if MS_T2_END_RELAXED
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+#else
+  cluster_sync_all();
+#endif
+}
 __device__ __forceinline__ void tma2_load(uint32_t dst, const CUtensorMap* tm, uint32_t bar_cluster, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
+}
+
+// Coupling epilogue with the records in shared memory (MS_T2_SREC): warp
+// (q4, part) handles rows q4*32 + lane of this CTA and trajectories
+// part*64 .. part*64+63 of the pair tile, eight per group g (TMEM columns
+// part*256 + 32g ..), group g's records in slot g. The arithmetic is
+// tc_epilogue's, element for element.
+template <class SlotPtr>
+__device__ __forceinline__ void tc_epilogue_srec(const TcArgs& t, uint32_t lane_addr, int i, int rr, int tb0, int part,
+                                                 const int* skip, double* const* outp, uint64_t* tmem_full,
+                                                 uint64_t* rec_full, uint64_t* rec_free, SlotPtr slot_ptr) {
+  const BatchDev& d = t.a.d;
+  const float mw = (float)d.mw;
+  const bool row_ok = i < t.n;
+  tc_wait(tmem_full, 0);
+  tc_fence_after();
+#pragma unroll 1
+  for (int g = 0; g < kT2NSlot; ++g) {
+    uint32_t r[32];
+#ifndef MS_T2_EXP_EPI  // timing experiments only (results wrong): 1 no k stores, 2 no record reads, 3 no TMEM loads
+#define MS_T2_EXP_EPI 0
+#endif
+#if MS_T2_EXP_EPI == 3
+#pragma unroll
+    for (int k = 0; k < 32; ++k) r[k] = (uint32_t)(k + g);
+#else
+    tc_ld32(lane_addr + (uint32_t)(part * 256 + g * 32), r);
+#endif
+#if MS_T2_EXP_EPI != 2
+    tc_wait(&rec_full[g], 0);
+#endif
+    const unsigned char* sb = slot_ptr(g);
+    if (row_ok) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int tq = part * 64 + g * 8 + q;
+        if (skip[tq]) continue;
+#if MS_T2_EXP_EPI == 2
+        const TcRec rc{0.5f + (float)q, 0.25f, 1.0};
+        (void)sb;
+#else
+        const int j = part * 8 + q;
+#if MS_TC_PACKED == 3
+        // block j starts at the 16-byte boundary below the trajectory's first row
+        const int64_t e0 = (int64_t)(tb0 + tq) * d.n + (i - rr);
+        const uint32_t sco = (uint32_t)(reinterpret_cast<uintptr_t>(reinterpret_cast<const float2*>(d.sc) + e0) & 15);
+        const uint32_t fo = (uint32_t)(reinterpret_cast<uintptr_t>(reinterpret_cast<const float*>(d.rec) + e0) & 15);
+        const float2 scv = *reinterpret_cast<const float2*>(sb + (size_t)j * kT2ScStride + sco + (size_t)rr * 8);
+        const float fv = *reinterpret_cast<const float*>(sb + 16 * kT2ScStride + (size_t)j * kT2FStride + fo + (size_t)rr * 4);
+        const TcRec rc{scv.x, scv.y, (double)fv};
+#else
+        const TcRec rc = *reinterpret_cast<const TcRec*>(sb + (size_t)j * kT2ScStride + (size_t)rr * 16);
+#endif
+#endif
+        const float A = __fadd_rn(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]));
+        const float Bv = __fadd_rn(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(rc.c, A), __fmul_rn(rc.s, Bv)));
+        MS_CHECK(i < d.n && (tb0 + tq < d.B), "contraction epilogue: element outside the ensemble");
+        const double o = ws_add(rc.f, (double)coup, t.a.ws32);
+#if MS_T2_EXP_EPI == 1
+        if (o == 12345.678) outp[tq][i] = o;
+#else
+        outp[tq][i] = o;
+#endif
+        if (!isfinite(o)) atomicOr(&d.ctl[tb0 + tq].nf_mask, 1 << t.a.l);
+      }
+    }
+    if (g < kT2Spare && kT2Spare + kT2RingUse + g < kT2NSlot) {  // this spare is refilled with a later slot
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&rec_free[g]);
+    }
+  }
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MINB)
@@ -454,10 +576,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kT2Stages * kT2StageBytes);
+  unsigned char* spare = smem + (size_t)kT2Stages * kT2StageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(spare + (size_t)kT2Spare * kT2SlotBytes);
   uint64_t* empty = full + kT2Stages;
   uint64_t* tmem_full = empty + kT2Stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* rec_full = tmem_full + 1;       // [kT2NSlot] (MS_T2_SREC)
+  uint64_t* rec_free = rec_full + kT2NSlot; // [2]: a spare slot's first records consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rec_free + 2);
+  // where record slot g lives: spare 0/1, then the drained ring, then the spares again
+  auto slot_ptr = [&](int g) -> unsigned char* {
+    if (g < kT2Spare) return spare + (size_t)g * kT2SlotBytes;
+    if (g < kT2Spare + kT2RingUse) return smem + (size_t)(g - kT2Spare) * kT2SlotBytes;
+    return spare + (size_t)((g - kT2Spare - kT2RingUse) & 1) * kT2SlotBytes;
+  };
+  (void)slot_ptr;
 
   __shared__ int tc_skip[kT2BN / 4];
   __shared__ double* tc_out[kT2BN / 4];
@@ -480,6 +612,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
+    for (int g = 0; g < kT2NSlot; ++g) mbar_init(&rec_full[g], 1);
+    mbar_init(&rec_free[0], kT2EpiWarps);
+    mbar_init(&rec_free[1], kT2EpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -497,8 +632,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
   // not released early (its blocks would sit on the SMs through the mainloop)
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
+  // bulk copies of record slot g: for each valid trajectory of the slot, this
+  // CTA's rows [m0, m0 + rows) are one contiguous 16-byte-per-row run
+  auto issue_slot = [&](int g) {
+    const BatchDev& d = t.a.d;
+    const int rows = min(kT2BM, d.n - m0);
+    const int tb0 = n0 >> 2;
+    unsigned char* dst = slot_ptr(g);
+#if MS_TC_PACKED == 3
+    // per valid trajectory: the 16-byte-aligned runs covering its (s, c) rows and
+    // F rows (the epilogue recomputes each run's start offset from the address)
+    auto run = [](const void* src, uint32_t bytes, uint32_t& lo_off) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+      const uintptr_t lo = a & ~uintptr_t(15), hi = (a + bytes + 15) & ~uintptr_t(15);
+      lo_off = (uint32_t)(a - lo);
+      return (uint32_t)(hi - lo);
+    };
+    uint32_t total = 0;
+    if (rows > 0)
+      for (int j = 0; j < 16; ++j) {
+        const int b = tb0 + (j >> 3) * 64 + g * 8 + (j & 7);
+        if (b >= d.B) continue;
+        uint32_t o;
+        total += run(reinterpret_cast<const float2*>(d.sc) + (int64_t)b * d.n + m0, rows * 8, o);
+        total += run(reinterpret_cast<const float*>(d.rec) + (int64_t)b * d.n + m0, rows * 4, o);
+      }
+    mbar_expect_tx(&rec_full[g], total);
+    if (rows <= 0) return;
+    for (int j = 0; j < 16; ++j) {
+      const int b = tb0 + (j >> 3) * 64 + g * 8 + (j & 7);
+      if (b >= d.B) continue;
+      uint32_t o1, o2;
+      const float2* s1 = reinterpret_cast<const float2*>(d.sc) + (int64_t)b * d.n + m0;
+      const float* s2 = reinterpret_cast<const float*>(d.rec) + (int64_t)b * d.n + m0;
+      const uint32_t n1 = run(s1, rows * 8, o1), n2 = run(s2, rows * 4, o2);
+      unsigned char* d1 = dst + (size_t)j * kT2ScStride;
+      unsigned char* d2 = dst + 16 * kT2ScStride + (size_t)j * kT2FStride;
+      bulk_g2s(d1, reinterpret_cast<const unsigned char*>(s1) - o1, n1, &rec_full[g]);
+      bulk_g2s(d2, reinterpret_cast<const unsigned char*>(s2) - o2, n2, &rec_full[g]);
+    }
+#else
+    uint32_t bytes = 0;
+    if (rows > 0)
+      for (int j = 0; j < 16; ++j) bytes += (tb0 + (j >> 3) * 64 + g * 8 + (j & 7) < d.B) ? rows * 16 : 0;
+    mbar_expect_tx(&rec_full[g], bytes);
+    if (rows <= 0) return;
+    const TcRec* rec = reinterpret_cast<const TcRec*>(d.rec);
+    for (int j = 0; j < 16; ++j) {
+      const int b = tb0 + (j >> 3) * 64 + g * 8 + (j & 7);
+      if (b < d.B) bulk_g2s(dst + (size_t)j * kT2ScStride, rec + (int64_t)b * d.n + m0, (uint32_t)rows * 16, &rec_full[g]);
+    }
+#endif
+  };
+  (void)issue_slot;
+
   if (warp == 0) {
     if (lane == 0) {  // TMA producer (both CTAs): own smem, completion on the leader's barrier
+#if MS_T2_SREC && MS_T2_EXP_EPI != 2
+      for (int g = 0; g < kT2Spare; ++g) issue_slot(g);  // overlap the mainloop
+#endif
       for (int kb = 0; kb < nkb; ++kb) {
         const int st = kb % kT2Stages;
         if (kb >= kT2Stages) tc_wait(&empty[st], ((kb / kT2Stages) & 1) ^ 1);
@@ -514,6 +706,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
         for (int hf = 0; hf < MS_T2_EXP_NB; ++hf)
           tma2_load(sb + hf * (kT2Half * kTcBK * 2), &tmB, bar, kb * kTcBK, n0 + hf * 2 * kT2Half + (int)rank * kT2Half);
       }
+#if MS_T2_SREC && MS_T2_EXP_EPI != 2
+      // the ring is free once the last use of every stage has been committed
+      // (the leader's commits arrive on both CTAs' empty barriers)
+      for (int st = 0; st < kT2Stages && st < nkb; ++st) {
+        const int kb_last = st + ((nkb - 1 - st) / kT2Stages) * kT2Stages;
+        tc_wait(&empty[st], (kb_last / kT2Stages) & 1);
+      }
+      for (int g = kT2Spare; g < kT2Spare + kT2RingUse; ++g) issue_slot(g);
+      for (int g = kT2Spare + kT2RingUse; g < kT2NSlot; ++g) {
+        tc_wait(&rec_free[(g - kT2Spare - kT2RingUse) & 1], 0);  // the spare's first slot is consumed
+        issue_slot(g);
+      }
+#endif
     }
     if (t.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else if (warp == 1) {
@@ -579,8 +784,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
     constexpr int kCols = kT2BN / (kT2EpiWarps / 4);  // columns per epilogue warp
 #ifndef MS_T2_NOEPI
+#if MS_T2_SREC
+    (void)kCols;
+    tc_epilogue_srec(t, lane_addr, i, q4 * 32 + lane, tb0, part, tc_skip, tc_out, tmem_full, rec_full, rec_free,
+                     slot_ptr);
+#else
     tc_epilogue(t, lane_addr, i, tb0, part * kCols, (part + 1) * kCols, tc_skip, tc_out, tmem_full,
                 t.a.fin ? tc_fin : nullptr);
+#endif
 #else
     tc_wait(tmem_full, 0);
     tc_fence_after();
@@ -589,7 +800,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
   }
   tc_fence_before();
   __syncthreads();
-  cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
+  cluster_sync_end();  // both CTAs done with the pair's TMEM and barriers
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kT2BN));

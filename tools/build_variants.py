@@ -145,6 +145,15 @@ VARIANTS = {
     "tcv_stcg": ("ms_batch.cu", {"MS_TC_STCG": 1}),
     "tcv_fin": ("ms_batch.cu", {"MS_TC_FIN": 1}),
     "tcv_noepi": ("ms_batch.cu", {"MS_T2_NOEPI": 1}),
+    # round 2: epilogue records staged in shared memory (default) vs per-thread loads
+    "tcs_new": ("ms_batch.cu", {}),
+    "tcs_old": ("ms_batch.cu", {"MS_T2_SREC": 0, "MS_T2_END_RELAXED": 0, "MS_TC_PACKED": 2}),
+    "tcs_noepi": ("ms_batch.cu", {"MS_T2_NOEPI": 1, "MS_T2_SREC": 0}),
+    "tcs_p3_nosrec": ("ms_batch.cu", {"MS_T2_SREC": 0}),
+    "tcs_p2": ("ms_batch.cu", {"MS_TC_PACKED": 2}),
+    "tcx_nostore": ("ms_batch.cu", {"MS_T2_EXP_EPI": 1}),
+    "tcx_norec": ("ms_batch.cu", {"MS_T2_EXP_EPI": 2}),
+    "tcx_notmem": ("ms_batch.cu", {"MS_T2_EXP_EPI": 3}),
     "pf_t384": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_THREADS": 384}),
     "pf_t256": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_THREADS": 256}),
     "pf_r4": ("ms_rhs_fast.cu", {"MS_PK_PREFETCH": 1, "MS_FAST_R": 4}),
