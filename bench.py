@@ -139,6 +139,11 @@ def sweep_kernel(kdtype, whole):
         name = f"void k_rhs_tma<float, float, 1, {nxt}>"
         label = f"k_rhs_tma<f32 sum, f32 G, K f32, NEXT={nxt}> (cp.async.bulk-fed K sweep" + \
                 (", folds the next stage's prep)" if nxt else ")")
+    elif kdtype == "f16" and os.environ.get("MS_SWEEP", "tc16") == "tc16":
+        name = "void k_rhs_tc16<2>"
+        label = ("k_rhs_tc16<K f16> (tcgen05 M128 N16 sweep over 16 KB K tile images, f16 hi+lo operands, "
+                 "binary32 sums of the 16-column dot products)")
+        kdtype = "f16tc"
     else:
         ks = {"f32": 1, "f16": 2, "bf16": 3}[kdtype]
         name = f"void k_rhs_fast<1, 1, float, float, {ks}>"

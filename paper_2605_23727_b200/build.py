@@ -24,7 +24,7 @@ ORACLE_DIR = ROOT / "oracle"
 
 SOURCES = ["ms_api.cu", "ms_rhs_fast.cu", "ms_rhs_faithful.cu", "ms_batch.cu", "ms_multi.cu"]
 HEADERS = ["ms_common.cuh", "ms_kernels.cuh", "ms_dispatch.h", "ms_ddpow.cuh", "ms_batch.cuh", "ms_gemm_tc.cuh",
-           "ms_internal.h", "ms_multi.cuh"]
+           "ms_internal.h", "ms_multi.cuh", "ms_tcgen05.cuh", "ms_gemv_tc.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

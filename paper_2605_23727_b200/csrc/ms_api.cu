@@ -322,6 +322,8 @@ struct ms_system {
   double* dense = nullptr;
   double* dense_t = nullptr;
   int64_t dense_cap = -1;
+  // f16-K tensor-core sweep resources (ms_gemv_tc.cuh GvRes) or null
+  void* gv = nullptr;
   // host-driven (sharded) loop
   bool loop_active = false;
   SolvePlanStore* loop_plan = nullptr;
@@ -362,6 +364,7 @@ size_t bufs_bytes(const ms_system* s, int64_t log_cap) {
   total += (kMaxStages + 1) * vec;                       // kb
   total += 3 * vec;                                      // xn, xt, scratch
   total += 2 * al256(sizeof(double) * 2 * s->ld);        // gin, gin2
+  total += al256((size_t)(s->ld / 64 + 1) * 512);         // op16
   total += al256(sizeof(double) * s->ld);                // rowc
   total += al256(sizeof(double) * s->n);                 // fvc
   total += al256(sizeof(double) * fin_blocks);           // part
@@ -386,6 +389,8 @@ void carve_bufs(const ms_system* s, char* base, int64_t log_cap, Bufs& B) {
   B.scratch = reinterpret_cast<double*>(take(sizeof(double) * dn));
   B.gin = take(sizeof(double) * 2 * s->ld);
   B.gin2 = take(sizeof(double) * 2 * s->ld);
+  B.op16 = take((size_t)(s->ld / 64 + 1) * 512);
+  if (!s->gv) B.op16 = nullptr;  // written by the preps only for the tensor-core sweep
   B.rowc = take(sizeof(double) * s->ld);
   B.fvc = reinterpret_cast<double*>(take(sizeof(double) * s->n));
   B.part = reinterpret_cast<double*>(take(sizeof(double) * fin_blocks));
@@ -527,6 +532,8 @@ RhsArgs rhs_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_
   a.ws32 = (is32(sp.f_prec) && is32(sp.sum_prec)) ? 1 : 0;
   a.k_stream = k_stream_of(s);
   a.pk = env_is("MS_SWEEP_PK", "off") ? 0 : 1;
+  a.tc16 = s->gv;
+  a.op16 = B.op16;
   return a;
 }
 
@@ -1769,6 +1776,7 @@ int ms_system_create(const ms_system_desc* d, ms_system_t* out) {
       }
       CK(cudaDeviceSynchronize());
       scan_k_tiny(s.get());
+      if (s->mkind == MD_KUR) s->gv = tc16_create(s->K, s->ld, s->row1 - s->row0, s->ks);
     }
     CK(cudaDeviceSynchronize());
     *out = s.release();
@@ -1786,6 +1794,7 @@ int ms_system_destroy(ms_system_t s) {
     }
     for (void* p : s->dev_arrays) cudaFree(p);
     if (s->K) cudaFree(s->K);
+    tc16_destroy(s->gv);
     if (s->ws_mem) cudaFree(s->ws_mem);
     if (s->snap) cudaFree(s->snap);
     if (s->dense) cudaFree(s->dense);
@@ -1809,6 +1818,7 @@ int ms_system_fill_k_uniform(ms_system_t s, uint64_t seed, uint64_t stream, doub
     else if (s->ks == MS_K_F16) k_fill_uniform<MS_K_F16><<<grid, 256, 0, s->stream>>>((__half*)s->K, s->n, s->row0, rows, s->ld, state0, lo, hi);
     else k_fill_uniform<MS_K_BF16><<<grid, 256, 0, s->stream>>>((__nv_bfloat16*)s->K, s->n, s->row0, rows, s->ld, state0, lo, hi);
     CK(cudaGetLastError());
+    tc16_refresh(s->gv, s->K, s->ld, rows, s->stream);
     scan_k_tiny(s);
   });
 }

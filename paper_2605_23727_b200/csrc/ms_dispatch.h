@@ -38,6 +38,14 @@ bool launch_eval_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, 
 // shared memory, one row per warp), MS_SWEEP=small only; false = not used
 bool launch_sweep_small(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a);
 
+// the f16-K tensor-core sweep's per-handle resources (K tensor map, chunk
+// partials, tickets): created with a Kuramoto system whose K is f16, null if
+// not applicable
+void* tc16_create(const void* K, int64_t ld, int rows, int ks);
+// rebuild the tile images after K changed (ms_system_fill_k_uniform)
+void tc16_refresh(void* r, const void* K, int64_t ld, int rows, cudaStream_t st);
+void tc16_destroy(void* r);
+
 // Programmatic dependent launch for the kernels of the attempt chain (each
 // starts with pdl_enter()); MS_PDL=off launches them plainly.
 bool pdl_enabled();

@@ -1,0 +1,339 @@
+// ms_gemv_tc.cuh — the split Kuramoto's K sweep for f16 K on the 5th-generation
+// tensor cores (MS_SWEEP=tc16).
+//
+//   A_i = sum_j K_ij s_j,  B_i = sum_j K_ij c_j      (systems.cpp:141-143, split)
+//   k_i = (double)(F_i + RN(mw (c_i A_i - s_i B_i)))  (systems.cpp:59-62)
+//
+// The CUDA-core sweeps spend three instructions per f16 K element (convert,
+// packed multiply, packed add) and sustain ~5.5 TB/s in the board's power
+// cap; here the products run on the tensor pipe and the SM only moves bytes.
+// Operands: A = a 128-row x 64-column tile of K (a 16 KB SWIZZLE_128B image
+// kept beside the row-major K, k_tile_k16; one bulk copy each), B = the
+// tile's 64 column values as four f16 rows s_hi, s_lo, c_hi, c_lo (hi =
+// RN16(v), lo = RN16(v - hi): ~22 bits of the binary32 value; products with
+// f16 K are exact; the stage prep writes them as a swizzled image,
+// ms_kernels.cuh op16_put) plus 12 zero rows (N = 16, the smallest M128 shape).
+//
+// Rounding: every MMA (16 columns) starts from a zero accumulator, so the
+// tensor core only forms a 16-term dot product; the products' sums are then
+// added in binary32 RN on the CUDA cores, in ascending column order:
+//   a_hi += dot_hi (k-step by k-step), a_lo += dot_lo, per 2048-column chunk
+//   A_chunk = a_hi + a_lo;  A = ((A_0 + A_1) + A_2) + ...
+// The order depends only on N (never on the row partition or the grid), so
+// sharded handles give the rows of the whole handle bit for bit. It is not the
+// CUDA-core sweeps' order: parity with the oracle is by tolerance (counts and
+// final state, tests/test_gpu_tc16.py).
+//
+// Work: units = (128-row tile, 2048-column chunk), split contiguously over one
+// CTA per SM. Per CTA:
+//   warp 0   producer: bulk copies of the K tile images (evict-first when K is
+//            streamed) and of the operand rows
+//   warp 1   TMEM allocator + MMA issuer (4 x M128 N16 K16 per k-block, into a
+//            ring of 8 TMEM groups)
+//   warps 2-5  accumulators: tcgen05.ld of each MMA's 4 useful columns, binary32
+//            sums; at a unit's end the chunk sums go to a partial buffer and
+//            the CTA that completes a tile's last chunk (ticket) forms the rows'
+//            totals in chunk order and writes k.
+#pragma once
+
+#include <cuda.h>
+
+#include "ms_kernels.cuh"
+#include "ms_tcgen05.cuh"
+
+namespace msb {
+
+constexpr int kGvBM = 128;      // rows per tile (TMEM lanes)
+constexpr int kGvBK = 64;       // columns per k-block: one 128-byte SW128 row of f16
+constexpr int kGvChunk = 2048;  // columns per unit (fixed: the sums' order depends on N only)
+// K-blocks per pipeline stage: their TMA boxes are issued together, so every
+// row of the tile is read as one KB x 128-byte run (DRAM page locality)
+#ifndef MS_GV_KB
+#define MS_GV_KB 4
+#endif
+constexpr int kGvKB = MS_GV_KB;
+constexpr int kGvABytes = kGvBM * kGvBK * 2;  // 16 KB of K per k-block
+constexpr int kGvBBytes = 16 * kGvBK * 2;     // 2 KB operand tile per k-block (rows 4..15 stay zero)
+constexpr int kGvStageBytes = kGvKB * (kGvABytes + kGvBBytes);
+#ifndef MS_GV_STAGES
+#define MS_GV_STAGES (12 / MS_GV_KB)
+#endif
+constexpr int kGvStages = MS_GV_STAGES;
+static_assert(kGvChunk % (kGvKB * kGvBK) == 0, "stages tile the chunk");
+#ifndef MS_GV_GROUPS
+#define MS_GV_GROUPS 8
+#endif
+constexpr int kGvGroups = MS_GV_GROUPS;       // TMEM groups (k-blocks between issuer and accumulators)
+#ifndef MS_GV_BATCH
+#define MS_GV_BATCH 1
+#endif
+constexpr int kGvBatch = MS_GV_BATCH;         // k-blocks the accumulators read per TMEM round trip
+static_assert(kGvBatch <= kGvGroups, "accumulator batch");
+#ifndef MS_GV_EXP
+#define MS_GV_EXP 0  // timing experiments only (results wrong): 1 = accumulators skip the TMEM loads
+#endif
+constexpr int kGvThreads = 6 * 32;
+constexpr size_t kGvSmem = 1024 + (size_t)kGvStages * kGvStageBytes + 256;
+constexpr uint32_t kGvTmemCols = kGvGroups * 64;  // kGvGroups x 4 MMAs x 16 columns (power of two)
+static_assert(kGvTmemCols == 256 || kGvTmemCols == 512, "TMEM allocation");
+
+// per-handle resources (created with the system, ms_api.cu)
+struct GvRes {
+  unsigned char* kt;  // K as MMA tile images: [tile][k-block][16 KB, SWIZZLE_128B] (kept beside row-major K)
+  float2* part;       // [tiles][chunks][128] chunk sums (A, B)
+  int* cnt;           // [tiles] chunk tickets (zero between launches)
+  int tiles, chunks, kblocks;
+};
+
+struct GvArgs {
+  const unsigned char* kt;
+  float2* part;
+  int* cnt;
+  int tiles, chunks, kblocks;
+  uint32_t idesc;
+};
+
+// Tile images of the handle's f16 K rows: 16-byte piece c of row r of
+// (tile, k-block) at r*128 + ((c ^ (r % 8)) * 16) -- the SWIZZLE_128B K-major
+// layout the MMA reads, so one contiguous 16 KB bulk copy stages a tile (the
+// row-major K's 128-byte row pieces cost DRAM page locality). Rows past the
+// handle are zero.
+__global__ void __launch_bounds__(256) k_tile_k16(const __half* K, unsigned char* kt, int64_t ld, int rows,
+                                                  int tiles, int kblocks) {
+  msb::count_launch();
+  const int64_t pieces = (int64_t)tiles * kblocks * kGvBM * 8;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < pieces; q += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(q & 7), r = (int)((q >> 3) % kGvBM);
+    const int64_t tk = q / (8 * kGvBM);  // tile * kblocks + kblock
+    const int tile = (int)(tk / kblocks), kb = (int)(tk % kblocks);
+    const int row = tile * kGvBM + r;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (row < rows) v = *reinterpret_cast<const uint4*>(K + (int64_t)row * ld + (int64_t)kb * kGvBK + c * 8);
+    *reinterpret_cast<uint4*>(kt + tk * kGvABytes + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+  }
+}
+
+__device__ __forceinline__ void gv_ld4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ uint32_t gv_pack(__half lo_col, __half hi_col) {
+  return (uint32_t)__half_as_ushort(lo_col) | ((uint32_t)__half_as_ushort(hi_col) << 16);
+}
+
+// unit u -> (tile, chunk); its k-block count
+__device__ __forceinline__ int gv_nkb(const RhsArgs& a, int ch) {
+  const int cols = min(kGvChunk, (int)a.ld - ch * kGvChunk);
+  return (cols + kGvBK - 1) / kGvBK;
+}
+
+template <int KS>
+__global__ void __launch_bounds__(kGvThreads, 1)
+    k_rhs_tc16(RhsArgs a, GvArgs g) {
+  static_assert(KS == MS_K_F16, "tc16 sweep: f16 K");
+  msb::count_launch();
+  pdl_enter();
+  if (stage_skip(a.ctl, a.l, a.gate)) return;
+  sweep_count(a);
+  extern __shared__ __align__(1024) unsigned char gv_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gv_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kGvStages * kGvStageBytes);
+  uint64_t* empty = full + kGvStages;
+  uint64_t* tfull = empty + kGvStages;
+  uint64_t* tempty = tfull + kGvGroups;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + kGvGroups);
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int U = g.tiles * g.chunks;
+  const int u0 = (int)((int64_t)U * blockIdx.x / gridDim.x);
+  const int u1 = (int)((int64_t)U * (blockIdx.x + 1) / gridDim.x);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGvStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int q = 0; q < kGvGroups; ++q) {
+      mbar_init(&tfull[q], 1);
+      mbar_init(&tempty[q], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // rows 4..15 of every operand tile are zero for the whole kernel
+  for (int idx = threadIdx.x; idx < kGvStages * kGvKB * (12 * 128 / 16); idx += blockDim.x) {
+    const int t = idx / (12 * 128 / 16), o = idx % (12 * 128 / 16);
+    *reinterpret_cast<uint4*>(smem + (size_t)(t / kGvKB) * kGvStageBytes + kGvKB * kGvABytes +
+                              (t % kGvKB) * kGvBBytes + 4 * 128 + o * 16) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "n"(kGvTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  bool nonfinite = false;
+
+  if (warp == 0) {
+    // producer: bulk copies of the K tile images and of the operand rows 0-3
+    const uint64_t pol = a.k_stream ? l2_evict_first() : l2_evict_normal();
+    const unsigned char* op = static_cast<const unsigned char*>(a.op16);
+    int sg = 0;  // stage counter
+    for (int u = u0; u < u1; ++u) {
+      const int tile = u / g.chunks, ch = u % g.chunks;
+      const int nkb = gv_nkb(a, ch);
+      for (int kb = 0; kb < nkb; kb += kGvKB, ++sg) {
+        const int st = sg % kGvStages;
+        if (sg >= kGvStages) {
+          if (lane == 0) tc_wait(&empty[st], ((sg / kGvStages) & 1) ^ 1);
+          __syncwarp();
+        }
+        unsigned char* sa = smem + (size_t)st * kGvStageBytes;
+        unsigned char* sb = sa + kGvKB * kGvABytes;
+        const int c0 = ch * kGvChunk + kb * kGvBK;
+        if (lane == 0) mbar_expect_tx(&full[st], kGvKB * (kGvABytes + 512));
+        __syncwarp();
+        if (lane < kGvKB)  // one contiguous 16 KB tile image per k-block
+          bulk_g2s_hint(sa + lane * kGvABytes,
+                        g.kt + ((int64_t)tile * g.kblocks + (c0 / kGvBK) + lane) * kGvABytes, kGvABytes, &full[st], pol);
+        else if (lane < 2 * kGvKB)  // and the operand rows 0-3 of its B tile (the prep's image)
+          bulk_g2s(sb + (lane - kGvKB) * kGvBBytes, op + (size_t)((c0 / kGvBK) + lane - kGvKB) * 512, 512, &full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int kbg = 0, sg = 0;
+      for (int u = u0; u < u1; ++u) {
+        const int nkb = gv_nkb(a, u % g.chunks);
+        for (int kb = 0; kb < nkb; kb += kGvKB, ++sg) {
+          const int st = sg % kGvStages;
+          tc_wait(&full[st], (sg / kGvStages) & 1);
+          const uint32_t sa = smem_u32(smem + (size_t)st * kGvStageBytes);
+          const uint32_t sb = sa + kGvKB * kGvABytes;
+#pragma unroll 1
+          for (int j = 0; j < kGvKB; ++j, ++kbg) {
+            const int grp = kbg % kGvGroups;
+            if (kbg >= kGvGroups) tc_wait(&tempty[grp], ((kbg / kGvGroups) & 1) ^ 1);
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < kGvBK / 16; ++k) {
+              const uint64_t adesc = umma_smem_desc(sa + j * kGvABytes + k * 32);
+              const uint64_t bdesc = umma_smem_desc(sb + j * kGvBBytes + k * 32);
+              asm volatile(
+                  "{\n .reg .pred p;\n setp.ne.b32 p, 0, 0;\n"
+                  " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                      tmem + (uint32_t)(grp * 64 + k * 16)),
+                  "l"(adesc), "l"(bdesc), "r"(g.idesc));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&tfull[grp]))
+                         : "memory");
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&empty[st]))
+                       : "memory");
+        }
+      }
+    }
+  } else {
+    // accumulators: warp%4 = TMEM lane quarter; row rr of the tile
+    const int q4 = warp & 3;
+    const int rr = q4 * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
+    const float* gin = reinterpret_cast<const float*>(a.gin);
+    const float mw = (float)a.mw;
+    double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
+    int kbg = 0;
+    for (int u = u0; u < u1; ++u) {
+      const int tile = u / g.chunks, ch = u % g.chunks;
+      const int nkb = gv_nkb(a, ch);
+      float ah = 0.f, al = 0.f, bh = 0.f, bl = 0.f;
+      // batches of up to kGvBatch k-blocks: one TMEM round trip per batch
+      for (int kb = 0; kb < nkb; kb += kGvBatch) {
+        const int nb = min(kGvBatch, nkb - kb);
+#pragma unroll
+        for (int j = 0; j < kGvBatch; ++j)
+          if (j < nb) tc_wait(&tfull[(kbg + j) % kGvGroups], ((kbg + j) / kGvGroups) & 1);
+        tc_fence_after();
+        uint32_t r[kGvBatch][4][4];
+#if MS_GV_EXP != 1
+#pragma unroll
+        for (int j = 0; j < kGvBatch; ++j)
+          if (j < nb) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gv_ld4(lane_base + (uint32_t)(((kbg + j) % kGvGroups) * 64 + k * 16), r[j][k]);
+          }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#else
+#pragma unroll
+        for (int j = 0; j < kGvBatch; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) r[j][k][0] = r[j][k][1] = r[j][k][2] = r[j][k][3] = 0u;
+#endif
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          for (int j = 0; j < nb; ++j) mbar_arrive(&tempty[(kbg + j) % kGvGroups]);
+#pragma unroll
+        for (int j = 0; j < kGvBatch; ++j)
+          if (j < nb) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              ah = __fadd_rn(ah, __uint_as_float(r[j][k][0]));
+              al = __fadd_rn(al, __uint_as_float(r[j][k][1]));
+              bh = __fadd_rn(bh, __uint_as_float(r[j][k][2]));
+              bl = __fadd_rn(bl, __uint_as_float(r[j][k][3]));
+            }
+          }
+        kbg += nb;
+      }
+      float2* pt = g.part + ((int64_t)tile * g.chunks) * kGvBM;
+      pt[(int64_t)ch * kGvBM + rr] = make_float2(__fadd_rn(ah, al), __fadd_rn(bh, bl));
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 2 && lane == 0) s_last = (atomicAdd(g.cnt + tile, 1) == g.chunks - 1) ? 1 : 0;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (s_last) {
+        __threadfence();
+        const int row = a.row0 + tile * kGvBM + rr;
+        if (row < a.row1) {
+          float2 p = __ldcg(pt + rr);
+          float A = p.x, B = p.y;
+          for (int c = 1; c < g.chunks; ++c) {
+            p = __ldcg(pt + (int64_t)c * kGvBM + rr);
+            A = __fadd_rn(A, p.x);
+            B = __fadd_rn(B, p.y);
+          }
+          const float si = gin[2 * row], ci = gin[2 * row + 1];
+          const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(ci, A), __fmul_rn(si, B)));
+          MS_CHECK(row >= a.row0 && row < a.row1, "tc16 sweep: output row outside the handle");
+          const double o = ws_add(a.fvc[row], (double)coup, a.ws32);
+          out[(int64_t)row * a.d + a.cs] = o;
+          nonfinite |= !isfinite(o);
+        }
+        if (warp == 2 && lane == 0) g.cnt[tile] = 0;  // ready for the next launch
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+  }
+  if (warp >= 2 && __any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kGvTmemCols));
+  }
+}
+
+// instruction descriptor: D f32, A/B f16, both K-major, N = 16, M = 128
+constexpr uint32_t kGvIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(16 >> 3) << 17) |
+                              ((uint32_t)(128 >> 4) << 24);
+
+}  // namespace msb

@@ -101,6 +101,10 @@ struct RhsArgs {
   // packed FMUL2.FTZ products allowed (MS_SWEEP_PK != off; the device flag
   // Ctl::pk_off can still veto them)
   int pk;
+  // host-side: the handle's tensor-core sweep resources (GvRes, ms_gemv_tc.cuh) or null
+  const void* tc16;
+  // the column data's f16 operand image (Bufs::op16), written by the prep
+  const void* op16;
 };
 
 __device__ __forceinline__ void sweep_count(const RhsArgs& a) {
@@ -246,6 +250,22 @@ __device__ __forceinline__ double prep_arg(const PrepArgs& p, const PrepCtx& c, 
   return v;
 }
 
+// The tensor-core sweep's operand image of column j (ms_gemv_tc.cuh): per
+// 64-column k-block 512 bytes = four 128-byte rows s_hi, s_lo, c_hi, c_lo of
+// f16 (hi = RN16(v), lo = RN16(v - hi)), 16-byte chunks in the SWIZZLE_128B
+// order (chunk index XOR row), i.e. rows 0-3 of the MMA's B tile as they sit
+// in shared memory.
+__device__ __forceinline__ void op16_put(void* img, int j, float s, float c) {
+  unsigned char* base = static_cast<unsigned char*>(img) + (size_t)(j >> 6) * 512;
+  const int col = j & 63;
+  const __half sh = __float2half_rn(s), ch = __float2half_rn(c);
+  const __half v[4] = {sh, __float2half_rn(__fsub_rn(s, __half2float(sh))), ch,
+                       __float2half_rn(__fsub_rn(c, __half2float(ch)))};
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    *reinterpret_cast<__half*>(base + r * 128 + ((((col >> 3) ^ r) & 7) << 4) + (col & 7) * 2) = v[r];
+}
+
 // Every per-agent output of one evaluation for agent i: F in FS, the uncoupled
 // slots, the coupled slot's F (fvc), the column value(s) (gin) and the CC row
 // constant (systems.cpp:35-62). Returns whether an output is non-finite.
@@ -288,6 +308,8 @@ __device__ __forceinline__ bool prep_agent(const PrepArgs& p, const PrepCtx& c, 
     MS_CHECK(i >= 0 && 2 * i + 1 < 2 * p.ld, "prep: column data index");
     gin[2 * i] = sv;  // split column data: interleaved (s_j, c_j) pairs
     gin[2 * i + 1] = cv;
+    if constexpr (sizeof(GS) == 4)
+      if (p.B.op16) op16_put(p.B.op16, i, sv, cv);
     if constexpr (sizeof(GS) == 4)
       if (sc_tiny(sv, cv)) c.ctl->pk_off = 1;
   } else {
@@ -1146,6 +1168,9 @@ __device__ __forceinline__ void tma_col_step_pk(const unsigned char* sk, const f
 // column data needs another buffer (pn.B.gin: the other CTAs still read this
 // stage's). The arithmetic is prep_agent's, so the results are bit-identical to
 // k_prep + sweep; host side: launch_attempt (fuse_next_ok in ms_rhs_fast.cu).
+#ifndef MS_TMA_KEEP
+#define MS_TMA_KEEP 0
+#endif
 template <class SS, class GS, int KS, bool NEXT = false>
 __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs a, PrepArgs pn) {
   msb::count_launch();
@@ -1215,8 +1240,10 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
       if (MS_TMA_LANES) {
         for (int r = lane; r < nr; r += 32)
 #if MS_TMA_KHINT
+          // the first MS_TMA_KEEP rows of every CTA's range stay in L2 across
+          // evaluations (evict-last); the rest of a streamed K is evict-first
           bulk_g2s_hint(sk + (size_t)r * G::TC * sizeof(KT), Kbase + (size_t)(r0 + r - a.row0) * ld + c0, kbytes,
-                        &full[st], pol_k);
+                        &full[st], (a.k_stream && r0 + r < rb + MS_TMA_KEEP) ? pol_sc : pol_k);
 #else
           bulk_g2s(sk + (size_t)r * G::TC * sizeof(KT), Kbase + (size_t)(r0 + r - a.row0) * ld + c0, kbytes,
                    &full[st]);

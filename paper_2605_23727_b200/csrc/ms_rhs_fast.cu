@@ -5,7 +5,10 @@
 #include <stdexcept>
 #include <string>
 
+#include <cudaTypedefs.h>
+
 #include "ms_dispatch.h"
+#include "ms_gemv_tc.cuh"
 #include "ms_multi.cuh"
 
 namespace msb {
@@ -32,6 +35,32 @@ bool use_tile_sweep(int ks, int64_t ld) {
   if (v && std::strcmp(v, "tile") == 0) return true;
   if (v && (std::strcmp(v, "ldg") == 0 || std::strcmp(v, "small") == 0)) return false;
   return (ks == MS_K_F16 || ks == MS_K_BF16) && ld <= 8192;
+}
+
+// f16 K through the tensor-core sweep (ms_gemv_tc.cuh): the default for
+// binary32 rows once K outgrows L2 (N >= 16384; C4: 806 vs 726 accepted
+// steps/s, profiles/r2_tc16.txt), MS_SWEEP=tc16 forces it at any N, any other
+// MS_SWEEP value selects a CUDA-core sweep
+bool use_tc16(const RhsArgs& a, int ks) {
+  if (!(ks == MS_K_F16 && a.tc16 != nullptr && a.op16 != nullptr && a.ld % (kGvKB * kGvBK) == 0)) return false;
+  const char* v = std::getenv("MS_SWEEP");
+  if (v && *v) return std::strcmp(v, "tc16") == 0;
+  return a.ld >= 16384;
+}
+
+void go_tc16(const RhsLaunch& L, const RhsArgs& a) {
+  const GvRes* r = static_cast<const GvRes*>(a.tc16);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(k_rhs_tc16<MS_K_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGvSmem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tc16 attribute: ") + cudaGetErrorString(e));
+    attr_done = true;
+  }
+  GvArgs g{r->kt, r->part, r->cnt, r->tiles, r->chunks, r->kblocks, kGvIdesc};
+  const int units = r->tiles * r->chunks;
+  const int grid = units < L.num_sms ? units : L.num_sms;
+  cudaError_t e = launch_k(k_rhs_tc16<MS_K_F16>, grid, kGvThreads, kGvSmem, L.stream, a, g);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tc16 launch: ") + cudaGetErrorString(e));
 }
 
 template <class SS, class GS, int KS>
@@ -88,6 +117,12 @@ void go(const RhsLaunch& L, const RhsArgs& a) {
   // the TMA-fed sweep wins for f32 K (7.2 vs 6.5 TB/s); with 16-bit K its
   // row copies get small and the s/c traffic per K byte doubles, and the
   // register-fed sweep stays ahead (profiles/r1_tune_tma.txt)
+  if constexpr (MODEL == MD_KUR && SPLIT && KS == MS_K_F16 && sizeof(SS) == 4 && sizeof(GS) == 4) {
+    if (use_tc16(a, KS)) {
+      go_tc16(L, a);
+      return;
+    }
+  }
   if constexpr (MODEL == MD_KUR && SPLIT && KS != MS_K_SCALAR && !(sizeof(SS) == 4 && sizeof(GS) == 8)) {
     if (use_tile_sweep(KS, a.ld)) {
       go_tile<SS, GS, KS>(L, a);
@@ -264,6 +299,42 @@ void launch_rhs_fast(const RhsLaunch& L, const RhsArgs& a) {
     case MD_CC: by_prec<MD_CC, false>(L, a); break;
     default: throw std::invalid_argument("rhs_fast: bad model");
   }
+}
+
+void* tc16_create(const void* K, int64_t ld, int rows, int ks) {
+  if (ks != MS_K_F16 || ld % (kGvKB * kGvBK) != 0 || rows < 1) return nullptr;
+  GvRes* r = new GvRes{};
+  r->tiles = (rows + kGvBM - 1) / kGvBM;
+  r->chunks = (int)((ld + kGvChunk - 1) / kGvChunk);
+  r->kblocks = (int)(ld / kGvBK);
+  const size_t ktbytes = (size_t)r->tiles * r->kblocks * kGvABytes;
+  const size_t pbytes = sizeof(float2) * (size_t)r->tiles * r->chunks * kGvBM;
+  if (cudaMalloc(&r->kt, ktbytes) != cudaSuccess || cudaMalloc(&r->part, pbytes) != cudaSuccess ||
+      cudaMalloc(&r->cnt, sizeof(int) * r->tiles) != cudaSuccess ||
+      cudaMemset(r->cnt, 0, sizeof(int) * r->tiles) != cudaSuccess) {
+    cudaGetLastError();
+    tc16_destroy(r);
+    return nullptr;  // no room for the tile images: the CUDA-core sweeps serve f16 K
+  }
+  tc16_refresh(r, K, ld, rows, nullptr);
+  return r;
+}
+
+void tc16_refresh(void* p, const void* K, int64_t ld, int rows, cudaStream_t st) {
+  GvRes* r = static_cast<GvRes*>(p);
+  if (!r) return;
+  k_tile_k16<<<1024, 256, 0, st>>>(static_cast<const __half*>(K), r->kt, ld, rows, r->tiles, r->kblocks);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("tc16 tile images: ") + cudaGetErrorString(e));
+}
+
+void tc16_destroy(void* p) {
+  GvRes* r = static_cast<GvRes*>(p);
+  if (!r) return;
+  if (r->kt) cudaFree(r->kt);
+  if (r->part) cudaFree(r->part);
+  if (r->cnt) cudaFree(r->cnt);
+  delete r;
 }
 
 MS_DEFINE_LAUNCH_READER(launches_tu_fast)

@@ -1,0 +1,45 @@
+// ms_tcgen05.cuh — the tcgen05 / mbarrier helpers shared by the tensor-core
+// kernels (the ensemble contraction ms_gemm_tc.cuh, the 16-bit-K sweep
+// ms_gemv_tc.cuh).
+#pragma once
+
+#include "ms_kernels.cuh"
+
+namespace msb {
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// bounded mbarrier wait: a pipeline bug traps (kernel error, process exits)
+// instead of hanging the GPU
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if ((it & 1023) == 0) {
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 2000000000ull) __trap();
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t umma_smem_desc(uint32_t smem_addr) {
+  // K-major, SWIZZLE_128B canonical layout: 8-row x 128-byte atoms,
+  // stride between 8-row groups (SBO) 1024 B, LBO unused (1), version 1.
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                    // LBO (16 B, ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // SBO
+  d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                    // layout: SWIZZLE_128B
+  return d;
+}
+
+}  // namespace msb

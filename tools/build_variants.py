@@ -147,6 +147,17 @@ VARIANTS = {
     "tcv_noepi": ("ms_batch.cu", {"MS_T2_NOEPI": 1}),
     # round 2: epilogue records staged in shared memory (default) vs per-thread loads
     "tcs_new": ("ms_batch.cu", {}),
+    # C4 f32 TMA sweep: the first rows of every CTA's range kept in L2 (evict-last) across evaluations
+    # f16 tensor-core sweep (MS_SWEEP=tc16): accumulator batch, TMEM groups, ring depth, no-TMEM-load timing
+    "gv_kb4": ("ms_rhs_fast.cu", {}),
+    "gv_kb2": ("ms_rhs_fast.cu", {"MS_GV_KB": 2}),
+    "gv_kb1": ("ms_rhs_fast.cu", {"MS_GV_KB": 1}),
+    "gv_kb4_g4": ("ms_rhs_fast.cu", {"MS_GV_GROUPS": 4}),
+    "gv_kb4_exp1": ("ms_rhs_fast.cu", {"MS_GV_EXP": 1}),
+    "keep0": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 0}),
+    "keep2": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 2}),
+    "keep4": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 4}),
+    "keep6": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 6}),
     "tcs_old": ("ms_batch.cu", {"MS_T2_SREC": 0, "MS_T2_END_RELAXED": 0, "MS_TC_PACKED": 2}),
     "tcs_noepi": ("ms_batch.cu", {"MS_T2_NOEPI": 1, "MS_T2_SREC": 0}),
     "tcs_p3_nosrec": ("ms_batch.cu", {"MS_T2_SREC": 0}),

@@ -7,7 +7,7 @@ export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
 ks=${1:-f32}
 MS_LOOP=host python tools/profile_c4.py --kdtype $ks --iters 1 --attempts 1 > gpurun_out/prof_plain_$ks.log 2>&1 || exit 1
-MS_LOOP=host ncu --set full --import-source on --clock-control none -k regex:"k_rhs_(tma|fast)" -c 8 -f \
+MS_LOOP=host ncu --set full --import-source on --clock-control none -k regex:"k_rhs_(tma|fast|tc16)" -c 8 -f \
   -o /tmp/c4_sweeps_$ks python tools/profile_c4.py --kdtype $ks --iters 1 --attempts 1 > gpurun_out/ncu_full_$ks.log 2>&1
 ncu -i /tmp/c4_sweeps_$ks.ncu-rep --page raw --csv > gpurun_out/ncu_c4_${ks}_raw.csv 2>/dev/null
 ncu -i /tmp/c4_sweeps_$ks.ncu-rep --page details > gpurun_out/ncu_c4_${ks}_details.txt 2>/dev/null
