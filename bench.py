@@ -37,12 +37,13 @@ UNIT = "accepted_steps/s"
 DATA = "synthetic (seeded SplitMix64: omega~N(0,1), K~U(0,2), theta0~U(0,2pi))"
 
 
-def peaks():
+def peaks(key="hbm_gbs", fallback=6650.0):
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        if key in d:
+            return float(d[key]), "measured"
+    return fallback, "fallback"
 
 
 class ClockSampler:
@@ -267,6 +268,108 @@ def project(per_eval_s, counts):
     if not counts:
         return None
     return counts["n_accepted"] / (per_eval_s * counts["rhs_evals"])
+
+
+def _c5_cpu_worker(item):
+    """One host process, one oracle thread: trajectories [b0, b1) of the C5
+    ensemble solved one after another (the reference's campaign model: B
+    independent single-threaded solves over a pool, harness.cpp:424-456),
+    inputs from the oracle's own SplitMix64 (rng.hpp:13-52)."""
+    b0, b1, n, tf = item
+    sys.path.insert(0, str(ROOT / "tests"))
+    import _oracle as O
+    from paper_2605_23727_b200.configs import SSS_D, TWO_PI
+    from paper_2605_23727_b200.solver import SolverConfig
+    from paper_2605_23727_b200.systems import SystemSpec
+    O.set_threads(1)
+    seed = 4
+    spec = SystemSpec("kuramoto", n, k_storage="bf16", omega=np.zeros(n), k_uniform=(seed, 2, 0.0, 2.0))
+    cfg = SolverConfig(rel_tol=1e-6, abs_tol=1e-9, time_limits_enabled=False)
+    orc = O.OracleSystem(spec)
+    orc.set_op_round(3)  # MS_K_BF16: the tensor-core operand rounding (hi + lo bf16)
+    omega = O.rng_normal(seed, 0, b1 * n).reshape(b1, n)
+    x0 = O.rng_uniform(seed, 1, b1 * n, 0.0, TWO_PI).reshape(b1, n)
+    acc = 0
+    t = time.perf_counter()
+    for b in range(b0, b1):
+        orc.set_omega(omega[b])
+        acc += O.solve(orc, x0[b], 0.0, tf, SSS_D, cfg, cap=1, snapshot_capacity=0).n_accepted
+    return acc, time.perf_counter() - t
+
+
+def c5_line(steps, cpu):
+    """BASELINE.json configs[4] (C5) on this GPU: B=1024 trajectories x N=2048
+    sharing a bf16 K, t in [0,20], rtol 1e-6: trajectory accepted steps/s of
+    the whole lock-step solve (device time), the contraction's tensor-pipe
+    rate, and the reference model on the host cores (one single-threaded
+    oracle solve per core over a sample of trajectories)."""
+    import ctypes as C
+    from paper_2605_23727_b200 import _abi
+    from paper_2605_23727_b200.batch import DeviceBatch
+    from paper_2605_23727_b200.configs import config5_batch
+    from paper_2605_23727_b200.precision import SSS
+    from paper_2605_23727_b200.systems import DeviceSystem
+    w = config5_batch()
+    dev = DeviceSystem(w.spec)
+    bat = DeviceBatch(dev, w.omega, tensor_cores=True)
+    B, n = w.omega.shape
+    rhs, prep = C.c_double(), C.c_double()
+    x = np.ascontiguousarray(w.x0)
+    _abi.check(_abi.lib().ms_batch_profile_rhs(bat._h, _abi.dptr(x), SSS.c(), 20, C.byref(rhs), C.byref(prep)), "prof")
+    bat.solve(w.x0, w.t0, w.tf, w.policy, w.cfg)  # graph instantiation
+    res = [bat.solve(w.x0, w.t0, w.tf, w.policy, w.cfg) for _ in range(steps)]
+    ms = sum(r.device_ms for r in res)
+    acc = sum(int(r.n_accepted.sum()) for r in res)
+    flops = 2.0 * n * n * 2 * B
+    peak, _ = peaks("bf16_tflops", 1682.1)
+    tf = flops / (rhs.value * 1e-3) / 1e12
+    out = {"workload": "C5 batched Kuramoto B=1024 N=2048 K bf16 (BASELINE configs[4]), t in [0,20], rtol 1e-6",
+           "value": acc / (ms / 1e3), "unit": "trajectory_accepted_steps/s", "ms_per_solve": ms / steps,
+           "lockstep_attempts": res[0].attempts, "accepted_per_traj_mean": float(res[0].n_accepted.mean()),
+           "contraction": {"kernel": "k_tc_gemm2 (tcgen05.mma.cta_group::2 kind::f16, 256 x 512 pair tiles)",
+                           "ms": rhs.value, "TFLOPs_algorithmic": tf, "peak_bf16_TFLOPs": peak, "frac": tf / peak}}
+    bat.close()
+    dev.close()
+    if cpu:
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+        cores = os.cpu_count() or 1
+        k = min(cores, 16)
+        t = time.perf_counter()
+        with ProcessPoolExecutor(k, mp_context=mp.get_context("spawn")) as ex:
+            parts = list(ex.map(_c5_cpu_worker, [(b, b + 1, n, w.tf) for b in range(k)]))
+        wall = time.perf_counter() - t
+        cacc = sum(p[0] for p in parts)
+        out["cpu_baseline"] = {"value": cacc / wall, "unit": "trajectory_accepted_steps/s", "cores": k, "kind": "port",
+                               "sample": f"trajectories 0..{k - 1} of the ensemble, whole t in [0,20] each, one "
+                                         f"single-threaded oracle solve per process ({cacc} accepted steps in "
+                                         f"{wall:.1f} s wall incl. process start and K generation)"}
+    return out
+
+
+def c4_f16_line(steps, seed):
+    """C4 with K stored f16 (BASELINE.json configs[3] names fp32 and fp16 K):
+    accepted steps/s over whole device-resident solves with the default f16
+    sweep (the tensor-core k_rhs_tc16 at this N)."""
+    import torch
+    from paper_2605_23727_b200 import solver as S
+    from paper_2605_23727_b200.configs import config4_kuramoto
+    from paper_2605_23727_b200.systems import DeviceSystem
+    w = config4_kuramoto(seed=seed, k_storage="f16")
+    dev = DeviceSystem(w.spec)
+    x0_d = torch.from_numpy(w.x0).to("cuda")
+    xf_d = torch.empty_like(x0_d)
+    st = torch.cuda.Stream()
+    one = lambda: S.solve_device(dev, x0_d.data_ptr(), xf_d.data_ptr(), w.t0, w.tf, w.policy, w.cfg,  # noqa: E731
+                                 stream=st.cuda_stream, log_capacity=0)
+    one()
+    res = [one() for _ in range(steps)]
+    ms = sum(r.device_ms for r in res)
+    dev.close()
+    return {"workload": "C4 Kuramoto N=32768 K f16", "value": sum(r.n_accepted for r in res) / (ms / 1e3),
+            "unit": UNIT, "ms_per_solve": ms / steps, "accepted_steps_per_solve": res[0].n_accepted,
+            "rejected_per_solve": res[0].n_failed,
+            "sweep": "k_rhs_tc16" if os.environ.get("MS_SWEEP", "tc16") == "tc16" else os.environ.get("MS_SWEEP")}
 
 
 def run_reference(args):
@@ -494,6 +597,14 @@ def run_ours(args):
                                           "in the reference eval_core order (per-pair sinf, systems.cpp:30-64) "
                                           f"restated in oracle/, OpenMP rows over {thr} threads"}
     line["clocks"] = clk.summary()
+    if rank == 0 and ws == 1 and not args.no_also and args.n == 32768:
+        # the other stated configurations this GPU runs, measured after the
+        # headline (informative; not part of the timed region above)
+        also = {}
+        if args.kdtype == "f32":
+            also["c4_f16"] = c4_f16_line(2, args.seed)
+        also["c5"] = c5_line(2, not args.no_cpu_baseline)
+        line["also"] = also
     if rank == 0:
         print(json.dumps(line), flush=True)
     if torch.distributed.is_initialized():
@@ -518,6 +629,7 @@ def main():
     ap.add_argument("--no-accuracy", action="store_true")
     ap.add_argument("--shard", action="store_true", help="use the row-sharded loop even on 1 GPU")
     ap.add_argument("--check-every", type=int, default=8)
+    ap.add_argument("--no-also", action="store_true", help="skip the C4-f16 and C5 lines after the headline")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
