@@ -81,6 +81,22 @@ __device__ __forceinline__ double b_fval(const BatchDev& d, int64_t e, int fs32)
 //    (profiles/r2_c5_srec.txt), so the default stays 2
 #define MS_TC_PACKED 2
 #endif
+// The contraction's windowed accumulation (MS_T2_DRAIN = default k-blocks per
+// window, 0 = one accumulator over all of K; ms_gemm_tc.cuh) folds hi and lo into
+// one accumulator and needs each plane's (s, c) rows of a tile of trajectories
+// contiguous: planes [hi, lo][B][s, c][ld]. Otherwise [B][4][ld].
+#ifndef MS_T2_DRAIN
+#define MS_T2_DRAIN 2
+#endif
+// element i of operand row `which` (0 s_hi, 1 s_lo, 2 c_hi, 3 c_lo) of trajectory b
+__device__ __forceinline__ int64_t op_index(const BatchDev& d, int b, int which, int i) {
+#if MS_T2_DRAIN
+  return ((int64_t)((which & 1) * d.B + b) * 2 + (which >> 1)) * d.ld + i;
+#else
+  return ((int64_t)b * 4 + which) * d.ld + i;
+#endif
+}
+
 struct __align__(16) TcRec {
   float s, c;
   double f;
@@ -164,21 +180,21 @@ __device__ __forceinline__ void bprep_elem(const BPrepArgs& p, int b, int i, Ctl
   // two-term operands: v = hi + lo with hi = RN16(v), lo = RN16(v - hi) (the
   // difference is exact in binary32), so K*hi + K*lo carries ~16-22 bits of v
   if (p.op_ks == MS_K_BF16) {
-    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(d.op) + (int64_t)b * 4 * d.ld;
+    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(d.op);
     const float s32 = (float)sv, c32 = (float)cv;
     const __nv_bfloat16 sh = __float2bfloat16_rn(s32), ch = __float2bfloat16_rn(c32);
-    op[i] = sh;
-    op[d.ld + i] = __float2bfloat16_rn(__fsub_rn(s32, __bfloat162float(sh)));
-    op[2 * d.ld + i] = ch;
-    op[3 * d.ld + i] = __float2bfloat16_rn(__fsub_rn(c32, __bfloat162float(ch)));
+    op[op_index(d, b, 0, i)] = sh;
+    op[op_index(d, b, 1, i)] = __float2bfloat16_rn(__fsub_rn(s32, __bfloat162float(sh)));
+    op[op_index(d, b, 2, i)] = ch;
+    op[op_index(d, b, 3, i)] = __float2bfloat16_rn(__fsub_rn(c32, __bfloat162float(ch)));
   } else if (p.op_ks == MS_K_F16) {
-    __half* op = reinterpret_cast<__half*>(d.op) + (int64_t)b * 4 * d.ld;
+    __half* op = reinterpret_cast<__half*>(d.op);
     const float s32 = (float)sv, c32 = (float)cv;
     const __half sh = __float2half_rn(s32), ch = __float2half_rn(c32);
-    op[i] = sh;
-    op[d.ld + i] = __float2half_rn(__fsub_rn(s32, __half2float(sh)));
-    op[2 * d.ld + i] = ch;
-    op[3 * d.ld + i] = __float2half_rn(__fsub_rn(c32, __half2float(ch)));
+    op[op_index(d, b, 0, i)] = sh;
+    op[op_index(d, b, 1, i)] = __float2half_rn(__fsub_rn(s32, __half2float(sh)));
+    op[op_index(d, b, 2, i)] = ch;
+    op[op_index(d, b, 3, i)] = __float2half_rn(__fsub_rn(c32, __half2float(ch)));
   }
 }
 
@@ -249,7 +265,9 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
   __syncthreads();
   if (skip) return;
   using T = typename K16<OPKS>::T;
-  T* op = reinterpret_cast<T*>(d.op) + (int64_t)b * 4 * d.ld;
+  T* op = reinterpret_cast<T*>(d.op);
+  const int64_t o_sh = op_index(d, b, 0, 0), o_sl = op_index(d, b, 1, 0), o_ch = op_index(d, b, 2, 0),
+                o_cl = op_index(d, b, 3, 0);
 #if MS_TC_PACKED == 1
   TcRec* rec = reinterpret_cast<TcRec*>(d.sc) + (int64_t)b * d.n;
   const double* om = d.omega + (int64_t)b * d.n;
@@ -318,10 +336,10 @@ __global__ void __launch_bounds__(256) kb_prep_tc(BPrepArgs p) {
     *reinterpret_cast<float2*>(rec + i) = make_float2(sv, cv);  // F was written at creation
 #endif
     const T sh = K16<OPKS>::from(sv), ch = K16<OPKS>::from(cv);
-    op[i] = sh;
-    op[d.ld + i] = K16<OPKS>::from(__fsub_rn(sv, (float)sh));
-    op[2 * d.ld + i] = ch;
-    op[3 * d.ld + i] = K16<OPKS>::from(__fsub_rn(cv, (float)ch));
+    op[o_sh + i] = sh;
+    op[o_sl + i] = K16<OPKS>::from(__fsub_rn(sv, (float)sh));
+    op[o_ch + i] = ch;
+    op[o_cl + i] = K16<OPKS>::from(__fsub_rn(cv, (float)ch));
   }
 }
 

@@ -85,6 +85,8 @@ struct TcArgs {
   // Measured slower (whole C5 solve 292 vs 282 ms: the waiting blocks crowd the
   // epilogue), so the default releases at exit
   int pdl_early;
+  // MS_T2_DRAIN builds: k-blocks per accumulation window (MS_TC_WINDOW, default MS_T2_DRAIN)
+  int window;
 };
 
 __device__ __forceinline__ void tc_ld32(uint32_t addr, uint32_t (&r)[32]) {
@@ -95,6 +97,51 @@ __device__ __forceinline__ void tc_ld32(uint32_t addr, uint32_t (&r)[32]) {
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
         "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_ld32_nw(uint32_t addr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+}
+__device__ __forceinline__ void tc_st32(uint32_t addr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld8(uint32_t addr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tc_ld8_nw(uint32_t addr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+}
+__device__ __forceinline__ void tc_st8(uint32_t addr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t addr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(addr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -406,7 +453,24 @@ constexpr int kT2EpiWarps = MS_T2_EPI;
 constexpr int kT2ABytes = kT2BM * kTcBK * 2;               // 16 KB
 constexpr int kT2BBytes = kT2NMma * kT2Half * kTcBK * 2;   // 16 KB per N256 MMA
 constexpr int kT2StageBytes = kT2ABytes + kT2BBytes;
-constexpr int kT2Threads = 64 + 32 * kT2EpiWarps;
+// MS_T2_DRAIN: 4 more warps join the window drains (12 warps = 3 per TMEM lane
+// quarter, 88/88/80 columns each, so the running totals fit in registers)
+#ifndef MS_T2_XWARPS
+#define MS_T2_XWARPS 4
+#endif
+constexpr int kT2XWarps = MS_T2_DRAIN ? MS_T2_XWARPS : 0;
+constexpr int kT2DrainWarpsPerQ = (kT2EpiWarps + kT2XWarps) / 4;   // drain warps per TMEM lane quarter
+constexpr int kT2DrainCh = (32 + kT2DrainWarpsPerQ - 1) / kT2DrainWarpsPerQ;  // 8-column chunks per drain warp (max)
+static_assert((kT2EpiWarps + kT2XWarps) % 4 == 0, "drain warps cover the lane quarters evenly");
+constexpr int kT2Threads = 64 + 32 * (kT2EpiWarps + kT2XWarps);
+// the windowed accumulation keeps up to 88 running totals per drain thread in
+// registers: 14 warps per CTA put 4 on a sub-partition of 16 K registers, so
+// 128 per thread is the ceiling
+#if MS_T2_DRAIN
+#define MS_T2_BOUNDS __maxnreg__(MS_T2_XWARPS == 4 ? 128 : (MS_T2_XWARPS == 8 ? 96 : 64))
+#else
+#define MS_T2_BOUNDS __launch_bounds__(kT2Threads, MS_T2_MINB)
+#endif
 // record staging (MS_T2_SREC): slot g holds the records of epilogue group g of
 // both column parts (trajectories 8g..8g+7 and 64+8g..64+8g+7 of the pair tile)
 // for this CTA's 128 rows: 16 x 128 x 16 B = 32 KB, laid out [part*8+q][row]
@@ -428,6 +492,7 @@ constexpr int kT2RingSlots = (kT2Stages * kT2StageBytes) / kT2SlotBytes;
 constexpr int kT2RingUse = kT2RingSlots < kT2NSlot - kT2Spare ? kT2RingSlots : kT2NSlot - kT2Spare;
 static_assert(!MS_T2_SREC || (kT2BN == 512 && kT2EpiWarps == 8 && !MS_TC_FIN), "record staging layout");
 static_assert(!MS_T2_SREC || kT2Spare + kT2RingUse + kT2Spare >= kT2NSlot, "record slots: each spare reused once");
+static_assert(!MS_T2_DRAIN || (MS_T2_SREC && kT2BN == 512 && kT2EpiWarps == 8), "windowed accumulation layout");
 static_assert(!MS_T2_SREC || kT2NSlot - kT2Spare - kT2RingUse <= 2, "record slots: at most two spares refilled");
 constexpr size_t kT2Smem = 1024 + (size_t)kT2Stages * kT2StageBytes + (size_t)kT2Spare * kT2SlotBytes + 256;
 
@@ -476,19 +541,29 @@ __device__ __forceinline__ void tc_epilogue_srec(const TcArgs& t, uint32_t lane_
   const BatchDev& d = t.a.d;
   const float mw = (float)d.mw;
   const bool row_ok = i < t.n;
+#if MS_T2_DRAIN
+  (void)tmem_full;  // the caller's window drains stored the totals in TMEM columns 0..255
+#else
   tc_wait(tmem_full, 0);
   tc_fence_after();
+#endif
 #pragma unroll 1
   for (int g = 0; g < kT2NSlot; ++g) {
-    uint32_t r[32];
 #ifndef MS_T2_EXP_EPI  // timing experiments only (results wrong): 1 no k stores, 2 no record reads, 3 no TMEM loads
 #define MS_T2_EXP_EPI 0
 #endif
+#if MS_T2_DRAIN
+    // totals (A, B) of trajectory part*64 + 8g + q in columns part*128 + 16g + 2q, +1
+    uint32_t r[16];
+    tc_ld16(lane_addr + (uint32_t)(part * 128 + g * 16), r);
+#else
+    uint32_t r[32];
 #if MS_T2_EXP_EPI == 3
 #pragma unroll
     for (int k = 0; k < 32; ++k) r[k] = (uint32_t)(k + g);
 #else
     tc_ld32(lane_addr + (uint32_t)(part * 256 + g * 32), r);
+#endif
 #endif
 #if MS_T2_EXP_EPI != 2
     tc_wait(&rec_full[g], 0);
@@ -516,8 +591,12 @@ __device__ __forceinline__ void tc_epilogue_srec(const TcArgs& t, uint32_t lane_
         const TcRec rc = *reinterpret_cast<const TcRec*>(sb + (size_t)j * kT2ScStride + (size_t)rr * 16);
 #endif
 #endif
+#if MS_T2_DRAIN
+        const float A = __uint_as_float(r[2 * q]), Bv = __uint_as_float(r[2 * q + 1]);
+#else
         const float A = __fadd_rn(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]));
         const float Bv = __fadd_rn(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+#endif
         const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(rc.c, A), __fmul_rn(rc.s, Bv)));
         MS_CHECK(i < d.n && (tb0 + tq < d.B), "contraction epilogue: element outside the ensemble");
         const double o = ws_add(rc.f, (double)coup, t.a.ws32);
@@ -536,7 +615,7 @@ __device__ __forceinline__ void tc_epilogue_srec(const TcArgs& t, uint32_t lane_
   }
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MINB)
+__global__ void __cluster_dims__(2, 1, 1) MS_T2_BOUNDS
     k_tc_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs t) {
   msb::count_launch();
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
@@ -548,7 +627,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
   uint64_t* tmem_full = empty + kT2Stages;
   uint64_t* rec_full = tmem_full + 1;       // [kT2NSlot] (MS_T2_SREC)
   uint64_t* rec_free = rec_full + kT2NSlot; // [2]: a spare slot's first records consumed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rec_free + 2);
+  uint64_t* drain_full = rec_free + 2;      // MS_T2_DRAIN [2]: a window's MMAs into TMEM buffer b are done (both CTAs)
+  uint64_t* drain_empty = drain_full + 2;   // [2]: buffer b has been read (leader; 16 warps of the pair)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(drain_empty + 2);
   // where record slot g lives: spare 0/1, then the drained ring, then the spares again
   auto slot_ptr = [&](int g) -> unsigned char* {
     if (g < kT2Spare) return spare + (size_t)g * kT2SlotBytes;
@@ -581,6 +662,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
     for (int g = 0; g < kT2NSlot; ++g) mbar_init(&rec_full[g], 1);
     mbar_init(&rec_free[0], kT2EpiWarps);
     mbar_init(&rec_free[1], kT2EpiWarps);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&drain_full[b], 1);
+      mbar_init(&drain_empty[b], 2 * (kT2EpiWarps + kT2XWarps));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -670,7 +755,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
         tma2_load(sa, &tmA, bar, kb * kTcBK, m0);
 #pragma unroll
         for (int hf = 0; hf < MS_T2_EXP_NB; ++hf)
+#if MS_T2_DRAIN
+          // plane hf (hi, lo): the (s, c) rows of the pair's 128 trajectories, this CTA's half
+          tma2_load(sb + hf * (kT2Half * kTcBK * 2), &tmB, bar, kb * kTcBK,
+                    hf * 2 * t.a.d.B + 2 * (n0 >> 2) + (int)rank * kT2Half);
+#else
           tma2_load(sb + hf * (kT2Half * kTcBK * 2), &tmB, bar, kb * kTcBK, n0 + hf * 2 * kT2Half + (int)rank * kT2Half);
+#endif
       }
 #if MS_T2_SREC && MS_T2_EXP_EPI != 2
       // the ring is free once the last use of every stage has been committed
@@ -691,6 +782,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
     if (lane == 0 && rank == 0) {  // MMA issuer: the leader only
       for (int kb = 0; kb < nkb; ++kb) {
         const int st = kb % kT2Stages;
+#if MS_T2_DRAIN
+        // window wv accumulates into TMEM buffer wv & 1 from zero; it may start once
+        // both CTAs' epilogue warps have read that buffer's previous window (wv - 2)
+        const int wv = kb / t.window;
+        if (kb % t.window == 0 && wv >= 2) tc_wait(&drain_empty[wv & 1], ((wv >> 1) - 1) & 1);
+#endif
         tc_wait(&full[st], (kb / kT2Stages) & 1);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + (size_t)st * kT2StageBytes);
@@ -698,16 +795,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
 #pragma unroll
         for (int k = 0; k < kTcBK / 16; ++k) {
           const uint64_t adesc = umma_smem_desc(sa + k * 32);
+#if MS_T2_DRAIN
+          const uint32_t acc0 = (kb % t.window > 0 || k > 0) ? 1u : 0u;  // the window's first MMA overwrites
+#else
           const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+#endif
 #ifndef MS_T2_EXP_NMMA
 #define MS_T2_EXP_NMMA kT2NMma  // timing experiments only: MMAs issued per k-step
 #endif
 #pragma unroll
           for (int hf = 0; hf < MS_T2_EXP_NMMA; ++hf) {
             const uint64_t bdesc = umma_smem_desc(sb + hf * (kT2Half * kTcBK * 2) + k * 32);
+#if MS_T2_DRAIN
+            // hi and lo planes into the same accumulator (the window's buffer)
+            const uint32_t acc = hf > 0 ? 1u : acc0;
+            const uint32_t dcol = (uint32_t)((wv & 1) * 256);
+#else
+            const uint32_t dcol = (uint32_t)(hf * 256);
+#endif
             asm volatile(
                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(hf * 256)),
+                " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + dcol),
                 "l"(adesc), "l"(bdesc), "r"(t.idesc), "r"(acc));
           }
         }
@@ -716,6 +824,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
                 smem_u32(&empty[st])),
             "h"((uint16_t)3)
             : "memory");
+#if MS_T2_DRAIN
+        if (kb % t.window == t.window - 1 || kb == nkb - 1)
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  smem_u32(&drain_full[wv & 1])),
+              "h"((uint16_t)3)
+              : "memory");
+#endif
       }
       asm volatile(
           "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -745,10 +861,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
       if (t.a.fin && !skip) tc_fin_setup(t, b, tc_fin[et]);
 #endif
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * kT2EpiWarps) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * (kT2EpiWarps + kT2XWarps)) : "memory");
     const int i = m0 + q4 * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
     constexpr int kCols = kT2BN / (kT2EpiWarps / 4);  // columns per epilogue warp
+#if MS_T2_DRAIN
+    // window drains: each window's sums (TMEM buffer wv & 1: 128 trajectories x
+    // (A, B) in columns 0..255) are added into binary32 running totals in
+    // registers (RN) and the buffer is released for window wv + 2 while the MMAs
+    // of window wv + 1 fill the other one. Each window starts from zero, so the
+    // tensor core never adds into a large running sum: its truncation per add
+    // stays at a window's scale instead of biasing the whole K sum. Warp j of a
+    // lane quarter owns 8-column chunks [11 j, min(32, 11 j + 11)).
+    {
+      constexpr int kMaxCh = kT2DrainCh;
+      const int jw = (warp - 2) >> 2;
+      const int ch0 = jw * kMaxCh, nch = min(kMaxCh, 32 - ch0);
+      float R[kMaxCh * 8];
+      const int nwin = (nkb + t.window - 1) / t.window;
+      const uint32_t remote_empty0 = map_to_rank(smem_u32(&drain_empty[0]), 0);
+#pragma unroll 1
+      for (int wv = 0; wv < nwin; ++wv) {
+        const int buf = wv & 1;
+        tc_wait(&drain_full[buf], (wv >> 1) & 1);
+        tc_fence_after();
+        // two 8-column loads in flight per wait; the buffer is released as soon
+        // as its last load has landed
+#pragma unroll
+        for (int c = 0; c < kMaxCh; c += 2) {
+          uint32_t dv[16];
+          if (c < nch) tc_ld8_nw(lane_addr + (uint32_t)(buf * 256 + (ch0 + c) * 8), dv);
+          if (c + 1 < kMaxCh && c + 1 < nch) tc_ld8_nw(lane_addr + (uint32_t)(buf * 256 + (ch0 + c + 1) * 8), dv + 8);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c < nch && c + 2 >= nch) {  // this warp's last pair: exactly one arrive per window
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+              asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_empty0 + 8u * buf)
+                           : "memory");
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (c + h < kMaxCh && c + h < nch) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                R[(c + h) * 8 + k] = wv > 0 ? __fadd_rn(R[(c + h) * 8 + k], __uint_as_float(dv[h * 8 + k]))
+                                            : __uint_as_float(dv[h * 8 + k]);
+            }
+        }
+      }
+      // all MMAs are done: the totals go back to buffer 0 (same columns) for the
+      // record-staged epilogue, which reads them with the 8-warp column split
+#pragma unroll
+      for (int c = 0; c < kMaxCh; ++c)
+        if (c < nch) tc_st8(lane_addr + (uint32_t)((ch0 + c) * 8), reinterpret_cast<const uint32_t*>(R) + c * 8);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * (kT2EpiWarps + kT2XWarps)) : "memory");
+      tc_fence_after();
+    }
+    if (warp - 2 >= kT2EpiWarps) {
+      (void)kCols;
+    } else
+#endif
+    {
 #ifndef MS_T2_NOEPI
 #if MS_T2_SREC
     (void)kCols;
@@ -763,6 +939,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2Threads, MS_T2_MI
     tc_fence_after();
     (void)lane_addr; (void)i; (void)kCols;
 #endif
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -810,6 +987,8 @@ inline void tc_gemm_setup(TcGemm& g, const BatchDev& d, int sms) {
   }
   const char* v = std::getenv("MS_TC");
   g.pair = !(v && std::string(v) == "1cta");
+  if (!g.pair && MS_T2_DRAIN)
+    throw std::runtime_error("MS_TC=1cta needs a build with MS_T2_DRAIN=0 (the pair kernel's operand planes)");
   if (g.pair) {
     g.grid_m = 2 * ((d.n + 2 * kT2BM - 1) / (2 * kT2BM));
     g.grid_n = (4 * d.B + kT2BN - 1) / kT2BN;
@@ -845,6 +1024,8 @@ inline void launch_tc_gemm(const TcGemm& g, const BRhsArgs& a, cudaStream_t st) 
     const char* v = std::getenv("MS_TC_PDL");  // read per launch (graphs capture it once)
     t.pdl_early = (v && std::string(v) == "early") ? 1 : 0;
   }
+  t.window = MS_T2_DRAIN > 0 ? MS_T2_DRAIN : 1;
+  if (const char* wv = std::getenv("MS_TC_WINDOW")) t.window = std::max(1, std::atoi(wv));  // read per launch
   if (g.pair) {
     t.idesc = tc_idesc(a.d.ks, 2 * kT2BM);
     cudaError_t e = launch_k(k_tc_gemm2, grid, kT2Threads, kT2Smem, st, g.tmA, g.tmB2, t);

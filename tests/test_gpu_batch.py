@@ -126,7 +126,12 @@ def test_batch_solve_vs_oracle(gpu, tc):
         tot["att"] += att
         assert res.t_reached[b] == o.t_reached
         scale = np.maximum(np.abs(o.final_state), 1e-3)
-        assert np.all(np.abs(res.final_state[b] - o.final_state) <= 1e-5 * scale), b
+        # the tensor core sums each window of the contraction in its own order
+        # (ms_gemm_tc.cuh, MS_T2_DRAIN), not the oracle's sequential one; the
+        # full-size ensemble's accuracy is gated against DP5(4) in
+        # tests/test_gpu_golden_solves.py
+        tol = 3e-5 if tc else 1e-5
+        assert np.all(np.abs(res.final_state[b] - o.final_state) <= tol * scale), b
         # evaluation budget of the reference loop: 2 (initial_step) + 1 (cold k1)
         # + 3 per accepted + 4 per rejected attempt (solver.cpp:255-306)
         assert res.rhs_evals[b] == 3 + 3 * res.n_accepted[b] + 4 * res.n_failed[b]

@@ -24,6 +24,7 @@ fewer rejections). There the counts gate runs the device in the ordered mode
 the fast mode is held to accuracy: its global error against the tight
 binary64 DP5(4) run no larger than the oracle's (x1.5 + 1e-7).
 """
+import copy
 from types import SimpleNamespace
 
 import numpy as np
@@ -147,13 +148,36 @@ def test_c5_full_ensemble_vs_oracle(gpu):
     assert np.all(np.abs(acc - oacc) <= np.maximum(2, 0.03 * oacc))
     assert np.all(np.abs(rej - orej) <= np.maximum(4, 0.05 * att))
     assert np.array_equal(res.rhs_evals, 3 + 3 * acc + 4 * rej)
+    # sampled final states. Each trajectory's step sequence is noise-driven (its
+    # accept/reject decisions follow the rounding of the sums) and the tensor
+    # core sums each window of the contraction in its own order, so final states
+    # are held to accuracy against each trajectory's tight binary64 DP5(4) run
+    # (rel = abs = 1e-9): over the sample, the device's mean and median global
+    # error no larger than 1.5x the oracle's (its hi + lo operand rounding and
+    # sequential binary32 sums), and no trajectory worse than 8x its oracle
+    # error + 1e-6 (per trajectory the errors scatter: the exact CUDA-core
+    # path is up to 1.8x the oracle's on this sample, tools/c5_accuracy.py)
+    bat.close()
     floor = w.cfg.abs_tol / w.cfg.rel_tol
-    worst = 0.0
+    wrel = lambda a, b_: float(np.max(np.abs(a - b_) / np.maximum(np.abs(b_), floor)))  # noqa: E731
+    e_dev, e_orc, dev_orc = [], [], []
     for k, b in enumerate(d["sample"]):
         of = d["final_states"][k]
-        rel = float(np.max(np.abs(res.final_state[b] - of) / np.maximum(np.abs(of), floor)))
-        worst = max(worst, rel)
-        assert rel <= 1e-5, (int(b), rel)
-    print(f"C5 sampled final states: worst weighted deviation {worst:.3e}")
-    bat.close()
+        spec = copy.copy(w.spec)
+        spec.omega = np.ascontiguousarray(w.omega[b])
+        one = DeviceSystem(spec)
+        ref = S.dp54_reference(one, w.x0[b], w.t0, w.tf, S.SolverConfig(time_limits_enabled=False), log_capacity=1)
+        one.close()
+        assert ref.status == S.SolveStatus.Completed
+        e_dev.append(wrel(res.final_state[b], ref.final_state))
+        e_orc.append(wrel(of, ref.final_state))
+        dev_orc.append(wrel(res.final_state[b], of))
+        print(f"  trajectory {int(b)}: vs oracle {dev_orc[-1]:.3e}; global error vs DP5(4) device {e_dev[-1]:.3e}, "
+              f"oracle {e_orc[-1]:.3e}")
+    e_dev, e_orc = np.array(e_dev), np.array(e_orc)
+    print(f"C5 sampled global errors: device mean {e_dev.mean():.3e} median {np.median(e_dev):.3e}; oracle mean "
+          f"{e_orc.mean():.3e} median {np.median(e_orc):.3e}; device vs oracle states worst {max(dev_orc):.3e}")
+    assert e_dev.mean() <= 1.5 * e_orc.mean()
+    assert np.median(e_dev) <= 1.5 * np.median(e_orc)
+    assert np.all(e_dev <= 8.0 * e_orc + 1e-6)
     dev.close()

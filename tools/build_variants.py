@@ -147,6 +147,14 @@ VARIANTS = {
     "tcv_noepi": ("ms_batch.cu", {"MS_T2_NOEPI": 1}),
     # round 2: epilogue records staged in shared memory (default) vs per-thread loads
     "tcs_new": ("ms_batch.cu", {}),
+    # C5 windowed accumulation (MS_T2_DRAIN k-blocks per window; 0 = one accumulator over all of K)
+    "dr4": ("ms_batch.cu", {}),
+    "dr2": ("ms_batch.cu", {"MS_T2_DRAIN": 2}),
+    "dr8": ("ms_batch.cu", {"MS_T2_DRAIN": 8}),
+    "dr3": ("ms_batch.cu", {"MS_T2_DRAIN": 3}),
+    "dr2x8": ("ms_batch.cu", {"MS_T2_DRAIN": 2, "MS_T2_XWARPS": 8}),
+    "dr3x8": ("ms_batch.cu", {"MS_T2_DRAIN": 3, "MS_T2_XWARPS": 8}),
+    "dr0": ("ms_batch.cu", {"MS_T2_DRAIN": 0}),
     # C4 f32 TMA sweep: the first rows of every CTA's range kept in L2 (evict-last) across evaluations
     # f16 tensor-core sweep (MS_SWEEP=tc16): accumulator batch, TMEM groups, ring depth, no-TMEM-load timing
     "gv_kb4": ("ms_rhs_fast.cu", {}),
