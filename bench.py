@@ -326,7 +326,9 @@ def c5_line(steps, cpu):
     out = {"workload": "C5 batched Kuramoto B=1024 N=2048 K bf16 (BASELINE configs[4]), t in [0,20], rtol 1e-6",
            "value": acc / (ms / 1e3), "unit": "trajectory_accepted_steps/s", "ms_per_solve": ms / steps,
            "lockstep_attempts": res[0].attempts, "accepted_per_traj_mean": float(res[0].n_accepted.mean()),
-           "contraction": {"kernel": "k_tc_gemm2 (tcgen05.mma.cta_group::2 kind::f16, 256 x 512 pair tiles)",
+           "contraction": {"kernel": ("k_tc_gemm2 (tcgen05.mma.cta_group::2 kind::f16, 256-row x 128-trajectory pair "
+                                      "tiles, hi+lo bf16 operands, sums in windows of "
+                                      f"{os.environ.get('MS_TC_WINDOW', '2')} k-blocks added in binary32)"),
                            "ms": rhs.value, "TFLOPs_algorithmic": tf, "peak_bf16_TFLOPs": peak, "frac": tf / peak}}
     bat.close()
     dev.close()
