@@ -900,13 +900,20 @@ __global__ void __cluster_dims__(2, 1, 1) MS_T2_BOUNDS
               asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_empty0 + 8u * buf)
                            : "memory");
           }
+#ifndef MS_T2_EXP_DRAIN  // timing experiments only (results wrong): 1 = no adds into the totals
+#define MS_T2_EXP_DRAIN 0
+#endif
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             if (c + h < kMaxCh && c + h < nch) {
 #pragma unroll
               for (int k = 0; k < 8; ++k)
+#if MS_T2_EXP_DRAIN == 1
+                R[(c + h) * 8 + k] = __uint_as_float(dv[h * 8 + k]);
+#else
                 R[(c + h) * 8 + k] = wv > 0 ? __fadd_rn(R[(c + h) * 8 + k], __uint_as_float(dv[h * 8 + k]))
                                             : __uint_as_float(dv[h * 8 + k]);
+#endif
             }
         }
       }
