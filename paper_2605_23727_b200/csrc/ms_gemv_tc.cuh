@@ -200,6 +200,8 @@ __global__ void __launch_bounds__(kGvThreads, 1)
         const int c0 = ch * kGvChunk + kb * kGvBK;
         if (lane == 0) mbar_expect_tx(&full[st], kGvKB * (kGvABytes + 512));
         __syncwarp();
+        MS_CHECK(tile < g.tiles && (c0 / kGvBK) + kGvKB <= g.kblocks && (c0 % kGvBK) == 0,
+                 "tc16 sweep: tile image outside the handle's K");
         if (lane < kGvKB)  // one contiguous 16 KB tile image per k-block
           bulk_g2s_hint(sa + lane * kGvABytes,
                         g.kt + ((int64_t)tile * g.kblocks + (c0 / kGvBK) + lane) * kGvABytes, kGvABytes, &full[st], pol);
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
           }
         kbg += nb;
       }
+      MS_CHECK(tile < g.tiles && ch < g.chunks, "tc16 sweep: partial outside the workspace");
       float2* pt = g.part + ((int64_t)tile * g.chunks) * kGvBM;
       pt[(int64_t)ch * kGvBM + rr] = make_float2(__fadd_rn(ah, al), __fadd_rn(bh, bl));
       __threadfence();

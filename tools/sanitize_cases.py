@@ -52,6 +52,17 @@ def c2_policies():
     return out
 
 
+def c4_f16_tc16():
+    """the f16-K tensor-core sweep (k_rhs_tc16: tile images, op16 image, chunk tickets)"""
+    os.environ["MS_SWEEP"] = "tc16"
+    try:
+        w = config2_kuramoto(n=4352, rtol=1e-5, k_storage="f16")
+        r = S.solve(DeviceSystem(w.spec), w.x0, 0.0, 0.3, w.policy, w.cfg)
+    finally:
+        del os.environ["MS_SWEEP"]
+    return r.status, r.n_accepted
+
+
 def c1_fused():
     w = config1_lco(n=256)
     r = S.solve(DeviceSystem(w.spec), w.x0, 0.0, 0.5, w.policy, w.cfg)
@@ -123,7 +134,7 @@ def sharded_one_rank():
     return r.status, r.n_accepted
 
 
-CASES = {f.__name__: f for f in (c2_f32, c2_f16, c2_policies, c1_fused, c3_fused, faithful, dense_snapshots,
+CASES = {f.__name__: f for f in (c2_f32, c2_f16, c4_f16_tc16, c2_policies, c1_fused, c3_fused, faithful, dense_snapshots,
                                  variants, batch_tc, batch_cuda_cores, dp54, sharded_one_rank)}
 
 if __name__ == "__main__":
