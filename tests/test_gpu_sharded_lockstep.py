@@ -138,3 +138,16 @@ def test_c4_row_shards_bitwise_equal_solve(gpu):
     w = config4_kuramoto()
     ref = _run(w, 2)
     assert ref.status == S.SolveStatus.Completed and ref.n_accepted > 1000
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("world", [2, 4])
+def test_c4_f16_tensor_core_sweep_row_shards_bitwise(gpu, world):
+    """C4 with K f16 (the tensor-core sweep k_rhs_tc16, the default at this N):
+    the row-sharded loop gives the whole-K solve bit for bit -- each row's
+    dot-product order depends only on N (rows that do not align
+    with the 128-row MMA tiles: tests/test_gpu_tc16.py). A shortened span keeps
+    the test quick."""
+    w = config4_kuramoto(k_storage="f16")
+    ref = _run(w, world, tf=2.0)
+    assert ref.status == S.SolveStatus.Completed and ref.n_accepted > 50
