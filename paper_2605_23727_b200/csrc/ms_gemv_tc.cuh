@@ -59,6 +59,9 @@ constexpr int kGvStageBytes = kGvKB * (kGvABytes + kGvBBytes);
 #define MS_GV_STAGES (12 / MS_GV_KB)
 #endif
 constexpr int kGvStages = MS_GV_STAGES;
+#ifndef MS_GV_PF
+#define MS_GV_PF 0  // stages of K tile images prefetched into L2 ahead of the ring (measured slower: profiles/r2_tc16.txt)
+#endif
 static_assert(kGvChunk % (kGvKB * kGvBK) == 0, "stages tile the chunk");
 #ifndef MS_GV_GROUPS
 #define MS_GV_GROUPS 8
@@ -186,11 +189,27 @@ __global__ void __launch_bounds__(kGvThreads, 1)
     const uint64_t pol = a.k_stream ? l2_evict_first() : l2_evict_normal();
     const unsigned char* op = static_cast<const unsigned char*>(a.op16);
     int sg = 0;  // stage counter
+    // L2 prefetch MS_GV_PF stages ahead: the DRAM reads of the tile images are in
+    // flight beyond the shared-memory ring, whose refills then come from L2
+    int pu = u0, pkb = 0;
+    auto prefetch_next = [&]() {
+      if (pu >= u1) return;
+      const int ptile = pu / g.chunks, pch = pu % g.chunks;
+      const unsigned char* src = g.kt + ((int64_t)ptile * g.kblocks + pch * (kGvChunk / kGvBK) + pkb) * kGvABytes;
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src),
+                   "r"((uint32_t)(kGvKB * kGvABytes)), "l"(pol)
+                   : "memory");
+      pkb += kGvKB;
+      if (pkb >= gv_nkb(a, pch)) { pkb = 0; ++pu; }
+    };
+    if (lane == 0)
+      for (int p = 0; p < MS_GV_PF; ++p) prefetch_next();
     for (int u = u0; u < u1; ++u) {
       const int tile = u / g.chunks, ch = u % g.chunks;
       const int nkb = gv_nkb(a, ch);
       for (int kb = 0; kb < nkb; kb += kGvKB, ++sg) {
         const int st = sg % kGvStages;
+        if (lane == 0 && MS_GV_PF > 0) prefetch_next();
         if (sg >= kGvStages) {
           if (lane == 0) tc_wait(&empty[st], ((sg / kGvStages) & 1) ^ 1);
           __syncwarp();
