@@ -102,3 +102,22 @@ def test_tc16_c4_whole_solve_vs_oracle(gpu, monkeypatch):
     assert r.flops.rhs_evals == 3 + 3 * r.n_accepted + 4 * r.n_failed
     gate(r, o, w.cfg, dev, w)
     dev.close()
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_tc16_non_finite_column_poisons_every_row_like_the_cuda_core_sweep(gpu, monkeypatch, bad):
+    """A non-finite state element (eval_core would produce non-finite rows:
+    systems.cpp:30-64; the solver then takes the non-finite branch,
+    solver.cpp:150-162): the tensor-core sweep's rows are non-finite exactly
+    where the CUDA-core sweep's are."""
+    n = 4096
+    dev = DeviceSystem(kur_spec(n))
+    x = rng_uniform(10, 1, n, 0.0, TWO_PI)
+    x[1234] = bad
+    monkeypatch.setenv("MS_SWEEP", "tc16")
+    a = dev.eval_rhs(0.0, x, SSS)
+    monkeypatch.setenv("MS_SWEEP", "ldg")
+    b = dev.eval_rhs(0.0, x, SSS)
+    assert np.array_equal(np.isfinite(a), np.isfinite(b))
+    assert not np.isfinite(a).any()
+    dev.close()
