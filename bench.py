@@ -603,9 +603,16 @@ def run_ours(args):
         # the other stated configurations this GPU runs, measured after the
         # headline (informative; not part of the timed region above)
         also = {}
-        if args.kdtype == "f32":
-            also["c4_f16"] = c4_f16_line(2, args.seed)
-        also["c5"] = c5_line(2, not args.no_cpu_baseline)
+        # an extra that fails is reported, never allowed to cost the headline line
+        try:
+            if args.kdtype == "f32":
+                also["c4_f16"] = c4_f16_line(2, args.seed)
+        except Exception as e:  # noqa: BLE001
+            also["c4_f16"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        try:
+            also["c5"] = c5_line(2, not args.no_cpu_baseline)
+        except Exception as e:  # noqa: BLE001
+            also["c5"] = {"error": f"{type(e).__name__}: {e}"[:300]}
         line["also"] = also
     if rank == 0:
         print(json.dumps(line), flush=True)
