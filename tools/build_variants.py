@@ -156,6 +156,8 @@ VARIANTS = {
     "dr3x8": ("ms_batch.cu", {"MS_T2_DRAIN": 3, "MS_T2_XWARPS": 8}),
     "dr0": ("ms_batch.cu", {"MS_T2_DRAIN": 0}),
     "drx_noadd": ("ms_batch.cu", {"MS_T2_EXP_DRAIN": 1}),
+    "rege1": ("ms_batch.cu", {}),
+    "rege0": ("ms_batch.cu", {"MS_T2_REGEPI": 0}),
     # C4 f32 TMA sweep: the first rows of every CTA's range kept in L2 (evict-last) across evaluations
     # f16 tensor-core sweep (MS_SWEEP=tc16): accumulator batch, TMEM groups, ring depth, no-TMEM-load timing
     "gv_kb4": ("ms_rhs_fast.cu", {}),
