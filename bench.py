@@ -170,7 +170,8 @@ def workload_config(n, kdtype, ws):
     return {"workload": f"C4 Kuramoto N={n} K {kdtype} (BASELINE configs[3])", "n_agents": n, "t_final": 20.0,
             "rtol": 1e-6, "atol": 1e-9, "policy": "SSS x3 rows, binary64 storage", "k_storage": kdtype,
             "l2": "K (4 GiB f32 / 2 GiB f16) > L2 (126 MB): no flush needed",
-            "parallelism": f"row-shard x{ws} (NCCL all-gather per stage)" if ws > 1 else "single GPU"}
+            "parallelism": (f"row-shard x{ws} (each stage's rows pushed into the peers' memory by the sweep, "
+                            "NCCL all-gather if the peer mappings fail)") if ws > 1 else "single GPU"}
 
 
 def dtype_label(kdtype):
@@ -450,8 +451,26 @@ def run_ours(args):
     dev = DeviceSystem(w.spec)  # K (this rank's rows) generated on the device, resident
     stream = torch.cuda.Stream()
 
+    exchange = None
     if shard:
-        solver = ShardedSolver(DeviceEngine(dev), TorchComm(), check_every=args.check_every)
+        from paper_2605_23727_b200.sharded import PushComm
+        engine = DeviceEngine(dev)
+        exchange = "push" if (ws > 1 and args.exchange == "push") else "nccl"
+        solver = ShardedSolver(engine, PushComm() if exchange == "push" else TorchComm(), check_every=args.check_every)
+        if exchange == "push":
+            # the peer mappings are made on the first solve; any rank failing
+            # there sends every rank to the NCCL all-gather
+            ok = 1
+            try:
+                solver.solve(w.x0, w.t0, min(w.tf, 0.05), w.policy, w.cfg, log_capacity=0)
+            except Exception as e:  # noqa: BLE001
+                print(f"push exchange unavailable ({type(e).__name__}: {e}); NCCL all-gather", file=sys.stderr)
+                ok = 0
+            t = torch.tensor([ok], device=f"cuda:{local}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+            if int(t.item()) == 0:
+                exchange = "nccl (push setup failed)"
+                solver = ShardedSolver(engine, TorchComm(), check_every=args.check_every)
 
         def one():
             return solver.solve(w.x0, w.t0, w.tf, w.policy, w.cfg, log_capacity=0)
@@ -588,6 +607,7 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,
                 "d2h_bytes_per_step": n * 8 + log_bytes},
         "gpu_launches": gpu_launches,
+        "exchange": exchange,
         "accuracy": err,
     }
     if rank == 0 and not args.no_cpu_baseline and ws == 1:
@@ -639,6 +659,8 @@ def main():
     ap.add_argument("--shard", action="store_true", help="use the row-sharded loop even on 1 GPU")
     ap.add_argument("--check-every", type=int, default=8)
     ap.add_argument("--no-also", action="store_true", help="skip the C4-f16 and C5 lines after the headline")
+    ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
+                    help="row-sharded runs (N>1): rows pushed into peer memory by the sweeps, or NCCL all-gather")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -310,6 +310,28 @@ int ms_loop_run_segment(ms_system_t sys, int list, int index, void* stream, ms_e
 int ms_loop_done(ms_system_t sys, void* stream, int* done);
 int ms_loop_end(ms_system_t sys, ms_solve_result* res, int final_on_device, void* stream);
 
+/* Push exchange (no reference counterpart; replaces the all-gather of the
+ * row-sharded loop). Each rank's sweeps store their output rows into their own
+ * workspace AND at the same offset into every peer's workspace (peer memory:
+ * NVLink P2P or CUDA IPC mappings), so the exchange rides on the sweep's own
+ * stores. Every segment then ends with a release-store of the rank's epoch into
+ * each peer's mailbox (ms_loop_run_segment returns exch->needed = 0), and the
+ * caller runs ms_loop_push_wait before the next segment (an acquire spin until
+ * every peer's slot reaches the epoch; a peer missing for 20 s traps).
+ * Sequence per solve: ms_loop_begin; ms_loop_push_info (this rank's workspace
+ * base and mailbox, to export); exchange them (ms_ipc_export / ms_ipc_import
+ * across processes); ms_loop_push_setup on every rank; synchronize the ranks;
+ * then the segments. The workspace must not move afterwards (same step-log
+ * capacity on every begin). world <= 8. */
+int ms_loop_push_info(ms_system_t sys, void** ws_base, size_t* ws_bytes, void** mailbox);
+int ms_loop_push_setup(ms_system_t sys, int world, int rank, void* const* peer_ws /* [world] */,
+                       void* const* peer_mailbox /* [world] */);
+int ms_loop_push_wait(ms_system_t sys, void* stream);
+/* CUDA IPC of a device allocation's base pointer (64-byte handle) */
+int ms_ipc_export(void* dev_ptr, unsigned char* handle64);
+int ms_ipc_import(const unsigned char* handle64, void** dev_ptr);
+int ms_ipc_close(void* dev_ptr);
+
 /* ---- concurrent policy variants ------------------------
  * Up to four solves of one system from the same x0, one policy each (the
  * harness's Single/Mixed1/Mixed2/Double, harness.cpp:113-121), advanced in

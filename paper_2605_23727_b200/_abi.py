@@ -136,6 +136,13 @@ SIGNATURES = [
     ("ms_loop_run_segment", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(ExchangeC)]),
     ("ms_loop_done", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]),
     ("ms_loop_end", C.c_int, [C.c_void_p, C.POINTER(SolveResultC), C.c_int, C.c_void_p]),
+    ("ms_loop_push_info", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                                    C.POINTER(C.c_void_p)]),
+    ("ms_loop_push_setup", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    ("ms_loop_push_wait", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("ms_ipc_export", C.c_int, [C.c_void_p, C.POINTER(C.c_ubyte)]),
+    ("ms_ipc_import", C.c_int, [C.POINTER(C.c_ubyte), C.POINTER(C.c_void_p)]),
+    ("ms_ipc_close", C.c_int, [C.c_void_p]),
     ("ms_variants_create", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
     ("ms_variants_destroy", C.c_int, [C.c_void_p]),
     ("ms_variants_solve", C.c_int, [C.c_void_p, _DP, C.c_double, C.c_double, C.POINTER(Policy),

@@ -324,6 +324,16 @@ struct ms_system {
   int64_t dense_cap = -1;
   // f16-K tensor-core sweep resources (ms_gemv_tc.cuh GvRes) or null
   void* gv = nullptr;
+  // push exchange of the row-sharded loop (ms_loop_push_*): peers' workspaces
+  // and mailbox slots; mem = this handle's mailbox [8] + epoch [1]
+  struct PushState {
+    int world = 1, rank = 0, np = 0;
+    char* peer_ws[kMaxPeers] = {};
+    unsigned long long* peer_slot[kMaxPeers] = {};
+    int peer_rank[kMaxPeers] = {};
+    unsigned long long* mem = nullptr;
+    const void* ws_at_setup = nullptr;  // the workspace the peers were told about
+  } push;
   // host-driven (sharded) loop
   bool loop_active = false;
   SolvePlanStore* loop_plan = nullptr;
@@ -534,6 +544,11 @@ RhsArgs rhs_args(ms_system* s, const Bufs& B, const EvalSpec& e, const ms_stage_
   a.pk = env_is("MS_SWEEP_PK", "off") ? 0 : 1;
   a.tc16 = s->gv;
   a.op16 = B.op16;
+  if (s->push.np && s->loop_active) {
+    a.push.ws = static_cast<const char*>(s->ws_mem);
+    a.push.np = s->push.np;
+    for (int q = 0; q < s->push.np; ++q) a.push.peer[q] = s->push.peer_ws[q];
+  }
   return a;
 }
 
@@ -1078,6 +1093,18 @@ namespace {
 
 cudaStream_t pick_stream(ms_system* s, void* stream) {
   return stream ? static_cast<cudaStream_t>(stream) : s->stream;
+}
+
+PushSig push_sig(const ms_system* s) {
+  PushSig g{};
+  g.mbox = s->push.mem;
+  g.epoch = s->push.mem + 8;
+  g.np = s->push.np;
+  for (int q = 0; q < s->push.np; ++q) {
+    g.peer_slot[q] = s->push.peer_slot[q];
+    g.peer_rank[q] = s->push.peer_rank[q];
+  }
+  return g;
 }
 
 void set_exch(ms_system* s, ms_exchange* ex, double* buf) {
@@ -1795,6 +1822,7 @@ int ms_system_destroy(ms_system_t s) {
     for (void* p : s->dev_arrays) cudaFree(p);
     if (s->K) cudaFree(s->K);
     tc16_destroy(s->gv);
+    if (s->push.mem) cudaFree(s->push.mem);
     if (s->ws_mem) cudaFree(s->ws_mem);
     if (s->snap) cudaFree(s->snap);
     if (s->dense) cudaFree(s->dense);
@@ -2109,7 +2137,96 @@ int ms_loop_run_segment(ms_system_t s, int list, int index, void* stream, ms_exc
     if (list != 0 && list != 1) throw InvalidArg("loop_run_segment: list is 0 or 1");
     if (index < 0 || index >= loop_segments(s->loop_plan->P, list)) throw InvalidArg("loop_run_segment: bad index");
     set_device(s);
+    if (s->push.np && s->push.ws_at_setup != s->ws_mem)
+      throw InvalidArg("loop_run_segment: the workspace moved since ms_loop_push_setup (set it up again)");
     loop_run(s, s->loop_plan->P, list, index, pick_stream(s, stream), ex);
+    if (s->push.np) {
+      // the segment's sweeps already stored their rows into every peer: no
+      // gather; signal the segment's end (the caller runs ms_loop_push_wait)
+      if (ex) ex->needed = 0;
+      CK(launch_k(k_push_signal, 1, 32, 0, pick_stream(s, stream), push_sig(s)));
+      CK(cudaGetLastError());
+    }
+  });
+}
+
+int ms_loop_push_info(ms_system_t s, void** ws_base, size_t* ws_bytes, void** mailbox) {
+  return guard([&] {
+    if (!s || !ws_base || !mailbox) throw InvalidArg("loop_push_info: null argument");
+    if (!s->ws_ready) throw InvalidArg("loop_push_info: no workspace yet (call ms_loop_begin first)");
+    set_device(s);
+    if (!s->push.mem) {
+      CK(cudaMalloc(&s->push.mem, sizeof(unsigned long long) * 16));
+      CK(cudaMemset(s->push.mem, 0, sizeof(unsigned long long) * 16));
+    }
+    *ws_base = s->ws_mem;
+    if (ws_bytes) *ws_bytes = bufs_bytes(s, s->log_cap);
+    *mailbox = s->push.mem;
+  });
+}
+
+int ms_loop_push_setup(ms_system_t s, int world, int rank, void* const* peer_ws, void* const* peer_mailbox) {
+  return guard([&] {
+    if (!s) throw InvalidArg("loop_push_setup: null handle");
+    set_device(s);
+    s->push.np = 0;
+    s->push.world = world;
+    s->push.rank = rank;
+    if (world <= 1) return;
+    if (world - 1 > kMaxPeers || rank < 0 || rank >= world || !peer_ws || !peer_mailbox)
+      throw InvalidArg("loop_push_setup: need 2 <= world <= 8, 0 <= rank < world and peer arrays");
+    if (!s->push.mem) throw InvalidArg("loop_push_setup: call ms_loop_push_info first");
+    int np = 0;
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) continue;
+      if (!peer_ws[q] || !peer_mailbox[q]) throw InvalidArg("loop_push_setup: null peer pointer");
+      s->push.peer_ws[np] = static_cast<char*>(peer_ws[q]);
+      s->push.peer_slot[np] = static_cast<unsigned long long*>(peer_mailbox[q]) + rank;
+      s->push.peer_rank[np] = q;
+      ++np;
+    }
+    // a fresh epoch sequence: the caller synchronizes the ranks after every
+    // rank's setup, before any segment runs
+    CK(cudaMemset(s->push.mem, 0, sizeof(unsigned long long) * 16));
+    CK(cudaDeviceSynchronize());
+    s->push.np = np;
+    s->push.ws_at_setup = s->ws_mem;
+  });
+}
+
+int ms_loop_push_wait(ms_system_t s, void* stream) {
+  return guard([&] {
+    if (!s || !s->loop_active) throw InvalidArg("loop_push_wait: no active loop");
+    if (!s->push.np) return;
+    set_device(s);
+    CK(launch_k(k_push_wait, 1, 32, 0, pick_stream(s, stream), push_sig(s)));
+    CK(cudaGetLastError());
+  });
+}
+
+int ms_ipc_export(void* dev_ptr, unsigned char* handle64) {
+  return guard([&] {
+    if (!dev_ptr || !handle64) throw InvalidArg("ipc_export: null argument");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, dev_ptr));
+    static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+    std::memcpy(handle64, &h, 64);
+  });
+}
+
+int ms_ipc_import(const unsigned char* handle64, void** dev_ptr) {
+  return guard([&] {
+    if (!handle64 || !dev_ptr) throw InvalidArg("ipc_import: null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    CK(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int ms_ipc_close(void* dev_ptr) {
+  return guard([&] {
+    if (!dev_ptr) throw InvalidArg("ipc_close: null argument");
+    CK(cudaIpcCloseMemHandle(dev_ptr));
   });
 }
 

@@ -252,6 +252,17 @@ struct StepLogRec {
 };
 
 // Pointers of one solve workspace (device addresses).
+// Row-sharded loop, push exchange (ms_loop_push_setup): a sweep stores each of
+// its output rows into its own workspace AND at the same offset into every
+// peer's workspace (peer memory over NVLink, P2P/IPC-mapped), so the exchange
+// rides on the sweep's own stores instead of a following all-gather.
+constexpr int kMaxPeers = 7;  // world <= 8
+struct PushDev {
+  const char* ws;              // this handle's workspace base
+  char* peer[kMaxPeers];       // the peers' workspace bases (same layout)
+  int np;                      // number of peers (0: no push)
+};
+
 struct Bufs {
   double* xb[2];                 // x / x_store ping-pong
   double* kb[kMaxStages + 1];    // stage derivatives; slot 0 <-> slot S for FSAL

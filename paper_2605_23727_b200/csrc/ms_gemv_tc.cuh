@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
           const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(ci, A), __fmul_rn(si, B)));
           MS_CHECK(row >= a.row0 && row < a.row1, "tc16 sweep: output row outside the handle");
           const double o = ws_add(a.fvc[row], (double)coup, a.ws32);
-          out[(int64_t)row * a.d + a.cs] = o;
+          push_row(a.push, out + (int64_t)row * a.d + a.cs, o);
           nonfinite |= !isfinite(o);
         }
         if (warp == 2 && lane == 0) g.cnt[tile] = 0;  // ready for the next launch
@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
     }
   }
+  if (warp >= 2) push_fence(a.push);
   if (warp >= 2 && __any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
   tc_fence_before();
   __syncthreads();

@@ -105,7 +105,21 @@ struct RhsArgs {
   const void* tc16;
   // the column data's f16 operand image (Bufs::op16), written by the prep
   const void* op16;
+  // push exchange of the row-sharded loop (np = 0: none)
+  PushDev push;
 };
+
+// store one output element of a sweep: here and, in the push exchange, at the
+// same workspace offset in every peer (then visible system-wide at the
+// sweep's push_fence)
+__device__ __forceinline__ void push_row(const PushDev& p, double* dst, double v) {
+  *dst = v;
+  for (int q = 0; q < p.np; ++q)
+    *reinterpret_cast<double*>(p.peer[q] + (reinterpret_cast<const char*>(dst) - p.ws)) = v;
+}
+__device__ __forceinline__ void push_fence(const PushDev& p) {
+  if (p.np) __threadfence_system();
+}
 
 __device__ __forceinline__ void sweep_count(const RhsArgs& a) {
   if (a.count_ctl && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -843,11 +857,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_rhs_fast(RhsAr
         }
         MS_CHECK(r >= a.row0 && r < a.row1, "register sweep: output row outside the handle");
         const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
-        out[(int64_t)r * a.d + a.cs] = o;
+        push_row(a.push, out + (int64_t)r * a.d + a.cs, o);
         nonfinite |= !isfinite(o);
       }
     }
   }
+  push_fence(a.push);
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
 }
 
@@ -1010,11 +1025,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_eval_fused(Pre
           coup = mul<SS>(mw, A[k]);
         }
         const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
-        out[(int64_t)r * a.d + a.cs] = o;
+        push_row(a.push, out + (int64_t)r * a.d + a.cs, o);
         nonfinite |= !isfinite(o);
       }
     }
   }
+  push_fence(a.push);
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
 }
 
@@ -1335,11 +1351,12 @@ __global__ void __launch_bounds__(kTmaThreadsMax, MS_TMA_MINB) k_rhs_tma(RhsArgs
         const SS si = (SS)gin[2 * r], ci = (SS)gin[2 * r + 1];
         const SS coup = mul<SS>(mw, sub<SS>(mul<SS>(ci, A[k]), mul<SS>(si, B[k])));
         const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
-        out[(int64_t)r * a.d + a.cs] = o;
+        push_row(a.push, out + (int64_t)r * a.d + a.cs, o);
         nonfinite |= !isfinite(o);
       }
     }
   }
+  push_fence(a.push);
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
   if constexpr (NEXT) {
     // the k_l rows of this CTA are written by the consumer warps (the producer
@@ -1457,9 +1474,10 @@ __global__ void __launch_bounds__(kSeqThreads) k_rhs_seq(RhsArgs a) {
     }
     double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
     const double o = ws_add(a.fvc[r], (double)coup, a.ws32);
-    out[(int64_t)r * a.d + a.cs] = o;
+    push_row(a.push, out + (int64_t)r * a.d + a.cs, o);
     nonfinite = !isfinite(o);
   }
+  push_fence(a.push);
   if (warp == 0 && __any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
 }
 
@@ -1953,6 +1971,48 @@ __global__ void k_nf_scan(Ctl* c, const double* v, int64_t n, int l) {
 }
 
 // sharded loop: FSAL k1 <- k_last on an accepted attempt (slot 0 stays k1)
+// Push exchange barrier (ms_loop_push_*): after every loop segment each rank
+// bumps its epoch and stores it into its slot of every peer's mailbox (system
+// scope, after the segment's pushes); before the next segment it waits until
+// every peer's slot in its own mailbox has reached its epoch. All ranks run the
+// same segment sequence, so the epochs agree.
+struct PushSig {
+  unsigned long long* epoch;                // this rank's counter
+  unsigned long long* mbox;                 // this rank's mailbox [world]
+  unsigned long long* peer_slot[kMaxPeers]; // &mailbox_q[rank] of every peer q
+  int peer_rank[kMaxPeers];                 // q of peer_slot[i]
+  int np;
+};
+__global__ void k_push_signal(PushSig s) {
+  msb::count_launch();
+  pdl_enter();
+  if (threadIdx.x != 0) return;
+  const unsigned long long e = *s.epoch + 1;
+  *s.epoch = e;
+  __threadfence_system();  // the segment's pushes (earlier kernels, stream order) before the flag
+  for (int q = 0; q < s.np; ++q)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(s.peer_slot[q]), "l"(e) : "memory");
+}
+__global__ void k_push_wait(PushSig s) {
+  msb::count_launch();
+  pdl_enter();
+  if (threadIdx.x != 0) return;
+  const unsigned long long e = *s.epoch;
+  uint64_t t0 = 0;
+  for (int q = 0; q < s.np; ++q) {
+    for (uint32_t it = 0;; ++it) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(s.mbox + s.peer_rank[q]) : "memory");
+      if (v >= e) break;
+      if ((it & 1023) == 0) {  // a peer that never arrives ends the kernel instead of hanging the GPU
+        const uint64_t now = globaltimer_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 20000000000ull) __trap();
+      }
+    }
+  }
+}
+
 __global__ void k_fsal_copy(const Ctl* c, double* k1, const double* klast, int64_t n) {
   msb::count_launch();
   if (!c->accepted) return;  // set by this attempt's k_finalize (stale only once done)

@@ -52,6 +52,7 @@ struct MultiArgs {
   Ctl* count_ctl;  // single-lane row-sharded loop: the sweep counts (RhsArgs::count)
   int count;
   int k_stream;    // K beyond L2: evict-first tile loads (RhsArgs::k_stream)
+  PushDev push;    // single-lane row-sharded loop: push exchange (RhsArgs::push)
 };
 
 #ifndef MS_MULTI_WARPS
@@ -359,11 +360,12 @@ __global__ void __launch_bounds__(kMultiThreads, 1)
         }
         const double o = ws_add(L.fvc[r], coup, L.ws32);
         double* out = L.kb[a.out_slot == SLOT_K1 ? L.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - L.ctl->k1i : a.out_slot)];
-        out[r] = o;
+        push_row(a.push, out + r, o);
         nonfinite[v] |= !isfinite(o);
       }
     }
   }
+  push_fence(a.push);
 #pragma unroll
   for (int v = 0; v < NL; ++v)
     if (act[v] && __any_sync(0xffffffffu, nonfinite[v]) && lane == 0) atomicOr(a.lane[v].nf_mask, 1 << a.l);

@@ -79,6 +79,7 @@ void go_tile(const RhsLaunch& L, const RhsArgs& a) {
   m.count_ctl = a.count_ctl;
   m.count = a.count;
   m.k_stream = a.k_stream;
+  m.push = a.push;
   LaneArgs& ln = m.lane[0];
   ln.ctl = a.ctl;
   ln.nf_mask = a.nf_mask;

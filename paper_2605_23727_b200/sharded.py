@@ -98,6 +98,22 @@ class DeviceEngine:
             self._views[key] = self.torch.as_tensor(_CAI(ex.buf, ex.total), device="cuda")
         return Exchange(True, self._views[key], ex.offset, ex.count, ex.total)
 
+    # push exchange (ms_loop_push_*): the sweeps store their rows into every
+    # peer's workspace; each segment ends with an epoch release into the peers'
+    # mailboxes and the next one starts after push_wait
+    def push_info(self):
+        ws, nb, mb = C.c_void_p(), C.c_size_t(), C.c_void_p()
+        _abi.check(self.L.ms_loop_push_info(self.sys.handle, C.byref(ws), C.byref(nb), C.byref(mb)), "push_info")
+        return ws.value, nb.value, mb.value
+
+    def push_setup(self, world: int, rank: int, peer_ws, peer_mbox) -> None:
+        pw = (C.c_void_p * world)(*[C.c_void_p(p) for p in peer_ws])
+        pm = (C.c_void_p * world)(*[C.c_void_p(p) for p in peer_mbox])
+        _abi.check(self.L.ms_loop_push_setup(self.sys.handle, world, rank, pw, pm), "push_setup")
+
+    def push_wait(self) -> None:
+        _abi.check(self.L.ms_loop_push_wait(self.sys.handle, C.c_void_p(self.stream())), "push_wait")
+
     def done(self) -> bool:
         d = C.c_int()
         _abi.check(self.L.ms_loop_done(self.sys.handle, C.c_void_p(self.stream()), C.byref(d)), "ms_loop_done")
@@ -145,6 +161,64 @@ class TorchComm:
                 p.copy_(t)
 
 
+def _ipc_export(ptr: int) -> bytes:
+    h = (C.c_ubyte * 64)()
+    _abi.check(_abi.lib().ms_ipc_export(C.c_void_p(ptr), h), "ms_ipc_export")
+    return bytes(h)
+
+
+def _ipc_import(handle: bytes) -> int:
+    h = (C.c_ubyte * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _abi.check(_abi.lib().ms_ipc_import(h, C.byref(p)), "ms_ipc_import")
+    return p.value
+
+
+class PushComm:
+    """The push exchange across processes (one GPU each): every rank exports
+    its workspace and mailbox with CUDA IPC, imports the peers' (NVLink peer
+    mappings), and hands them to ms_loop_push_setup; the sweeps then store
+    their rows straight into the peers' memory and the segments synchronize
+    through the mailboxes (ms_loop_push_wait) -- no all-gather. Setup runs
+    after every ms_loop_begin (cheap when the workspace did not move)."""
+
+    push = True
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self._opened = {}
+
+    def setup(self, engine) -> None:
+        if self.world <= 1:
+            return
+        ws, _, mb = engine.push_info()
+        # collective on every solve (a rank whose workspace moved needs the
+        # others to import its new handle); handles already open are reused
+        mine = (_ipc_export(ws), _ipc_export(mb))
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        peer_ws, peer_mb = [], []
+        for q, (hw, hm) in enumerate(allh):
+            if q == self.rank:
+                peer_ws.append(ws)
+                peer_mb.append(mb)
+                continue
+            for h in (hw, hm):
+                if h not in self._opened:
+                    self._opened[h] = _ipc_import(h)
+            peer_ws.append(self._opened[hw])
+            peer_mb.append(self._opened[hm])
+        engine.push_setup(self.world, self.rank, peer_ws, peer_mb)
+        self.dist.barrier(group=self.group)  # every mailbox reset before any epoch is released
+
+    def gather(self, ex: Exchange) -> None:
+        raise RuntimeError("push exchange: the segments need no gather")
+
+
 class ShardedSolver:
     def __init__(self, engine, comm, check_every: int = 8, use_graph: bool = True):
         self.engine = engine
@@ -153,9 +227,12 @@ class ShardedSolver:
         self.use_graph = use_graph
 
     def _segments(self, lst: int) -> None:
+        push = getattr(self.comm, "push", False) and getattr(self.comm, "world", 1) > 1
         for i in range(self.engine.segment_count(lst)):
             ex = self.engine.run_segment(lst, i)
-            if ex.needed:
+            if push:
+                self.engine.push_wait()
+            elif ex.needed:
                 self.comm.gather(ex)
 
     def solve(self, x0, t0: float, t_final: float, policy: PrecisionPolicy, cfg: SolverConfig,
@@ -165,6 +242,8 @@ class ShardedSolver:
         ctx = self.engine.context() if hasattr(self.engine, "context") else contextlib.nullcontext()
         with ctx:
             self.engine.begin(x0, t0, t_final, policy, cfg, cap)
+            if getattr(self.comm, "push", False):
+                self.comm.setup(self.engine)
             self._segments(0)
             graph = self._capture() if self.use_graph else None
             while True:
