@@ -532,6 +532,18 @@ def run_ours(args):
         e2e_s = float(t.item())
     e2e_value = sum(r.n_accepted for r in e2e_res) / e2e_s
     log_bytes = max(r.step_log_count for r in e2e_res) * 32
+    replicas = None
+    if ws > 1:
+        # every rank holds the whole (replicated) final state and counts: they
+        # must agree bit for bit across ranks, whichever exchange ran
+        fs = np.ascontiguousarray(e2e_res[0].final_state)
+        sig = float(np.frombuffer(fs.tobytes(), dtype=np.uint64).astype(np.float64).sum() % 1e15)
+        v = torch.tensor([sig, float(e2e_res[0].n_accepted), float(e2e_res[0].n_failed)], device=f"cuda:{local}",
+                         dtype=torch.float64)
+        lo, hi = v.clone(), v.clone()
+        torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
+        torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
+        replicas = bool(torch.equal(lo, hi))
 
     # roofline of the dominant kernel (this rank's K sweep), CUDA events on its stream
     from paper_2605_23727_b200.precision import SSS
@@ -608,6 +620,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": n * 8 + log_bytes},
         "gpu_launches": gpu_launches,
         "exchange": exchange,
+        "replicas_agree": replicas,
         "accuracy": err,
     }
     if rank == 0 and not args.no_cpu_baseline and ws == 1:
