@@ -46,17 +46,25 @@ namespace msb {
 constexpr int kGvBM = 128;      // rows per tile (TMEM lanes)
 constexpr int kGvBK = 64;       // columns per k-block: one 128-byte SW128 row of f16
 constexpr int kGvChunk = 2048;  // columns per unit (fixed: the sums' order depends on N only)
-// K-blocks per pipeline stage: their TMA boxes are issued together, so every
-// row of the tile is read as one KB x 128-byte run (DRAM page locality)
+// MS_GV_FINE: one k-block per ring stage (released as soon as its MMAs are
+// done), issued four at a time, and 1 KB operand tiles (rows 0-7; the MMA reads
+// rows 8-15 from one shared zero atom through the descriptor's stride), which
+// fits 13 stages = 208 KB of K in flight instead of 192
+#ifndef MS_GV_FINE
+#define MS_GV_FINE 0  // measured slower: 5.73 vs 6.43 TB/s (profiles/r2_tc16.txt)
+#endif
+// K-blocks per pipeline stage: their copies are issued together
 #ifndef MS_GV_KB
-#define MS_GV_KB 4
+#define MS_GV_KB (MS_GV_FINE ? 1 : 4)
 #endif
 constexpr int kGvKB = MS_GV_KB;
+constexpr int kGvIssue = 4;                   // MS_GV_FINE: stages issued per producer step
 constexpr int kGvABytes = kGvBM * kGvBK * 2;  // 16 KB of K per k-block
-constexpr int kGvBBytes = 16 * kGvBK * 2;     // 2 KB operand tile per k-block (rows 4..15 stay zero)
+// operand tile per k-block: rows 4.. stay zero (MS_GV_FINE: rows 8-15 are the zero atom)
+constexpr int kGvBBytes = (MS_GV_FINE ? 8 : 16) * kGvBK * 2;
 constexpr int kGvStageBytes = kGvKB * (kGvABytes + kGvBBytes);
 #ifndef MS_GV_STAGES
-#define MS_GV_STAGES (12 / MS_GV_KB)
+#define MS_GV_STAGES (MS_GV_FINE ? 13 : 12 / MS_GV_KB)
 #endif
 constexpr int kGvStages = MS_GV_STAGES;
 #ifndef MS_GV_PF
@@ -76,7 +84,9 @@ static_assert(kGvBatch <= kGvGroups, "accumulator batch");
 #define MS_GV_EXP 0  // timing experiments only (results wrong): 1 = accumulators skip the TMEM loads
 #endif
 constexpr int kGvThreads = 6 * 32;
-constexpr size_t kGvSmem = 1024 + (size_t)kGvStages * kGvStageBytes + 256;
+constexpr size_t kGvZeroBytes = MS_GV_FINE ? 1024 : 0;  // the shared zero atom (rows 8-15 of every B tile)
+constexpr size_t kGvSmem = 1024 + (size_t)kGvStages * kGvStageBytes + kGvZeroBytes + 256;
+static_assert(!MS_GV_FINE || (kGvKB == 1 && kGvChunk % (kGvIssue * kGvBK) == 0), "fine ring layout");
 constexpr uint32_t kGvTmemCols = kGvGroups * 64;  // kGvGroups x 4 MMAs x 16 columns (power of two)
 static_assert(kGvTmemCols == 256 || kGvTmemCols == 512, "TMEM allocation");
 
@@ -143,7 +153,8 @@ __global__ void __launch_bounds__(kGvThreads, 1)
   extern __shared__ __align__(1024) unsigned char gv_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gv_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kGvStages * kGvStageBytes);
+  unsigned char* zero_atom = smem + (size_t)kGvStages * kGvStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(zero_atom + kGvZeroBytes);
   uint64_t* empty = full + kGvStages;
   uint64_t* tfull = empty + kGvStages;
   uint64_t* tempty = tfull + kGvGroups;
@@ -166,12 +177,15 @@ __global__ void __launch_bounds__(kGvThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // rows 4..15 of every operand tile are zero for the whole kernel
-  for (int idx = threadIdx.x; idx < kGvStages * kGvKB * (12 * 128 / 16); idx += blockDim.x) {
-    const int t = idx / (12 * 128 / 16), o = idx % (12 * 128 / 16);
+  // rows 4.. of every operand tile (and the zero atom) are zero for the whole kernel
+  constexpr int kZeroRowBytes = kGvBBytes - 4 * 128;
+  for (int idx = threadIdx.x; idx < kGvStages * kGvKB * (kZeroRowBytes / 16); idx += blockDim.x) {
+    const int t = idx / (kZeroRowBytes / 16), o = idx % (kZeroRowBytes / 16);
     *reinterpret_cast<uint4*>(smem + (size_t)(t / kGvKB) * kGvStageBytes + kGvKB * kGvABytes +
                               (t % kGvKB) * kGvBBytes + 4 * 128 + o * 16) = make_uint4(0u, 0u, 0u, 0u);
   }
+  for (int o = threadIdx.x; o < (int)(kGvZeroBytes / 16); o += blockDim.x)
+    reinterpret_cast<uint4*>(zero_atom)[o] = make_uint4(0u, 0u, 0u, 0u);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -204,6 +218,28 @@ __global__ void __launch_bounds__(kGvThreads, 1)
     };
     if (lane == 0)
       for (int p = 0; p < MS_GV_PF; ++p) prefetch_next();
+#if MS_GV_FINE
+    // lane j fills stage sg + j (its own empty wait), kGvIssue stages per step
+    for (int u = u0; u < u1; ++u) {
+      const int tile = u / g.chunks, ch = u % g.chunks;
+      const int nkb = gv_nkb(a, ch);
+      for (int kb = 0; kb < nkb; kb += kGvIssue) {
+        const int nb = min(kGvIssue, nkb - kb);
+        if (lane < nb) {
+          const int s_ = sg + lane, st = s_ % kGvStages;
+          if (s_ >= kGvStages) tc_wait(&empty[st], ((s_ / kGvStages) & 1) ^ 1);
+          unsigned char* sa = smem + (size_t)st * kGvStageBytes;
+          const int kbi = ch * (kGvChunk / kGvBK) + kb + lane;  // k-block of the row
+          MS_CHECK(tile < g.tiles && kbi < g.kblocks, "tc16 sweep: tile image outside the handle's K");
+          mbar_expect_tx(&full[st], kGvABytes + 512);
+          bulk_g2s_hint(sa, g.kt + ((int64_t)tile * g.kblocks + kbi) * kGvABytes, kGvABytes, &full[st], pol);
+          bulk_g2s(sa + kGvABytes, op + (size_t)kbi * 512, 512, &full[st]);
+        }
+        __syncwarp();
+        sg += nb;
+      }
+    }
+#else
     for (int u = u0; u < u1; ++u) {
       const int tile = u / g.chunks, ch = u % g.chunks;
       const int nkb = gv_nkb(a, ch);
@@ -228,6 +264,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
           bulk_g2s(sb + (lane - kGvKB) * kGvBBytes, op + (size_t)((c0 / kGvBK) + lane - kGvKB) * 512, 512, &full[st]);
       }
     }
+#endif
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       int kbg = 0, sg = 0;
@@ -246,7 +283,13 @@ __global__ void __launch_bounds__(kGvThreads, 1)
 #pragma unroll
             for (int k = 0; k < kGvBK / 16; ++k) {
               const uint64_t adesc = umma_smem_desc(sa + j * kGvABytes + k * 32);
+#if MS_GV_FINE
+              // rows 8-15 of the B tile: the zero atom (descriptor stride = its distance)
+              const uint64_t bdesc = umma_smem_desc_sbo(sb + j * kGvBBytes + k * 32,
+                                                        smem_u32(zero_atom) - (sb + j * kGvBBytes));
+#else
               const uint64_t bdesc = umma_smem_desc(sb + j * kGvBBytes + k * 32);
+#endif
               asm volatile(
                   "{\n .reg .pred p;\n setp.ne.b32 p, 0, 0;\n"
                   " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(

@@ -42,4 +42,16 @@ __device__ __forceinline__ uint64_t umma_smem_desc(uint32_t smem_addr) {
   return d;
 }
 
+// the same descriptor with an explicit stride between the 8-row groups (bytes,
+// multiple of 16, < 256 KB): rows 8.. of an operand can live elsewhere
+__device__ __forceinline__ uint64_t umma_smem_desc_sbo(uint32_t smem_addr, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 }  // namespace msb
