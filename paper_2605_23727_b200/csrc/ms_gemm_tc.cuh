@@ -179,6 +179,7 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
   const BatchDev& d = t.a.d;
   const float mw = (float)d.mw;
   const float2* sc2 = reinterpret_cast<const float2*>(d.sc);
+  (void)sc2;  // the (s, c)-pair record layouts only
   const bool row_ok = i < t.n;
   TcRec cur[8];
   auto load = [&](int c0, TcRec (&v)[8]) {
@@ -651,6 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) MS_T2_BOUNDS
   __shared__ TcFin tc_fin[kT2BN / 4];
 #else
   constexpr TcFin* tc_fin = nullptr;
+  (void)tc_fin;
 #endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();

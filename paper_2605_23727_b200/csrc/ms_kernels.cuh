@@ -322,7 +322,7 @@ __device__ __forceinline__ bool prep_agent(const PrepArgs& p, const PrepCtx& c, 
     MS_CHECK(i >= 0 && 2 * i + 1 < 2 * p.ld, "prep: column data index");
     gin[2 * i] = sv;  // split column data: interleaved (s_j, c_j) pairs
     gin[2 * i + 1] = cv;
-    if constexpr (sizeof(GS) == 4)
+    if constexpr (sizeof(GS) == 4 && MODEL == MD_KUR)
       if (p.B.op16) op16_put(p.B.op16, i, sv, cv);
     if constexpr (sizeof(GS) == 4)
       if (sc_tiny(sv, cv)) c.ctl->pk_off = 1;
