@@ -178,8 +178,7 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& t, uint32_t lane_addr,
                                             const TcFin* fin = nullptr) {
   const BatchDev& d = t.a.d;
   const float mw = (float)d.mw;
-  const float2* sc2 = reinterpret_cast<const float2*>(d.sc);
-  (void)sc2;  // the (s, c)-pair record layouts only
+  [[maybe_unused]] const float2* sc2 = reinterpret_cast<const float2*>(d.sc);  // (s, c)-pair record layouts
   const bool row_ok = i < t.n;
   TcRec cur[8];
   auto load = [&](int c0, TcRec (&v)[8]) {
