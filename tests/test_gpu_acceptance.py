@@ -1,0 +1,153 @@
+"""The reference's acceptance criteria that touch the hot path
+(proj/tests/acceptance.cpp), run on the DEVICE through the C-ABI with the
+reference's own thresholds. The campaign cases of the reference come from its
+Sobol campaign generator (out of scope here); the device
+versions use the same system sizes, tolerances and time spans with test ids /
+parameters drawn from SplitMix64 seeds, which the criteria do not depend on.
+
+  criterion 1  one-step error ratios in [12, 20] when h halves (exp, LCO)   acceptance.cpp:91-142
+  criterion 2  a custom all-binary64 policy is bitwise the Double policy    acceptance.cpp:144-192
+  criterion 3  the estimator contract on every logged step                  acceptance.cpp:194-230
+  criterion 10 DP5(4) at 1e-9 within 1e-7 of the analytic LCO propagator    acceptance.cpp:357-380
+  criterion 11 the Kuramoto mean phase drifts with mean(omega) only         acceptance.cpp:382-411
+  criterion 12 two runs of a campaign give identical results and step logs  acceptance.cpp:413-454
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2605_23727_b200 import harness as H
+from paper_2605_23727_b200 import solver as S
+from paper_2605_23727_b200.configs import TWO_PI, rng_uniform
+from paper_2605_23727_b200.metrics import lco_analytic
+from paper_2605_23727_b200.precision import B64, PolicyVariant, StagePrecision, custom_policy, policy_for
+from paper_2605_23727_b200.systems import DeviceSystem, SystemSpec, make_kuramoto, make_lco
+
+pytestmark = pytest.mark.gpu
+
+DDD = StagePrecision(B64, B64, B64)
+
+
+def test_criterion1_order(gpu):
+    """one BS3(2) step from x0 with k1 = f(x0): the error against the exact
+    solution falls by 2^3 +- when h halves (ratios in [12, 20])."""
+    cfg = S.SolverConfig(rel_tol=0.5, abs_tol=0.5)
+    dbl = policy_for(PolicyVariant.Double)
+    exp_sys = DeviceSystem(SystemSpec("scalar_exp", 1))
+    prev = 0.0
+    for i in range(4):
+        h = 0.1 / 2.0 ** i
+        o = S.bs32_step(exp_sys, 0.0, np.array([1.0]), h, np.array([1.0]), dbl, cfg)
+        err = abs(o.x_next[0] - math.exp(h))
+        if i > 0:
+            assert 12.0 <= prev / err <= 20.0, (h, prev / err)
+        prev = err
+    lco = make_lco(6)
+    x0 = rng_uniform(17, 0, 12, 0.0, 2.0)
+    k1 = lco.eval_rhs(0.0, x0, DDD)
+    prev = 0.0
+    for i in range(4):
+        h = 0.1 / 2.0 ** i
+        o = S.bs32_step(lco, 0.0, x0, h, k1, dbl, cfg)
+        err = float(np.max(np.abs(o.x_next - lco_analytic(x0, h))))
+        if i > 0:
+            assert 12.0 <= prev / err <= 20.0, (h, prev / err)
+        prev = err
+
+
+def test_criterion2_all_binary64_policy_is_double(gpu):
+    """ten LCO / Kuramoto solves (N = 40): a custom policy with every stage
+    (and the first-step k1) binary64 gives the Double policy's status, final
+    state and step log bit for bit."""
+    all_d = custom_policy([DDD, DDD, DDD], first_step_k1=DDD, storage=B64)
+    for t in range(10):
+        tid = 100 + t
+        if t % 2 == 0:
+            sys, tf = make_lco(40), 4.0
+            x0 = rng_uniform(tid, 1, 80, -1.0, 1.0)
+        else:
+            sys, tf = make_kuramoto(40, 0.5, 0.8, tid), 15.0
+            x0 = rng_uniform(tid, 1, 40, 0.0, TWO_PI)
+        rel = 1e-5 if t % 3 == 0 else 1e-6
+        cfg = S.SolverConfig(rel_tol=rel, abs_tol=1e-2 * rel)
+        a = S.solve(sys, x0, 0.0, tf, policy_for(PolicyVariant.Double), cfg)
+        b = S.solve(sys, x0, 0.0, tf, all_d, cfg)
+        assert a.status == b.status
+        assert np.array_equal(a.final_state, b.final_state)
+        assert [(s.t, s.h, s.err, s.accepted) for s in a.step_log] == \
+               [(s.t, s.h, s.err, s.accepted) for s in b.step_log]
+        sys.close()
+
+
+@pytest.mark.parametrize("variant", [PolicyVariant.Single, PolicyVariant.Mixed1, PolicyVariant.Mixed2,
+                                     PolicyVariant.Double])
+def test_criterion3_estimator_contract(gpu, variant):
+    """every logged attempt of LCO solves at tolerances 1e-3..1e-8: accepted
+    exactly when the estimate is finite and <= rel_tol (solver.cpp:212)."""
+    for k, rel in enumerate((1e-3, 1e-4, 1e-5, 1e-6, 1e-7, 1e-8)):
+        sys = make_lco(100)
+        x0 = rng_uniform(300 + k, 1, 200, -1.0, 1.0)
+        cfg = S.SolverConfig(rel_tol=rel, abs_tol=1e-2 * rel, max_iterations=20000)
+        r = S.solve(sys, x0, 0.0, TWO_PI, policy_for(variant), cfg)
+        assert r.step_log, rel
+        for s in r.step_log:
+            if s.accepted:
+                assert math.isfinite(s.err) and s.err <= rel
+            else:
+                assert not (s.err <= rel)  # > rel or non-finite
+        sys.close()
+
+
+def test_criterion10_reference_quality(gpu):
+    """the tight binary64 DP5(4) run (rel = abs = 1e-9) of 20 LCO cases
+    (N = 100) ends within 1e-7 of the analytic propagator per component."""
+    worst = 0.0
+    for t in range(20):
+        sys = make_lco(100)
+        x0 = rng_uniform(500 + t, 1, 200, -1.0, 1.0)
+        tf = 2.0 + 0.5 * t  # spans of a few periods
+        ref = S.dp54_reference(sys, x0, 0.0, tf, S.SolverConfig())
+        assert ref.status == S.SolveStatus.Completed
+        worst = max(worst, float(np.max(np.abs(ref.final_state - lco_analytic(x0, tf)))))
+        sys.close()
+    print(f"criterion 10: worst per-component deviation over 20 tests {worst:.3e}")
+    assert worst <= 1e-7
+
+
+def test_criterion11_mean_phase_drift(gpu):
+    """ten Kuramoto cases (N = 100, rtol 1e-8, abs 1e-10, Double): the mean
+    phase moves with mean(omega) only (the all-to-all sine coupling sums to
+    zero), |drift| <= 1e-5 t_f."""
+    worst = 0.0
+    for t in range(10):
+        sigma, kc = 0.2 + 0.1 * t, 0.3 + 0.15 * t
+        sys = make_kuramoto(100, sigma, kc, 700 + t)
+        x0 = rng_uniform(700 + t, 1, 100, 0.0, TWO_PI)
+        tf = 10.0
+        cfg = S.SolverConfig(rel_tol=1e-8, abs_tol=1e-10)
+        r = S.solve(sys, x0, 0.0, tf, policy_for(PolicyVariant.Double), cfg)
+        assert r.status == S.SolveStatus.Completed
+        omega = sys.spec.omega
+        drift = abs(r.final_state.mean() - x0.mean() - omega.mean() * tf)
+        worst = max(worst, drift / tf)
+        assert drift <= 1e-5 * tf, (t, drift)
+        sys.close()
+    print(f"criterion 11: worst |mean-phase drift| / t_f {worst:.3e}")
+
+
+def test_criterion12_determinism(gpu, tmp_path):
+    """a campaign (8 LCO tests, N = 20, tolerances 1e-4 and 1e-6, t_f = 2 pi,
+    four variants each) run twice through the harness: identical results.csv
+    and steps.csv bytes."""
+    cases = [H.TestCase(test_id=900 + 2 * k + j, benchmark="lco", agents=20, rel_tol=tol, abs_tol=1e-2 * tol,
+                        t_final=TWO_PI)
+             for k in range(8) for j, tol in enumerate((1e-4, 1e-6))]
+    outs = []
+    for run in range(2):
+        d = tmp_path / f"run{run}"
+        opt = H.RunOptions(output_dir=str(d), step_log_csv=True, time_limits=False)
+        H.run_cases(cases, opt=opt)
+        outs.append(((d / "results.csv").read_bytes(), (d / "steps.csv").read_bytes()))
+    assert outs[0][0] == outs[1][0]
+    assert outs[0][1] == outs[1][1] and len(outs[0][1]) > 0
