@@ -151,3 +151,61 @@ def test_criterion12_determinism(gpu, tmp_path):
         outs.append(((d / "results.csv").read_bytes(), (d / "steps.csv").read_bytes()))
     assert outs[0][0] == outs[1][0]
     assert outs[0][1] == outs[1][1] and len(outs[0][1]) > 0
+
+
+@pytest.mark.slow
+def test_criteria7_8_9_precision_plateaus(gpu):
+    """The paper's precision effects on an LCO campaign (N = 100, tolerances
+    1e-3..1e-8, t_f = 10 pi, snapshots; 20 tests per tolerance), through the
+    harness on the device (acceptance.cpp:288-355):
+      7  Single's median final error sits in [1e-6, 1e-3] for tol <= 1e-5 and
+         falls less than 10x from 1e-5 to 1e-8, Double's at least 100x;
+      8  at tol 1e-8 Mixed2's median final error is within 10x of Double's and
+         below Single's;
+      9  Single's mean analytic local error plateaus in [1e-8, 1e-6] for
+         tol <= 1e-6 (above tol below the plateau; 1e-7 vs 1e-8 within 10x),
+         Double's and Mixed2's stay within 10x of every tolerance."""
+    tols = (1e-3, 1e-4, 1e-5, 1e-6, 1e-7, 1e-8)
+    cases = [H.TestCase(test_id=2000 + 20 * k + j, benchmark="lco", agents=100, rel_tol=tol, abs_tol=1e-2 * tol,
+                        t_final=10.0 * math.pi)
+             for k, tol in enumerate(tols) for j in range(20)]
+    rows = H.run_cases(cases, spec=H.CampaignSpec(snapshots=True), opt=H.RunOptions(time_limits=False))
+    ok_ids = {}
+    for r in rows:
+        ok_ids.setdefault(r.test_id, []).append(r.status == S.SolveStatus.Completed)
+    complete = {t for t, v in ok_ids.items() if all(v)}
+    fin, ana = {}, {}
+    for r in rows:
+        if r.test_id not in complete or r.variant == "Reference":
+            continue
+        if r.final_error is not None:
+            fin.setdefault(r.variant, {}).setdefault(r.rel_tol, []).append(r.final_error)
+        if r.mean_eanalytic is not None:
+            ana.setdefault(r.variant, {}).setdefault(r.rel_tol, []).append(r.mean_eanalytic)
+    med = lambda d, v, t: float(np.median(d[v][t]))  # noqa: E731
+    for v in fin:
+        for t in fin[v]:
+            assert len(fin[v][t]) >= 20, (v, t, len(fin[v][t]))
+    # criterion 7
+    for t in (1e-5, 1e-6, 1e-7, 1e-8):
+        assert 1e-6 <= med(fin, "Single", t) <= 1e-3, (t, med(fin, "Single", t))
+    s_drop = med(fin, "Single", 1e-5) / med(fin, "Single", 1e-8)
+    d_drop = med(fin, "Double", 1e-5) / med(fin, "Double", 1e-8)
+    print(f"criterion 7: Single 1e-5 -> 1e-8 decrease {s_drop:.3g}x, Double {d_drop:.3g}x")
+    assert s_drop < 10.0 and d_drop >= 100.0
+    # criterion 8
+    m2, d, s = med(fin, "Mixed2", 1e-8), med(fin, "Double", 1e-8), med(fin, "Single", 1e-8)
+    print(f"criterion 8: tol 1e-8 medians Mixed2 {m2:.3e}, Double {d:.3e}, Single {s:.3e}")
+    assert m2 <= 10.0 * d and m2 < s
+    # criterion 9
+    for t in (1e-6, 1e-7, 1e-8):
+        m = med(ana, "Single", t)
+        assert 1e-8 <= m <= 1e-6, (t, m)
+        if t < 1e-6:
+            assert m > t, (t, m)
+    p7, p8 = med(ana, "Single", 1e-7), med(ana, "Single", 1e-8)
+    assert max(p7, p8) / min(p7, p8) < 10.0
+    for v in ("Double", "Mixed2"):
+        for t in ana[v]:
+            assert med(ana, v, t) <= 10.0 * t, (v, t, med(ana, v, t))
+    print(f"criterion 9: Single plateau {p7:.3e} (1e-7), {p8:.3e} (1e-8)")
