@@ -8,6 +8,7 @@ parameters drawn from SplitMix64 seeds, which the criteria do not depend on.
   criterion 1  one-step error ratios in [12, 20] when h halves (exp, LCO)   acceptance.cpp:91-142
   criterion 2  a custom all-binary64 policy is bitwise the Double policy    acceptance.cpp:144-192
   criterion 3  the estimator contract on every logged step                  acceptance.cpp:194-230
+  criteria 6-9 step-count ratios and the precision plateaus (LCO campaign)  acceptance.cpp:251-355
   criterion 10 DP5(4) at 1e-9 within 1e-7 of the analytic LCO propagator    acceptance.cpp:357-380
   criterion 11 the Kuramoto mean phase drifts with mean(omega) only         acceptance.cpp:382-411
   criterion 12 two runs of a campaign give identical results and step logs  acceptance.cpp:413-454
@@ -209,3 +210,14 @@ def test_criteria7_8_9_precision_plateaus(gpu):
         for t in ana[v]:
             assert med(ana, v, t) <= 10.0 * t, (v, t, med(ana, v, t))
     print(f"criterion 9: Single plateau {p7:.3e} (1e-7), {p8:.3e} (1e-8)")
+    # criterion 6 (its LCO half, acceptance.cpp:251-286): every variant's step
+    # count ratio beta to Double has median 1 and quartiles within 2 %
+    betas = {}
+    for r in rows:
+        if r.test_id in complete and r.variant != "Reference" and r.beta is not None:
+            betas.setdefault(r.variant, []).append(r.beta)
+    assert len(betas) == 4
+    for v, vals in betas.items():
+        q1, q2, q3 = np.percentile(vals, [25, 50, 75])
+        print(f"criterion 6: {v} beta (q1, median, q3) = ({q1:.4f}, {q2:.4f}, {q3:.4f})")
+        assert abs(q2 - 1.0) <= 1e-12 and 0.98 <= q1 <= 1.02 and 0.98 <= q3 <= 1.02
