@@ -221,3 +221,40 @@ def test_criteria7_8_9_precision_plateaus(gpu):
         q1, q2, q3 = np.percentile(vals, [25, 50, 75])
         print(f"criterion 6: {v} beta (q1, median, q3) = ({q1:.4f}, {q2:.4f}, {q3:.4f})")
         assert abs(q2 - 1.0) <= 1e-12 and 0.98 <= q1 <= 1.02 and 0.98 <= q3 <= 1.02
+
+
+@pytest.mark.slow
+def test_criterion6_beta_band_cc(gpu):
+    """criterion 6, its circadian-clock half (acceptance.cpp:270-286): a CC
+    campaign (N = 50 and 100, tolerances 1e-3..1e-6, couplings 0.001 / 0.1 / 1,
+    stimuli 0.228249 / 1.5): every variant's step-count ratio to Double has
+    median 1 and quartiles within 2 %, over >= 100 complete tests."""
+    cases = []
+    tid = 3000
+    for n in (50, 100):
+        for tol in (1e-3, 1e-4, 1e-5, 1e-6):
+            for kc in (0.001, 0.1, 1.0):
+                for i0 in (0.228249, 1.5):
+                    cases.append(H.TestCase(test_id=tid, benchmark="cc", agents=n, rel_tol=tol, abs_tol=1e-2 * tol,
+                                            t_final=48.0, coupling_k=kc, stimulus_i0=i0))
+                    tid += 1
+    # 48 parameter combinations; 120 tests as in the reference campaign (other
+    # test ids draw other cell parameters)
+    cases = cases + [H.TestCase(**{**c.__dict__, "test_id": c.test_id + 1000}) for c in cases] + \
+        [H.TestCase(**{**c.__dict__, "test_id": c.test_id + 2000}) for c in cases[:24]]
+    rows = H.run_cases(cases, opt=H.RunOptions(time_limits=False))
+    ok_ids = {}
+    for r in rows:
+        ok_ids.setdefault(r.test_id, []).append(r.status == S.SolveStatus.Completed)
+    complete = {t for t, v in ok_ids.items() if all(v)}
+    bad = sorted({(r.variant, r.rel_tol, int(r.status)) for r in rows if r.status != S.SolveStatus.Completed})
+    assert len(complete) >= 100, (len(complete), len(ok_ids), bad[:12])
+    betas = {}
+    for r in rows:
+        if r.test_id in complete and r.variant != "Reference" and r.beta is not None:
+            betas.setdefault(r.variant, []).append(r.beta)
+    assert len(betas) == 4
+    for v, vals in betas.items():
+        q1, q2, q3 = np.percentile(vals, [25, 50, 75])
+        print(f"criterion 6 (cc): {v} beta (q1, median, q3) = ({q1:.4f}, {q2:.4f}, {q3:.4f})")
+        assert abs(q2 - 1.0) <= 1e-12 and 0.98 <= q1 <= 1.02 and 0.98 <= q3 <= 1.02
