@@ -250,7 +250,12 @@ int ms_policy_lowest_format(const ms_policy* p);
 int ms_rng_uniform(uint64_t seed, uint64_t stream, int64_t n, double lo, double hi, double* out);
 int ms_rng_normal(uint64_t seed, uint64_t stream, int64_t n, double* out);
 
-/* ---- systems ---------------------------------------------------------- */
+/* ---- systems ----------------------------------------------------------
+ * ms_system_create uploads K once, converted to k_storage (read-only from then
+ * on). A Kuramoto handle with f16 K also keeps K as MMA tile images for the
+ * tensor-core sweep (another f16 copy of its rows: 2 GiB at N = 32768), used
+ * by binary32 rows at N >= 16384; without room for them the
+ * CUDA-core sweeps serve it. */
 int ms_system_create(const ms_system_desc* desc, ms_system_t* out);
 int ms_system_destroy(ms_system_t sys);
 /* K_ij = lo + (hi - lo) * uniform01() of SplitMix64(seed, stream), row-major

@@ -161,6 +161,9 @@ VARIANTS = {
     # C4 f32 TMA sweep: the first rows of every CTA's range kept in L2 (evict-last) across evaluations
     # f16 tensor-core sweep (MS_SWEEP=tc16): accumulator batch, TMEM groups, ring depth, no-TMEM-load timing
     "gv_kb4": ("ms_rhs_fast.cu", {}),
+    "gv_cur": ("ms_rhs_fast.cu", {}),
+    "gv_exp1": ("ms_rhs_fast.cu", {"MS_GV_EXP": 1}),
+    "gv_g4": ("ms_rhs_fast.cu", {"MS_GV_GROUPS": 4}),
     "gv_fine1": ("ms_rhs_fast.cu", {}),
     "gv_fine0": ("ms_rhs_fast.cu", {"MS_GV_FINE": 0}),
     "gv_pf0": ("ms_rhs_fast.cu", {"MS_GV_PF": 0}),
