@@ -58,10 +58,17 @@ constexpr int kGvChunk = 2048;  // columns per unit (fixed: the sums' order depe
 #define MS_GV_KB (MS_GV_FINE ? 1 : 4)
 #endif
 constexpr int kGvKB = MS_GV_KB;
-constexpr int kGvIssue = 4;                   // MS_GV_FINE: stages issued per producer step
+#ifndef MS_GV_ISSUE
+#define MS_GV_ISSUE 4
+#endif
+constexpr int kGvIssue = MS_GV_ISSUE;         // MS_GV_FINE: stages issued per producer step
 constexpr int kGvABytes = kGvBM * kGvBK * 2;  // 16 KB of K per k-block
-// operand tile per k-block: rows 4.. stay zero (MS_GV_FINE: rows 8-15 are the zero atom)
-constexpr int kGvBBytes = (MS_GV_FINE ? 8 : 16) * kGvBK * 2;
+// MS_GV_ZATOM: rows 8-15 of every operand tile are one shared zero atom (descriptor stride)
+#ifndef MS_GV_ZATOM
+#define MS_GV_ZATOM MS_GV_FINE
+#endif
+// operand tile per k-block: rows 4.. stay zero (MS_GV_ZATOM: rows 8-15 are the zero atom)
+constexpr int kGvBBytes = (MS_GV_ZATOM ? 8 : 16) * kGvBK * 2;
 constexpr int kGvStageBytes = kGvKB * (kGvABytes + kGvBBytes);
 #ifndef MS_GV_STAGES
 #define MS_GV_STAGES (MS_GV_FINE ? 13 : 12 / MS_GV_KB)
@@ -84,7 +91,7 @@ static_assert(kGvBatch <= kGvGroups, "accumulator batch");
 #define MS_GV_EXP 0  // timing experiments only (results wrong): 1 = accumulators skip the TMEM loads
 #endif
 constexpr int kGvThreads = 6 * 32;
-constexpr size_t kGvZeroBytes = MS_GV_FINE ? 1024 : 0;  // the shared zero atom (rows 8-15 of every B tile)
+constexpr size_t kGvZeroBytes = MS_GV_ZATOM ? 1024 : 0;  // the shared zero atom (rows 8-15 of every B tile)
 constexpr size_t kGvSmem = 1024 + (size_t)kGvStages * kGvStageBytes + kGvZeroBytes + 256;
 static_assert(!MS_GV_FINE || (kGvKB == 1 && kGvChunk % (kGvIssue * kGvBK) == 0), "fine ring layout");
 constexpr uint32_t kGvTmemCols = kGvGroups * 64;  // kGvGroups x 4 MMAs x 16 columns (power of two)
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
 #pragma unroll
             for (int k = 0; k < kGvBK / 16; ++k) {
               const uint64_t adesc = umma_smem_desc(sa + j * kGvABytes + k * 32);
-#if MS_GV_FINE
+#if MS_GV_ZATOM
               // rows 8-15 of the B tile: the zero atom (descriptor stride = its distance)
               const uint64_t bdesc = umma_smem_desc_sbo(sb + j * kGvBBytes + k * 32,
                                                         smem_u32(zero_atom) - (sb + j * kGvBBytes));

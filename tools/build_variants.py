@@ -174,6 +174,13 @@ VARIANTS = {
     "gv_kb1": ("ms_rhs_fast.cu", {"MS_GV_KB": 1}),
     "gv_kb4_g4": ("ms_rhs_fast.cu", {"MS_GV_GROUPS": 4}),
     "gv_kb4_exp1": ("ms_rhs_fast.cu", {"MS_GV_EXP": 1}),
+    "gv_fine_i1": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 1}),
+    "gv_fine_i2": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 2}),
+    "gv_fine_i4": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 4}),
+    "gv_zatom": ("ms_rhs_fast.cu", {"MS_GV_ZATOM": 1}),
+    "gv_fine_s12": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 1, "MS_GV_STAGES": 12}),
+    "gv_fine_s8": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 1, "MS_GV_STAGES": 8}),
+    "gv_kb2_s6z": ("ms_rhs_fast.cu", {"MS_GV_KB": 2, "MS_GV_STAGES": 6, "MS_GV_ZATOM": 1}),
     "keep0": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 0}),
     "keep2": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 2}),
     "keep4": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 4}),
