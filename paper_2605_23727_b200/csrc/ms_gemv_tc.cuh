@@ -143,6 +143,24 @@ __device__ __forceinline__ uint32_t gv_pack(__half lo_col, __half hi_col) {
   return (uint32_t)__half_as_ushort(lo_col) | ((uint32_t)__half_as_ushort(hi_col) << 16);
 }
 
+// MS_GV_REV: every CTA walks its units in the opposite order on alternate
+// launches (a per-CTA toggle), so a sweep starts with the unit the CTA's previous
+// sweep read last -- still in L2 under the evict-first stream. Each unit's sums go
+// to their own partial slot, combined in chunk order, so the order is free.
+#ifndef MS_GV_REV
+#define MS_GV_REV 1
+#endif
+static __device__ unsigned char g_gv_rev[4096];
+// MS_GV_KEEPKB: the last MS_GV_KEEPKB k-blocks of a CTA's stream are read with
+// policy MS_GV_KEEPPOL (1 evict-normal, 2 evict-last) instead of evict-first, so
+// more of what the next (reversed) sweep reads first survives in L2
+#ifndef MS_GV_KEEPKB
+#define MS_GV_KEEPKB 0
+#endif
+#ifndef MS_GV_KEEPPOL
+#define MS_GV_KEEPPOL 1
+#endif
+
 // unit u -> (tile, chunk); its k-block count
 __device__ __forceinline__ int gv_nkb(const RhsArgs& a, int ch) {
   const int cols = min(kGvChunk, (int)a.ld - ch * kGvChunk);
@@ -173,7 +191,11 @@ __global__ void __launch_bounds__(kGvThreads, 1)
   const int u0 = (int)((int64_t)U * blockIdx.x / gridDim.x);
   const int u1 = (int)((int64_t)U * (blockIdx.x + 1) / gridDim.x);
 
+  __shared__ int s_rev;
   if (threadIdx.x == 0) {
+    const int r = MS_GV_REV ? (int)g_gv_rev[blockIdx.x & 4095] : 0;
+    s_rev = r;
+    if (MS_GV_REV) g_gv_rev[blockIdx.x & 4095] = (unsigned char)(r ^ 1);
     for (int s = 0; s < kGvStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -204,6 +226,9 @@ __global__ void __launch_bounds__(kGvThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   bool nonfinite = false;
+  const int rev = s_rev;
+  // the CTA's k-th unit this launch
+  auto unit = [&](int uu) { return rev ? u1 - 1 - (uu - u0) : uu; };
 
   if (warp == 0) {
     // producer: bulk copies of the K tile images and of the operand rows 0-3
@@ -227,7 +252,8 @@ __global__ void __launch_bounds__(kGvThreads, 1)
       for (int p = 0; p < MS_GV_PF; ++p) prefetch_next();
 #if MS_GV_FINE
     // lane j fills stage sg + j (its own empty wait), kGvIssue stages per step
-    for (int u = u0; u < u1; ++u) {
+    for (int uu = u0; uu < u1; ++uu) {
+      const int u = unit(uu);
       const int tile = u / g.chunks, ch = u % g.chunks;
       const int nkb = gv_nkb(a, ch);
       for (int kb = 0; kb < nkb; kb += kGvIssue) {
@@ -247,7 +273,8 @@ __global__ void __launch_bounds__(kGvThreads, 1)
       }
     }
 #else
-    for (int u = u0; u < u1; ++u) {
+    for (int uu = u0; uu < u1; ++uu) {
+      const int u = unit(uu);
       const int tile = u / g.chunks, ch = u % g.chunks;
       const int nkb = gv_nkb(a, ch);
       for (int kb = 0; kb < nkb; kb += kGvKB, ++sg) {
@@ -264,9 +291,12 @@ __global__ void __launch_bounds__(kGvThreads, 1)
         __syncwarp();
         MS_CHECK(tile < g.tiles && (c0 / kGvBK) + kGvKB <= g.kblocks && (c0 % kGvBK) == 0,
                  "tc16 sweep: tile image outside the handle's K");
+        uint64_t upol = pol;
+        if (MS_GV_KEEPKB > 0 && a.k_stream && uu == u1 - 1 && kb + kGvKB > nkb - MS_GV_KEEPKB)
+          upol = MS_GV_KEEPPOL == 2 ? l2_evict_last() : l2_evict_normal();
         if (lane < kGvKB)  // one contiguous 16 KB tile image per k-block
           bulk_g2s_hint(sa + lane * kGvABytes,
-                        g.kt + ((int64_t)tile * g.kblocks + (c0 / kGvBK) + lane) * kGvABytes, kGvABytes, &full[st], pol);
+                        g.kt + ((int64_t)tile * g.kblocks + (c0 / kGvBK) + lane) * kGvABytes, kGvABytes, &full[st], upol);
         else if (lane < 2 * kGvKB)  // and the operand rows 0-3 of its B tile (the prep's image)
           bulk_g2s(sb + (lane - kGvKB) * kGvBBytes, op + (size_t)((c0 / kGvBK) + lane - kGvKB) * 512, 512, &full[st]);
       }
@@ -275,7 +305,8 @@ __global__ void __launch_bounds__(kGvThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       int kbg = 0, sg = 0;
-      for (int u = u0; u < u1; ++u) {
+      for (int uu = u0; uu < u1; ++uu) {
+      const int u = unit(uu);
         const int nkb = gv_nkb(a, u % g.chunks);
         for (int kb = 0; kb < nkb; kb += kGvKB, ++sg) {
           const int st = sg % kGvStages;
@@ -322,7 +353,8 @@ __global__ void __launch_bounds__(kGvThreads, 1)
     const float mw = (float)a.mw;
     double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
     int kbg = 0;
-    for (int u = u0; u < u1; ++u) {
+    for (int uu = u0; uu < u1; ++uu) {
+      const int u = unit(uu);
       const int tile = u / g.chunks, ch = u % g.chunks;
       const int nkb = gv_nkb(a, ch);
       float ah = 0.f, al = 0.f, bh = 0.f, bl = 0.f;

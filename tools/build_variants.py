@@ -178,6 +178,12 @@ VARIANTS = {
     "gv_fine_i2": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 2}),
     "gv_fine_i4": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 4}),
     "gv_zatom": ("ms_rhs_fast.cu", {"MS_GV_ZATOM": 1}),
+    "gv_rev0": ("ms_rhs_fast.cu", {"MS_GV_REV": 0}),
+    "gv_rev1": ("ms_rhs_fast.cu", {"MS_GV_REV": 1}),
+    "gv_keep32n": ("ms_rhs_fast.cu", {"MS_GV_KEEPKB": 32, "MS_GV_KEEPPOL": 1}),
+    "gv_keep16n": ("ms_rhs_fast.cu", {"MS_GV_KEEPKB": 16, "MS_GV_KEEPPOL": 1}),
+    "gv_keep32l": ("ms_rhs_fast.cu", {"MS_GV_KEEPKB": 32, "MS_GV_KEEPPOL": 2}),
+    "gv_keep16l": ("ms_rhs_fast.cu", {"MS_GV_KEEPKB": 16, "MS_GV_KEEPPOL": 2}),
     "gv_fine_s12": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 1, "MS_GV_STAGES": 12}),
     "gv_fine_s8": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 1, "MS_GV_STAGES": 8}),
     "gv_kb2_s6z": ("ms_rhs_fast.cu", {"MS_GV_KB": 2, "MS_GV_STAGES": 6, "MS_GV_ZATOM": 1}),
