@@ -87,6 +87,17 @@ constexpr int kGvGroups = MS_GV_GROUPS;       // TMEM groups (k-blocks between i
 #endif
 constexpr int kGvBatch = MS_GV_BATCH;         // k-blocks the accumulators read per TMEM round trip
 static_assert(kGvBatch <= kGvGroups, "accumulator batch");
+// MS_GV_UISSUE: warp-uniform MMA issuer (descriptors and barrier addresses in uniform registers)
+#ifndef MS_GV_UISSUE
+#define MS_GV_UISSUE 1
+#endif
+// MS_GV_PRE: the prologue runs before griddepcontrol.wait; MS_GV_COMB: batched loads in the chunk combine
+#ifndef MS_GV_PRE
+#define MS_GV_PRE 1
+#endif
+#ifndef MS_GV_COMB
+#define MS_GV_COMB 1
+#endif
 #ifndef MS_GV_EXP
 #define MS_GV_EXP 0  // timing experiments only (results wrong): 1 = accumulators skip the TMEM loads
 #endif
@@ -150,7 +161,7 @@ __device__ __forceinline__ uint32_t gv_pack(__half lo_col, __half hi_col) {
 #ifndef MS_GV_REV
 #define MS_GV_REV 1
 #endif
-static __device__ unsigned char g_gv_rev[4096];
+static __device__ unsigned int g_gv_rev[4096];
 // MS_GV_KEEPKB: the last MS_GV_KEEPKB k-blocks of a CTA's stream are read with
 // policy MS_GV_KEEPPOL (1 evict-normal, 2 evict-last) instead of evict-first, so
 // more of what the next (reversed) sweep reads first survives in L2
@@ -172,9 +183,11 @@ __global__ void __launch_bounds__(kGvThreads, 1)
     k_rhs_tc16(RhsArgs a, GvArgs g) {
   static_assert(KS == MS_K_F16, "tc16 sweep: f16 K");
   msb::count_launch();
+#if !MS_GV_PRE
   pdl_enter();
   if (stage_skip(a.ctl, a.l, a.gate)) return;
   sweep_count(a);
+#endif
   extern __shared__ __align__(1024) unsigned char gv_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gv_raw) + 1023) & ~uintptr_t(1023));
@@ -193,9 +206,9 @@ __global__ void __launch_bounds__(kGvThreads, 1)
 
   __shared__ int s_rev;
   if (threadIdx.x == 0) {
-    const int r = MS_GV_REV ? (int)g_gv_rev[blockIdx.x & 4095] : 0;
-    s_rev = r;
-    if (MS_GV_REV) g_gv_rev[blockIdx.x & 4095] = (unsigned char)(r ^ 1);
+    // one L2 atomic: coherent whatever this SM's L1 holds (the order is free, so a
+    // stale toggle could only cost the L2 reuse, never a result)
+    s_rev = MS_GV_REV ? (int)(atomicXor(&g_gv_rev[blockIdx.x & 4095], 1u) & 1u) : 0;
     for (int s = 0; s < kGvStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -225,6 +238,17 @@ __global__ void __launch_bounds__(kGvThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+#if MS_GV_PRE
+  // the prologue above (barriers, zero rows, TMEM) touches nothing the previous
+  // kernel writes, so under programmatic dependent launch it overlaps that
+  // kernel's tail; everything below reads its results
+  pdl_enter();
+  if (stage_skip(a.ctl, a.l, a.gate)) {
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kGvTmemCols));
+    return;
+  }
+  sweep_count(a);
+#endif
   bool nonfinite = false;
   const int rev = s_rev;
   // the CTA's k-th unit this launch
@@ -303,6 +327,64 @@ __global__ void __launch_bounds__(kGvThreads, 1)
     }
 #endif
   } else if (warp == 1) {
+#if MS_GV_UISSUE
+    // MMA issuer, warp-uniform: the whole warp walks the loops and waits (every
+    // address, descriptor and counter stays in uniform registers); one elected
+    // lane issues the tcgen05 instructions. Descriptors are a per-stage base
+    // plus a 16-byte-unit offset (no carry: the ring lies below 256 KB).
+    {
+      const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t idesc = g.idesc;
+      int kbg = 0, sg = 0;
+      for (int uu = u0; uu < u1; ++uu) {
+        const int u = unit(uu);
+        const int nkb = gv_nkb(a, u % g.chunks);
+        for (int kb = 0; kb < nkb; kb += kGvKB, ++sg) {
+          const int st = sg % kGvStages;
+          tc_wait(&full[st], (sg / kGvStages) & 1);
+          const uint32_t sa = smem_u32(smem + (size_t)st * kGvStageBytes);
+          const uint32_t sb = sa + kGvKB * kGvABytes;
+          const uint64_t adesc0 = umma_smem_desc(sa);
+#if MS_GV_ZATOM
+          const uint32_t zat = smem_u32(zero_atom);
+#else
+          const uint64_t bdesc0 = umma_smem_desc(sb);
+#endif
+#pragma unroll
+          for (int j = 0; j < kGvKB; ++j, ++kbg) {
+            const int grp = kbg % kGvGroups;
+            if (kbg >= kGvGroups) tc_wait(&tempty[grp], ((kbg / kGvGroups) & 1) ^ 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < kGvBK / 16; ++k) {
+                const uint64_t adesc = adesc0 + (uint64_t)((j * kGvABytes + k * 32) >> 4);
+#if MS_GV_ZATOM
+                const uint64_t bdesc =
+                    umma_smem_desc_sbo(sb + j * kGvBBytes + k * 32, zat - (sb + j * kGvBBytes));
+#else
+                const uint64_t bdesc = bdesc0 + (uint64_t)((j * kGvBBytes + k * 32) >> 4);
+#endif
+                asm volatile(
+                    "{\n .reg .pred p;\n setp.ne.b32 p, 0, 0;\n"
+                    " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                        tmem_u + (uint32_t)(grp * 64 + k * 16)),
+                    "l"(adesc), "l"(bdesc), "r"(idesc));
+              }
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                               smem_u32(&tfull[grp]))
+                           : "memory");
+              if (j == kGvKB - 1)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(&empty[st]))
+                             : "memory");
+            }
+            __syncwarp();
+          }
+        }
+      }
+    }
+#else
     if (lane == 0) {  // MMA issuer
       int kbg = 0, sg = 0;
       for (int uu = u0; uu < u1; ++uu) {
@@ -344,6 +426,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
         }
       }
     }
+#endif
   } else {
     // accumulators: warp%4 = TMEM lane quarter; row rr of the tile
     const int q4 = warp & 3;
@@ -410,11 +493,27 @@ __global__ void __launch_bounds__(kGvThreads, 1)
         if (row < a.row1) {
           float2 p = __ldcg(pt + rr);
           float A = p.x, B = p.y;
+#if MS_GV_COMB
+          // the chunk sums in batches of 8 independent loads, added in chunk order
+          for (int c0 = 1; c0 < g.chunks; c0 += 8) {
+            float2 q[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              q[e] = c0 + e < g.chunks ? __ldcg(pt + (int64_t)(c0 + e) * kGvBM + rr) : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (c0 + e < g.chunks) {
+                A = __fadd_rn(A, q[e].x);
+                B = __fadd_rn(B, q[e].y);
+              }
+          }
+#else
           for (int c = 1; c < g.chunks; ++c) {
             p = __ldcg(pt + (int64_t)c * kGvBM + rr);
             A = __fadd_rn(A, p.x);
             B = __fadd_rn(B, p.y);
           }
+#endif
           const float si = gin[2 * row], ci = gin[2 * row + 1];
           const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(ci, A), __fmul_rn(si, B)));
           MS_CHECK(row >= a.row0 && row < a.row1, "tc16 sweep: output row outside the handle");

@@ -10,6 +10,15 @@ namespace msb {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// one lane of the (converged) warp: elect.sync
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // bounded mbarrier wait: a pipeline bug traps (kernel error, process exits)
 // instead of hanging the GPU
 __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {

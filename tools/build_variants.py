@@ -187,6 +187,15 @@ VARIANTS = {
     "gv_fine_s12": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 1, "MS_GV_STAGES": 12}),
     "gv_fine_s8": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 1, "MS_GV_STAGES": 8}),
     "gv_kb2_s6z": ("ms_rhs_fast.cu", {"MS_GV_KB": 2, "MS_GV_STAGES": 6, "MS_GV_ZATOM": 1}),
+    # round 2, fourth session: warp-uniform MMA issuer, prologue before griddepcontrol.wait, batched combine
+    "gv_old": ("ms_rhs_fast.cu", {"MS_GV_UISSUE": 0, "MS_GV_PRE": 0, "MS_GV_COMB": 0}),
+    "gv_u": ("ms_rhs_fast.cu", {"MS_GV_UISSUE": 1, "MS_GV_PRE": 0, "MS_GV_COMB": 0}),
+    "gv_uc": ("ms_rhs_fast.cu", {"MS_GV_UISSUE": 1, "MS_GV_PRE": 0, "MS_GV_COMB": 1}),
+    "gv_new": ("ms_rhs_fast.cu", {}),
+    "gv_new_fine": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1}),
+    "gv_new_fine_i1": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 1}),
+    "gv_new_kb2": ("ms_rhs_fast.cu", {"MS_GV_KB": 2, "MS_GV_STAGES": 6, "MS_GV_ZATOM": 1}),
+    "gv_new_zatom": ("ms_rhs_fast.cu", {"MS_GV_ZATOM": 1}),
     "keep0": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 0}),
     "keep2": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 2}),
     "keep4": ("ms_rhs_fast.cu", {"MS_TMA_KEEP": 4}),
