@@ -374,7 +374,7 @@ size_t bufs_bytes(const ms_system* s, int64_t log_cap) {
   total += (kMaxStages + 1) * vec;                       // kb
   total += 3 * vec;                                      // xn, xt, scratch
   total += 2 * al256(sizeof(double) * 2 * s->ld);        // gin, gin2
-  total += al256((size_t)(s->ld / 64 + 1) * 512);         // op16
+  total += 2 * al256((size_t)(s->ld / 64 + 1) * 512);     // op16, op16b
   total += al256(sizeof(double) * s->ld);                // rowc
   total += al256(sizeof(double) * s->n);                 // fvc
   total += al256(sizeof(double) * fin_blocks);           // part
@@ -400,7 +400,8 @@ void carve_bufs(const ms_system* s, char* base, int64_t log_cap, Bufs& B) {
   B.gin = take(sizeof(double) * 2 * s->ld);
   B.gin2 = take(sizeof(double) * 2 * s->ld);
   B.op16 = take((size_t)(s->ld / 64 + 1) * 512);
-  if (!s->gv) B.op16 = nullptr;  // written by the preps only for the tensor-core sweep
+  B.op16b = take((size_t)(s->ld / 64 + 1) * 512);
+  if (!s->gv) B.op16 = B.op16b = nullptr;  // written by the preps only for the tensor-core sweep
   B.rowc = take(sizeof(double) * s->ld);
   B.fvc = reinterpret_cast<double*>(take(sizeof(double) * s->n));
   B.part = reinterpret_cast<double*>(take(sizeof(double) * fin_blocks));
@@ -719,8 +720,10 @@ bool launch_stage(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_sta
                   void*& gin_now, const EvalSpec* en, const ms_stage_prec* spn) {
   Bufs B = s->B;
   B.gin = gin_now;
+  B.op16 = gin_now == s->B.gin ? s->B.op16 : s->B.op16b;  // the operand image travels with its column buffer
   const bool split = s->mkind == MD_KUR && s->rhs_mode == MS_RHS_FAST;
   RhsLaunch L{s->mkind, split, is32(sp.sum_prec), is32(sp.g_prec), s->ks, s->sms, st};
+  L.tc16 = split && is32(sp.sum_prec) && is32(sp.g_prec) && tc16_selected(rhs_args(s, B, e, sp), s->ks);
   const bool whole = s->row0 == 0 && s->row1 == s->n;
   const bool can = en && whole && !s->fixture && split && fuse_next_ok(L, is32(spn->f_prec), is32(spn->g_prec));
   if (!prepped && !can) {
@@ -739,6 +742,7 @@ bool launch_stage(ms_system* s, cudaStream_t st, const EvalSpec& e, const ms_sta
   if (can) {
     Bufs B2 = s->B;
     B2.gin = other;
+    B2.op16 = other == s->B.gin ? s->B.op16 : s->B.op16b;
     pn = prep_args(s, B2, *en, *spn);
     L.next = &pn;
     L.next_fs32 = is32(spn->f_prec);

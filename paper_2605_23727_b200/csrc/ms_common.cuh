@@ -272,6 +272,7 @@ struct Bufs {
   void* gin;                     // GS-typed column data (2 * ld doubles)
   void* gin2;                    // the other column buffer: a sweep that runs the next stage's prep writes it
   void* op16;                    // f16 operand image of the column data for the tensor-core sweep, or null
+  void* op16b;                   // gin2's operand image (a tensor-core sweep that runs the next stage's prep writes it)
   void* rowc;                    // GS-typed per-row G constant (CC prefactor)
   double* fvc;                   // F of the coupled slot, per agent
   double* part;                  // per-block partials of finalize

@@ -18,7 +18,12 @@ struct RhsLaunch {
   const PrepArgs* next = nullptr;
   bool next_fs32 = false, next_gs32 = false;
   bool* fused = nullptr;
+  bool tc16 = false;  // this sweep runs on the tensor cores (tc16_selected)
 };
+
+// whether launch_rhs_fast sends this binary32 split-Kuramoto sweep to the
+// tensor-core kernel (f16 K with tile images, operand image present, size / MS_SWEEP)
+bool tc16_selected(const RhsArgs& a, int ks);
 
 // whether launch_rhs_fast folds the next stage's prep (row F/G precisions
 // next_fs32/next_gs32) into this sweep: the split Kuramoto's row-copy TMA sweep

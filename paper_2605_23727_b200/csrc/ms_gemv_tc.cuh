@@ -178,9 +178,15 @@ __device__ __forceinline__ int gv_nkb(const RhsArgs& a, int ch) {
   return (cols + kGvBK - 1) / kGvBK;
 }
 
-template <int KS>
+// NEXT: the CTA that completes a tile also runs the next stage's prep (pn) for
+// the tile's rows -- every per-agent input of that prep is row-local (x, the k
+// slots including the one just written by the same thread), and its column data
+// and operand image go to the other buffers (pn.B.gin / pn.B.op16: this stage's
+// are still being read). prep_agent's arithmetic, so bit-identical to k_prep +
+// sweep; host side: launch_stage (fuse_next_ok in ms_rhs_fast.cu).
+template <int KS, bool NEXT = false>
 __global__ void __launch_bounds__(kGvThreads, 1)
-    k_rhs_tc16(RhsArgs a, GvArgs g) {
+    k_rhs_tc16(RhsArgs a, GvArgs g, PrepArgs pn) {
   static_assert(KS == MS_K_F16, "tc16 sweep: f16 K");
   msb::count_launch();
 #if !MS_GV_PRE
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
   }
   sweep_count(a);
 #endif
-  bool nonfinite = false;
+  bool nonfinite = false, nfp = false;
   const int rev = s_rev;
   // the CTA's k-th unit this launch
   auto unit = [&](int uu) { return rev ? u1 - 1 - (uu - u0) : uu; };
@@ -436,6 +442,8 @@ __global__ void __launch_bounds__(kGvThreads, 1)
     const float mw = (float)a.mw;
     double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
     int kbg = 0;
+    PrepCtx pc{};
+    if constexpr (NEXT) pc = prep_ctx(pn);
     for (int uu = u0; uu < u1; ++uu) {
       const int u = unit(uu);
       const int tile = u / g.chunks, ch = u % g.chunks;
@@ -520,6 +528,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
           const double o = ws_add(a.fvc[row], (double)coup, a.ws32);
           push_row(a.push, out + (int64_t)row * a.d + a.cs, o);
           nonfinite |= !isfinite(o);
+          if constexpr (NEXT) nfp |= prep_agent<MD_KUR, float, float>(pn, pc, row);
         }
         if (warp == 2 && lane == 0) g.cnt[tile] = 0;  // ready for the next launch
       }
@@ -528,6 +537,16 @@ __global__ void __launch_bounds__(kGvThreads, 1)
   }
   if (warp >= 2) push_fence(a.push);
   if (warp >= 2 && __any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(a.nf_mask, 1 << a.l);
+  if constexpr (NEXT) {
+    if (warp >= 2 && __any_sync(0xffffffffu, nfp) && lane == 0) atomicOr(a.nf_mask, 1 << pn.l);
+    if (blockIdx.x == 0 && warp >= 2) {  // the padding columns of the target buffer (k_prep does the same)
+      float* gp = reinterpret_cast<float*>(pn.B.gin);
+      for (int j = pn.md.n + (int)threadIdx.x - 64; j < pn.ld; j += 128) {
+        gp[2 * j] = 0.f;
+        gp[2 * j + 1] = 0.f;
+      }
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

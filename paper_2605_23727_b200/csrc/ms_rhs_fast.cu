@@ -48,18 +48,20 @@ bool use_tc16(const RhsArgs& a, int ks) {
   return a.ld >= 16384;
 }
 
-void go_tc16(const RhsLaunch& L, const RhsArgs& a) {
+template <bool NEXT>
+void go_tc16(const RhsLaunch& L, const RhsArgs& a, const PrepArgs& pn = PrepArgs{}) {
   const GvRes* r = static_cast<const GvRes*>(a.tc16);
+  auto kern = k_rhs_tc16<MS_K_F16, NEXT>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_rhs_tc16<MS_K_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGvSmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGvSmem);
     if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tc16 attribute: ") + cudaGetErrorString(e));
     attr_done = true;
   }
   GvArgs g{r->kt, r->part, r->cnt, r->tiles, r->chunks, r->kblocks, kGvIdesc};
   const int units = r->tiles * r->chunks;
   const int grid = units < L.num_sms ? units : L.num_sms;
-  cudaError_t e = launch_k(k_rhs_tc16<MS_K_F16>, grid, kGvThreads, kGvSmem, L.stream, a, g);
+  cudaError_t e = launch_k(kern, grid, kGvThreads, kGvSmem, L.stream, a, g, pn);
   if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tc16 launch: ") + cudaGetErrorString(e));
 }
 
@@ -120,7 +122,12 @@ void go(const RhsLaunch& L, const RhsArgs& a) {
   // register-fed sweep stays ahead (profiles/r1_tune_tma.txt)
   if constexpr (MODEL == MD_KUR && SPLIT && KS == MS_K_F16 && sizeof(SS) == 4 && sizeof(GS) == 4) {
     if (use_tc16(a, KS)) {
-      go_tc16(L, a);
+      if (L.next && L.tc16 && fuse_next_ok(L, L.next_fs32, L.next_gs32)) {
+        go_tc16<true>(L, a, *L.next);
+        if (L.fused) *L.fused = true;
+        return;
+      }
+      go_tc16<false>(L, a);
       return;
     }
   }
@@ -273,13 +280,17 @@ bool launch_eval_fused(const RhsLaunch& L, const PrepArgs& p, const RhsArgs& a, 
   }
 }
 
+bool tc16_selected(const RhsArgs& a, int ks) { return use_tc16(a, ks); }
+
 bool fuse_next_ok(const RhsLaunch& L, bool next_fs32, bool next_gs32) {
   const char* f = std::getenv("MS_FUSE_NEXT");  // read per launch (graphs capture it once)
   const bool on = !(f && std::strcmp(f, "off") == 0);
   const char* v = std::getenv("MS_SWEEP");
   const bool tma = !(v && (std::strcmp(v, "ldg") == 0 || std::strcmp(v, "tile") == 0 || std::strcmp(v, "small") == 0));
   // the kernel runs prep_agent<KUR, FS = SS, GS>: the next row's F must be this row's sum format
-  return on && tma && L.model == MD_KUR && L.split && L.ks == MS_K_F32 && next_fs32 == L.ss32 && next_gs32 == L.gs32;
+  const bool f32_tma = tma && L.ks == MS_K_F32;
+  const bool f16_tc = L.tc16 && L.ks == MS_K_F16 && L.ss32 && L.gs32;  // the tensor-core sweep (binary32 rows)
+  return on && L.model == MD_KUR && L.split && (f32_tma || f16_tc) && next_fs32 == L.ss32 && next_gs32 == L.gs32;
 }
 
 bool pdl_enabled() {

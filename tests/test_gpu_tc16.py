@@ -121,3 +121,41 @@ def test_tc16_non_finite_column_poisons_every_row_like_the_cuda_core_sweep(gpu, 
     assert np.array_equal(np.isfinite(a), np.isfinite(b))
     assert not np.isfinite(a).any()
     dev.close()
+
+
+@pytest.mark.parametrize("n", [1024, 4352])
+@pytest.mark.parametrize("storage32", [False, True])
+def test_tc16_folded_next_prep_is_bitwise_the_separate_prep(gpu, n, storage32, monkeypatch):
+    """The tensor-core sweep runs the next stage's prep for the rows of every
+    tile it completes (k_rhs_tc16<NEXT>, launch_stage in ms_api.cu; column data
+    and operand image into the other buffers): the whole solve -- final state,
+    counts, evaluation tallies and every step record -- must equal the solve
+    with k_prep launched for every stage (MS_FUSE_NEXT=off)."""
+    from paper_2605_23727_b200.configs import config2_kuramoto
+    from paper_2605_23727_b200.precision import PolicyVariant, policy_for
+    from paper_2605_23727_b200.solver import SolveStatus
+    monkeypatch.setenv("MS_SWEEP", "tc16")
+    w = config2_kuramoto(n=n, rtol=1e-6, k_storage="f16")
+    w.tf = 5.0
+    pol = policy_for(PolicyVariant.Single) if storage32 else w.policy
+    res, launches = [], []
+    from paper_2605_23727_b200 import _abi
+    for f in ("on", "off"):
+        monkeypatch.setenv("MS_FUSE_NEXT", f)
+        dev = DeviceSystem(w.spec)  # its own graph cache: the env is read while capturing
+        monkeypatch.setenv("MS_LOOP", "host")  # plain launches, so the launch counter sees the fold
+        l0 = _abi.lib().ms_launch_count()
+        res.append(S.solve(dev, w.x0, w.t0, w.tf, pol, w.cfg))
+        launches.append(_abi.lib().ms_launch_count() - l0)
+        monkeypatch.delenv("MS_LOOP")
+        dev.close()
+    a, b = res
+    assert a.status == b.status == SolveStatus.Completed
+    assert (a.n_accepted, a.n_failed) == (b.n_accepted, b.n_failed)
+    assert a.flops.rhs_evals == b.flops.rhs_evals
+    assert np.array_equal(a.final_state, b.final_state)
+    assert [(r.t, r.h, r.err, r.accepted) for r in a.step_log] == [(r.t, r.h, r.err, r.accepted) for r in b.step_log]
+    # the fold is live: two k_prep launches fewer per attempt
+    attempts = a.n_accepted + a.n_failed
+    print(f"n={n}: launches folded {launches[0]} vs separate {launches[1]} over {attempts} attempts")
+    assert launches[1] - launches[0] >= 2 * attempts - 2
