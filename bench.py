@@ -141,9 +141,11 @@ def sweep_kernel(kdtype, whole):
         label = f"k_rhs_tma<f32 sum, f32 G, K f32, NEXT={nxt}> (cp.async.bulk-fed K sweep" + \
                 (", folds the next stage's prep)" if nxt else ")")
     elif kdtype == "f16" and os.environ.get("MS_SWEEP", "tc16") == "tc16":
-        name = "void k_rhs_tc16<2>"
-        label = ("k_rhs_tc16<K f16> (tcgen05 M128 N16 sweep over 16 KB K tile images, f16 hi+lo operands, "
-                 "binary32 sums of the 16-column dot products)")
+        nxt = 1 if whole and os.environ.get("MS_FUSE_NEXT", "on") != "off" else 0
+        name = f"void k_rhs_tc16<2, {nxt}>"
+        label = (f"k_rhs_tc16<K f16, NEXT={nxt}> (tcgen05 M128 N16 sweep over 16 KB K tile images, f16 hi+lo "
+                 "operands, binary32 sums of the 16-column dot products" +
+                 (", folds the next stage's prep)" if nxt else ")"))
         kdtype = "f16tc"
     else:
         ks = {"f32": 1, "f16": 2, "bf16": 3}[kdtype]
