@@ -60,7 +60,12 @@ void go_tc16(const RhsLaunch& L, const RhsArgs& a, const PrepArgs& pn = PrepArgs
   }
   GvArgs g{r->kt, r->part, r->cnt, r->tiles, r->chunks, r->kblocks, kGvIdesc};
   const int units = r->tiles * r->chunks;
-  const int grid = units < L.num_sms ? units : L.num_sms;
+  static const int cap = [] {  // MS_GV_GRID: CTAs (tuning; default one per SM)
+    const char* v = std::getenv("MS_GV_GRID");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int slots = cap > 0 && cap < L.num_sms ? cap : L.num_sms;
+  const int grid = units < slots ? units : slots;
   cudaError_t e = launch_k(kern, grid, kGvThreads, kGvSmem, L.stream, a, g, pn);
   if (e != cudaSuccess) throw std::runtime_error(std::string("rhs_tc16 launch: ") + cudaGetErrorString(e));
 }
