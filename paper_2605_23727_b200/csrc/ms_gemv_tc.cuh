@@ -98,15 +98,23 @@ static_assert(kGvBatch <= kGvGroups, "accumulator batch");
 #ifndef MS_GV_COMB
 #define MS_GV_COMB 1
 #endif
+// MS_GV_KBFULL: one full barrier per k-block of a stage (the MMAs of a k-block start when its 16 KB have
+// landed, while the rest of the stage is still arriving); the stage is still released as a whole
+#ifndef MS_GV_KBFULL
+#define MS_GV_KBFULL 0
+#endif
 #ifndef MS_GV_EXP
 #define MS_GV_EXP 0  // timing experiments only (results wrong): 1 = accumulators skip the TMEM loads
 #endif
+constexpr int kGvNFull = (MS_GV_KBFULL && !MS_GV_FINE) ? kGvStages * kGvKB : kGvStages;
 constexpr int kGvThreads = 6 * 32;
 constexpr size_t kGvZeroBytes = MS_GV_ZATOM ? 1024 : 0;  // the shared zero atom (rows 8-15 of every B tile)
 constexpr size_t kGvSmem = 1024 + (size_t)kGvStages * kGvStageBytes + kGvZeroBytes + 256;
 static_assert(!MS_GV_FINE || (kGvKB == 1 && kGvChunk % (kGvIssue * kGvBK) == 0), "fine ring layout");
 constexpr uint32_t kGvTmemCols = kGvGroups * 64;  // kGvGroups x 4 MMAs x 16 columns (power of two)
 static_assert(kGvTmemCols == 256 || kGvTmemCols == 512, "TMEM allocation");
+static_assert(!MS_GV_KBFULL || MS_GV_UISSUE, "per-k-block full barriers: uniform issuer only");
+static_assert((kGvNFull + kGvStages + 2 * kGvGroups) * 8 + 4 <= 256, "barrier block");
 
 // per-handle resources (created with the system, ms_api.cu)
 struct GvRes {
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gv_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* zero_atom = smem + (size_t)kGvStages * kGvStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(zero_atom + kGvZeroBytes);
-  uint64_t* empty = full + kGvStages;
+  uint64_t* empty = full + kGvNFull;
   uint64_t* tfull = empty + kGvStages;
   uint64_t* tempty = tfull + kGvGroups;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + kGvGroups);
@@ -215,10 +223,8 @@ __global__ void __launch_bounds__(kGvThreads, 1)
     // one L2 atomic: coherent whatever this SM's L1 holds (the order is free, so a
     // stale toggle could only cost the L2 reuse, never a result)
     s_rev = MS_GV_REV ? (int)(atomicXor(&g_gv_rev[blockIdx.x & 4095], 1u) & 1u) : 0;
-    for (int s = 0; s < kGvStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
+    for (int s = 0; s < kGvNFull; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kGvStages; ++s) mbar_init(&empty[s], 1);
     for (int q = 0; q < kGvGroups; ++q) {
       mbar_init(&tfull[q], 1);
       mbar_init(&tempty[q], 4);
@@ -317,18 +323,23 @@ __global__ void __launch_bounds__(kGvThreads, 1)
         unsigned char* sa = smem + (size_t)st * kGvStageBytes;
         unsigned char* sb = sa + kGvKB * kGvABytes;
         const int c0 = ch * kGvChunk + kb * kGvBK;
+#if MS_GV_KBFULL
+        if (lane < kGvKB) mbar_expect_tx(&full[st * kGvKB + lane], kGvABytes + 512);
+#else
         if (lane == 0) mbar_expect_tx(&full[st], kGvKB * (kGvABytes + 512));
+#endif
         __syncwarp();
         MS_CHECK(tile < g.tiles && (c0 / kGvBK) + kGvKB <= g.kblocks && (c0 % kGvBK) == 0,
                  "tc16 sweep: tile image outside the handle's K");
         uint64_t upol = pol;
         if (MS_GV_KEEPKB > 0 && a.k_stream && uu == u1 - 1 && kb + kGvKB > nkb - MS_GV_KEEPKB)
           upol = MS_GV_KEEPPOL == 2 ? l2_evict_last() : l2_evict_normal();
+        uint64_t* fb = MS_GV_KBFULL ? &full[st * kGvKB + (lane % kGvKB)] : &full[st];
         if (lane < kGvKB)  // one contiguous 16 KB tile image per k-block
           bulk_g2s_hint(sa + lane * kGvABytes,
-                        g.kt + ((int64_t)tile * g.kblocks + (c0 / kGvBK) + lane) * kGvABytes, kGvABytes, &full[st], upol);
+                        g.kt + ((int64_t)tile * g.kblocks + (c0 / kGvBK) + lane) * kGvABytes, kGvABytes, fb, upol);
         else if (lane < 2 * kGvKB)  // and the operand rows 0-3 of its B tile (the prep's image)
-          bulk_g2s(sb + (lane - kGvKB) * kGvBBytes, op + (size_t)((c0 / kGvBK) + lane - kGvKB) * 512, 512, &full[st]);
+          bulk_g2s(sb + (lane - kGvKB) * kGvBBytes, op + (size_t)((c0 / kGvBK) + lane - kGvKB) * 512, 512, fb);
       }
     }
 #endif
@@ -347,7 +358,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
         const int nkb = gv_nkb(a, u % g.chunks);
         for (int kb = 0; kb < nkb; kb += kGvKB, ++sg) {
           const int st = sg % kGvStages;
-          tc_wait(&full[st], (sg / kGvStages) & 1);
+          if (!(MS_GV_KBFULL && !MS_GV_FINE)) tc_wait(&full[st], (sg / kGvStages) & 1);
           const uint32_t sa = smem_u32(smem + (size_t)st * kGvStageBytes);
           const uint32_t sb = sa + kGvKB * kGvABytes;
           const uint64_t adesc0 = umma_smem_desc(sa);
@@ -359,6 +370,7 @@ __global__ void __launch_bounds__(kGvThreads, 1)
 #pragma unroll
           for (int j = 0; j < kGvKB; ++j, ++kbg) {
             const int grp = kbg % kGvGroups;
+            if (MS_GV_KBFULL && !MS_GV_FINE) tc_wait(&full[st * kGvKB + j], (sg / kGvStages) & 1);
             if (kbg >= kGvGroups) tc_wait(&tempty[grp], ((kbg / kGvGroups) & 1) ^ 1);
             tc_fence_after();
             if (elect_one()) {
