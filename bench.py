@@ -332,7 +332,10 @@ def c5_line(steps, cpu):
            "contraction": {"kernel": ("k_tc_gemm2 (tcgen05.mma.cta_group::2 kind::f16, 256-row x 128-trajectory pair "
                                       "tiles, hi+lo bf16 operands, sums in windows of "
                                       f"{os.environ.get('MS_TC_WINDOW', '2')} k-blocks added in binary32)"),
-                           "ms": rhs.value, "TFLOPs_algorithmic": tf, "peak_bf16_TFLOPs": peak, "frac": tf / peak}}
+                           "ms": rhs.value, "TFLOPs_algorithmic": tf, "peak_bf16_TFLOPs": peak, "frac": tf / peak,
+                           # the tensor pipe executes both operand terms (hi and lo): twice the algorithmic flops,
+                           # on the 128 SMs the 64 pair tiles occupy
+                           "TFLOPs_mma_issued": 2.0 * tf, "frac_mma_issued": 2.0 * tf / peak}}
     bat.close()
     dev.close()
     if cpu:
