@@ -519,6 +519,11 @@ __device__ __forceinline__ void cluster_sync_all() {
 // end-of-kernel pair barrier without release semantics: it only orders the two
 // CTAs' TMEM use before the collective dealloc; a .release arrive compiles to
 // MEMBAR.ALL.GPU, which makes every CTA wait for its k stores to drain first
+// MS_T2_DRAIN_RELAXED: the drain warps' "window buffer read" arrive on the leader's barrier carries no
+// memory release (see the arrive in the drain loop)
+#ifndef MS_T2_DRAIN_RELAXED
+#define MS_T2_DRAIN_RELAXED 1
+#endif
 #ifndef MS_T2_END_RELAXED
 #define MS_T2_END_RELAXED 1
 #endif
@@ -905,8 +910,17 @@ __global__ void __cluster_dims__(2, 1, 1) MS_T2_BOUNDS
             tc_fence_before();
             __syncwarp();
             if (lane == 0)
+#if MS_T2_DRAIN_RELAXED
+              // the buffer's reads are complete (tcgen05.wait::ld) and fenced for the issuer
+              // (tcgen05.fence::before_thread_sync); no memory of this thread has to be
+              // published. A .release.cluster arrive compiles to MEMBAR.ALL.GPU + ERRBAR in
+              // every drain warp, once per window, in the path that frees the buffer
+              asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_empty0 + 8u * buf)
+                           : "memory");
+#else
               asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_empty0 + 8u * buf)
                            : "memory");
+#endif
           }
 #ifndef MS_T2_EXP_DRAIN  // timing experiments only (results wrong): 1 = no adds into the totals
 #define MS_T2_EXP_DRAIN 0
