@@ -103,6 +103,11 @@ static_assert(kGvBatch <= kGvGroups, "accumulator batch");
 #ifndef MS_GV_KBFULL
 #define MS_GV_KBFULL 0
 #endif
+// MS_GV_OWN: tiles whose chunks all belong to one CTA skip the partial buffer, the fences and the ticket
+#ifndef MS_GV_OWN
+#define MS_GV_OWN 0  // measured slower: 6.60 vs 6.91 TB/s per launch (profiles/r2_tc16.txt)
+#endif
+constexpr int kGvMaxOwn = 32;  // chunks per tile the owner keeps (N <= 65536)
 #ifndef MS_GV_EXP
 #define MS_GV_EXP 0  // timing experiments only (results wrong): 1 = accumulators skip the TMEM loads
 #endif
@@ -453,7 +458,8 @@ __global__ void __launch_bounds__(kGvThreads, 1)
     const float* gin = reinterpret_cast<const float*>(a.gin);
     const float mw = (float)a.mw;
     double* out = a.kb[a.out_slot == SLOT_K1 ? a.ctl->k1i : (a.out_slot == SLOT_KLAST ? a.S - a.ctl->k1i : a.out_slot)];
-    int kbg = 0;
+    int kbg = 0, own_done = 0;
+    float2 cs[kGvMaxOwn];  // chunk sums of a tile this CTA owns entirely (MS_GV_OWN)
     PrepCtx pc{};
     if constexpr (NEXT) pc = prep_ctx(pn);
     for (int uu = u0; uu < u1; ++uu) {
@@ -502,38 +508,63 @@ __global__ void __launch_bounds__(kGvThreads, 1)
       }
       MS_CHECK(tile < g.tiles && ch < g.chunks, "tc16 sweep: partial outside the workspace");
       float2* pt = g.part + ((int64_t)tile * g.chunks) * kGvBM;
-      pt[(int64_t)ch * kGvBM + rr] = make_float2(__fadd_rn(ah, al), __fadd_rn(bh, bl));
-      __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (warp == 2 && lane == 0) s_last = (atomicAdd(g.cnt + tile, 1) == g.chunks - 1) ? 1 : 0;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (s_last) {
+      const float2 usum = make_float2(__fadd_rn(ah, al), __fadd_rn(bh, bl));
+      // A tile whose chunks all lie in this CTA's unit range needs no partial buffer,
+      // fence or ticket: its chunk sums wait in the thread's own (local-memory) array and
+      // are combined in the same ascending chunk order when its last unit is done (the
+      // walk is contiguous, so the tile's units follow one another). Same bits either way.
+      const bool owned = MS_GV_OWN && g.chunks <= kGvMaxOwn && tile * g.chunks >= u0 && (tile + 1) * g.chunks <= u1;
+      bool finish;
+      if (owned) {
+        cs[ch] = usum;
+        finish = ++own_done == g.chunks;
+        if (finish) own_done = 0;
+      } else {
+        pt[(int64_t)ch * kGvBM + rr] = usum;
         __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) s_last = (atomicAdd(g.cnt + tile, 1) == g.chunks - 1) ? 1 : 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        finish = s_last != 0;
+        if (finish) __threadfence();
+      }
+      if (finish) {
         const int row = a.row0 + tile * kGvBM + rr;
         if (row < a.row1) {
-          float2 p = __ldcg(pt + rr);
-          float A = p.x, B = p.y;
+          float A, B;
+          if (owned) {
+            A = cs[0].x;
+            B = cs[0].y;
+            for (int c = 1; c < g.chunks; ++c) {
+              A = __fadd_rn(A, cs[c].x);
+              B = __fadd_rn(B, cs[c].y);
+            }
+          } else {
+            float2 p = __ldcg(pt + rr);
+            A = p.x;
+            B = p.y;
 #if MS_GV_COMB
-          // the chunk sums in batches of 8 independent loads, added in chunk order
-          for (int c0 = 1; c0 < g.chunks; c0 += 8) {
-            float2 q[8];
+            // the chunk sums in batches of 8 independent loads, added in chunk order
+            for (int c0 = 1; c0 < g.chunks; c0 += 8) {
+              float2 q[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              q[e] = c0 + e < g.chunks ? __ldcg(pt + (int64_t)(c0 + e) * kGvBM + rr) : make_float2(0.f, 0.f);
+              for (int e = 0; e < 8; ++e)
+                q[e] = c0 + e < g.chunks ? __ldcg(pt + (int64_t)(c0 + e) * kGvBM + rr) : make_float2(0.f, 0.f);
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (c0 + e < g.chunks) {
-                A = __fadd_rn(A, q[e].x);
-                B = __fadd_rn(B, q[e].y);
-              }
-          }
+              for (int e = 0; e < 8; ++e)
+                if (c0 + e < g.chunks) {
+                  A = __fadd_rn(A, q[e].x);
+                  B = __fadd_rn(B, q[e].y);
+                }
+            }
 #else
-          for (int c = 1; c < g.chunks; ++c) {
-            p = __ldcg(pt + (int64_t)c * kGvBM + rr);
-            A = __fadd_rn(A, p.x);
-            B = __fadd_rn(B, p.y);
-          }
+            for (int c = 1; c < g.chunks; ++c) {
+              p = __ldcg(pt + (int64_t)c * kGvBM + rr);
+              A = __fadd_rn(A, p.x);
+              B = __fadd_rn(B, p.y);
+            }
 #endif
+          }
           const float si = gin[2 * row], ci = gin[2 * row + 1];
           const float coup = __fmul_rn(mw, __fsub_rn(__fmul_rn(ci, A), __fmul_rn(si, B)));
           MS_CHECK(row >= a.row0 && row < a.row1, "tc16 sweep: output row outside the handle");
@@ -542,9 +573,9 @@ __global__ void __launch_bounds__(kGvThreads, 1)
           nonfinite |= !isfinite(o);
           if constexpr (NEXT) nfp |= prep_agent<MD_KUR, float, float>(pn, pc, row);
         }
-        if (warp == 2 && lane == 0) g.cnt[tile] = 0;  // ready for the next launch
+        if (!owned && warp == 2 && lane == 0) g.cnt[tile] = 0;  // ready for the next launch
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (!owned) asm volatile("bar.sync 1, 128;" ::: "memory");
     }
   }
   if (warp >= 2) push_fence(a.push);

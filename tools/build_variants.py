@@ -198,6 +198,8 @@ VARIANTS = {
     "gv_new_zatom": ("ms_rhs_fast.cu", {"MS_GV_ZATOM": 1}),
     "t2_rel0": ("ms_batch.cu", {"MS_T2_DRAIN_RELAXED": 0}),
     "t2_rel1": ("ms_batch.cu", {"MS_T2_DRAIN_RELAXED": 1}),
+    "gv_own0": ("ms_rhs_fast.cu", {"MS_GV_OWN": 0}),
+    "gv_own1": ("ms_rhs_fast.cu", {"MS_GV_OWN": 1}),
     "gv_kbfull": ("ms_rhs_fast.cu", {"MS_GV_KBFULL": 1}),
     "gv_kbfull_z": ("ms_rhs_fast.cu", {"MS_GV_KBFULL": 1, "MS_GV_ZATOM": 1}),
     "gv_g8b2": ("ms_rhs_fast.cu", {"MS_GV_BATCH": 2}),
