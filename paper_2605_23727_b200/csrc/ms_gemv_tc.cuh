@@ -108,6 +108,10 @@ static_assert(kGvBatch <= kGvGroups, "accumulator batch");
 #define MS_GV_OWN 0  // measured slower: 6.60 vs 6.91 TB/s per launch (profiles/r2_tc16.txt)
 #endif
 constexpr int kGvMaxOwn = 32;  // chunks per tile the owner keeps (N <= 65536)
+// MS_GV_ATOMREL: the unit-end ticket is one acq_rel atomic after a barrier instead of a fence in every thread
+#ifndef MS_GV_ATOMREL
+#define MS_GV_ATOMREL 1
+#endif
 #ifndef MS_GV_EXP
 #define MS_GV_EXP 0  // timing experiments only (results wrong): 1 = accumulators skip the TMEM loads
 #endif
@@ -521,9 +525,23 @@ __global__ void __launch_bounds__(kGvThreads, 1)
         if (finish) own_done = 0;
       } else {
         pt[(int64_t)ch * kGvBM + rr] = usum;
+#if MS_GV_ATOMREL
+        // the barrier orders the 128 partial stores before thread (warp 2, lane 0), whose
+        // acq_rel ticket publishes them (release) and, for the CTA that takes the last
+        // ticket, orders the other CTAs' partials before its reads (acquire; the readers
+        // follow through the second barrier and read at L2): one fenced atomic per unit
+        // instead of a MEMBAR.ALL.GPU + CCTL.IVALL in every accumulator thread
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) {
+          int tk;
+          asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(tk) : "l"(g.cnt + tile) : "memory");
+          s_last = tk == g.chunks - 1 ? 1 : 0;
+        }
+#else
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (warp == 2 && lane == 0) s_last = (atomicAdd(g.cnt + tile, 1) == g.chunks - 1) ? 1 : 0;
+#endif
         asm volatile("bar.sync 1, 128;" ::: "memory");
         finish = s_last != 0;
         if (finish) __threadfence();

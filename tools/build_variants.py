@@ -198,6 +198,9 @@ VARIANTS = {
     "gv_new_zatom": ("ms_rhs_fast.cu", {"MS_GV_ZATOM": 1}),
     "t2_rel0": ("ms_batch.cu", {"MS_T2_DRAIN_RELAXED": 0}),
     "t2_rel1": ("ms_batch.cu", {"MS_T2_DRAIN_RELAXED": 1}),
+    "gv_ar0": ("ms_rhs_fast.cu", {"MS_GV_ATOMREL": 0}),
+    "gv_ar1": ("ms_rhs_fast.cu", {"MS_GV_ATOMREL": 1}),
+    "gv_ar1_own1": ("ms_rhs_fast.cu", {"MS_GV_ATOMREL": 1, "MS_GV_OWN": 1}),
     "gv_own0": ("ms_rhs_fast.cu", {"MS_GV_OWN": 0}),
     "gv_own1": ("ms_rhs_fast.cu", {"MS_GV_OWN": 1}),
     "gv_kbfull": ("ms_rhs_fast.cu", {"MS_GV_KBFULL": 1}),
