@@ -524,6 +524,9 @@ __device__ __forceinline__ void cluster_sync_all() {
 #ifndef MS_T2_DRAIN_RELAXED
 #define MS_T2_DRAIN_RELAXED 1
 #endif
+#ifndef MS_T2_PRO_RELAXED
+#define MS_T2_PRO_RELAXED 0  // measured no change (the prologue runs under the previous kernel's tail): the release barrier stays
+#endif
 #ifndef MS_T2_END_RELAXED
 #define MS_T2_END_RELAXED 1
 #endif
@@ -688,7 +691,15 @@ __global__ void __cluster_dims__(2, 1, 1) MS_T2_BOUNDS
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
+#if MS_T2_PRO_RELAXED
+  // the barrier inits were published cluster-wide by fence.mbarrier_init.release.cluster,
+  // the TMEM slot is this CTA's own shared memory (__syncthreads): the pair barrier only
+  // has to order execution, and a .release arrive is a MEMBAR.ALL.GPU in every thread
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+#else
   cluster_sync_all();  // the peer's barriers exist before any remote arrive
+#endif
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // the prologue above (barriers, TMEM, tensor-map prefetch) overlaps the
