@@ -8,8 +8,20 @@
 
 #ifdef __CUDACC__
 #define MS_HD __host__ __device__
+// the general double-double path (~1200 operations) is cold in the controller (the 1/q
+// exponents take pow_root): kept out of line so the hot path stays dense in the
+// instruction cache (MS_POW_COLD=0 inlines it again)
+#ifndef MS_POW_COLD
+#define MS_POW_COLD 1
+#endif
+#if MS_POW_COLD
+#define MS_COLD inline __noinline__
+#else
+#define MS_COLD inline
+#endif
 #else
 #define MS_HD
+#define MS_COLD inline
 #endif
 
 namespace msb {
@@ -29,6 +41,8 @@ using std::rint;
 // double-double (~100 bits) rounded once. glibc's pow, the reference's
 // (solver.cpp:416, 448), is correctly rounded in all but ~1e-3 of calls, so
 // this agrees with it far more often than CUDA's pow (<= 2 ulp).
+// libm pow (a long routine) for the starts and fall-backs below: one out-of-line copy
+MS_HD MS_COLD double pow_libm(double x, double y) { return pow(x, y); }
 struct dd {
   double hi, lo;
 };
@@ -96,13 +110,13 @@ MS_HD inline dd dd_log(double x) {
   return dd_add(dd{y0, 0.0}, t);      // one Newton step
 }
 // general path: exp(y log x) in double-double (two dd_exp: ~1200 dependent ops)
-MS_HD inline double pow_cr_general(double x, double y) {
-  if (!(x > 0.0) || !isfinite(x) || !isfinite(y)) return pow(x, y);
+MS_HD MS_COLD double pow_cr_general(double x, double y) {
+  if (!(x > 0.0) || !isfinite(x) || !isfinite(y)) return pow_libm(x, y);
   if (y == 0.0 || x == 1.0) return 1.0;
   const dd l = dd_log(x);
   const dd r = dd_exp(dd_mul_d(l, y));
   const double v = msb_add(r.hi, r.lo);
-  return isfinite(v) ? v : pow(x, y);
+  return isfinite(v) ? v : pow_libm(x, y);
 }
 
 // y = RN(1/q), the controller's exponents (1/3 step control, 1/4 initial_step,
@@ -121,9 +135,9 @@ MS_HD inline bool pow_root(double x, double y, double* out) {
 #ifndef MS_POW_ROOT_START
 #define MS_POW_ROOT_START 1  // 0: start from libm pow (A/B: tools/build_variants.py pow_libm_*)
 #endif
-  const double r0 = !MS_POW_ROOT_START ? pow(x, y)
+  const double r0 = !MS_POW_ROOT_START ? pow_libm(x, y)
                     : q == 2 ? std::sqrt(x)
-                    : (q == 3 ? std::cbrt(x) : (q == 4 ? std::sqrt(std::sqrt(x)) : pow(x, y)));
+                    : (q == 3 ? std::cbrt(x) : (q == 4 ? std::sqrt(std::sqrt(x)) : pow_libm(x, y)));
   if (!(r0 > 0.0) || !isfinite(r0)) return false;
   dd p{r0, 0.0};
   for (int i = 1; i < q; ++i) p = dd_mul_d(p, r0);  // r0^q
@@ -142,7 +156,7 @@ MS_HD inline bool pow_root(double x, double y, double* out) {
 }
 
 MS_HD inline double pow_cr(double x, double y) {
-  if (!(x > 0.0) || !isfinite(x) || !isfinite(y)) return pow(x, y);
+  if (!(x > 0.0) || !isfinite(x) || !isfinite(y)) return pow_libm(x, y);
   if (y == 0.0 || x == 1.0) return 1.0;
   double v;
   if (pow_root(x, y, &v)) return v;

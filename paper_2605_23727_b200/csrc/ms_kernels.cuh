@@ -1681,6 +1681,10 @@ __device__ inline double seq_sum(const double* v, int64_t n) {
 }
 
 #ifdef MS_DEFINE_STEP_KERNELS
+#ifndef MS_FIN_UNROLL
+#define MS_FIN_UNROLL 1
+#endif
+constexpr int kFinUnroll = MS_FIN_UNROLL;
 __global__ void __launch_bounds__(kFinSmallThreads) k_finalize(FinArgs f) {
   msb::count_launch();
   pdl_enter();
@@ -1698,7 +1702,9 @@ __global__ void __launch_bounds__(kFinSmallThreads) k_finalize(FinArgs f) {
     const double* xnx = c->store32 ? f.B.xn : xst;
     const double h = c->h_att;
     const double floor_w = __ddiv_rn(c->abs_tol, c->rel_tol);
-#pragma unroll 4
+    // not unrolled: a thread has at most a few elements at every BASELINE size (the grid
+    // covers dn), and the kernel's time is its instruction footprint (MS_FIN_UNROLL)
+#pragma unroll kFinUnroll
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < f.dn; e += (int64_t)gridDim.x * blockDim.x) {
       // x_tilde = x + h * (sum b~_l k_l), solver.cpp:188-199
       double comb = __dmul_rn(f.bt[0], resolve_slot(f.B, f.S, f.bslot[0], k1i)[e]);

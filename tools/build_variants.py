@@ -196,6 +196,10 @@ VARIANTS = {
     "gv_new_fine_i1": ("ms_rhs_fast.cu", {"MS_GV_FINE": 1, "MS_GV_ISSUE": 1}),
     "gv_new_kb2": ("ms_rhs_fast.cu", {"MS_GV_KB": 2, "MS_GV_STAGES": 6, "MS_GV_ZATOM": 1}),
     "gv_new_zatom": ("ms_rhs_fast.cu", {"MS_GV_ZATOM": 1}),
+    "fin_u4": ("ms_api.cu", {"MS_FIN_UNROLL": 4}),
+    "fin_u1": ("ms_api.cu", {"MS_FIN_UNROLL": 1}),
+    "pow_cold0": ("ms_api.cu", {"MS_POW_COLD": 0}),
+    "pow_cold1": ("ms_api.cu", {"MS_POW_COLD": 1}),
     "t2_pro0": ("ms_batch.cu", {"MS_T2_PRO_RELAXED": 0}),
     "t2_pro1": ("ms_batch.cu", {"MS_T2_PRO_RELAXED": 1}),
     "t2_rel0": ("ms_batch.cu", {"MS_T2_DRAIN_RELAXED": 0}),
