@@ -230,6 +230,10 @@ __device__ __forceinline__ void prep_count(const PrepArgs& p, Ctl* ctl) {
 // own = false nothing is written (a fused sweep recomputing other agents'
 // column values); the in-place binary32 rounding of x is idempotent, so
 // readers racing with the owner see the same value either way.
+#ifndef MS_PREP_ROLL
+#define MS_PREP_ROLL 1
+#endif
+constexpr int kPrepUnroll = MS_PREP_ROLL ? 1 : 4;
 __device__ __forceinline__ double prep_arg(const PrepArgs& p, const PrepCtx& c, int64_t e, bool own) {
   double v;
   if (p.kind == PREP_X) {
@@ -242,7 +246,10 @@ __device__ __forceinline__ double prep_arg(const PrepArgs& p, const PrepCtx& c, 
     v = __dadd_rn(c.xs[e], __dmul_rn(c.h, p.B.kb[1][e]));  // x0 + h1 * f0 (solver.cpp:435)
   } else {
     // combo = a_l0*k_0 (+ a_lm*k_m ...), arg = x + h*combo (solver.cpp:130-142)
+    // the short runtime loops below stay rolled (MS_PREP_ROLL): unrolled copies of
+    // every stage shape made the preps 3-4 x larger than the path an attempt executes
     double cm = __dmul_rn(p.coef[0], resolve_slot(p.B, p.S, p.slot[0], c.k1i)[e]);
+#pragma unroll kPrepUnroll
     for (int t = 1; t < p.nterms; ++t)
       cm = __dadd_rn(cm, __dmul_rn(p.coef[t], resolve_slot(p.B, p.S, p.slot[t], c.k1i)[e]));
     v = __dadd_rn(c.xs[e], __dmul_rn(c.h, cm));
@@ -251,6 +258,7 @@ __device__ __forceinline__ double prep_arg(const PrepArgs& p, const PrepCtx& c, 
         // combine_binary32 (solver.cpp:86-104)
         const float hf = __double2float_rn(c.h);
         float acc = __double2float_rn(c.xs[e]);
+#pragma unroll kPrepUnroll
         for (int t = 0; t < p.nterms; ++t) {
           const float cf = __fmul_rn(hf, __double2float_rn(p.coef[t]));
           acc = __fadd_rn(acc, __fmul_rn(cf, __double2float_rn(resolve_slot(p.B, p.S, p.slot[t], c.k1i)[e])));
@@ -288,6 +296,7 @@ __device__ __forceinline__ bool prep_agent(const PrepArgs& p, const PrepCtx& c, 
   const int d = p.md.d;
   bool nonfinite = false;
   double a[4];
+#pragma unroll kPrepUnroll
   for (int s = 0; s < d; ++s) a[s] = prep_arg(p, c, (int64_t)i * d + s, true);
   if (MODEL < 0) {
     // reference test fixtures (test_support.hpp:21-53): the whole RHS is F
