@@ -38,6 +38,16 @@ def test_reference_arm_contract():
     assert d["config"] == bench.workload_config(512, "f32", 1)
 
 
+def test_reference_arm_other_ranks_exit_without_work():
+    """Under torchrun only rank 0 runs and prints the reference arm; the other
+    ranks exit 0 at once with no output."""
+    env = dict(os.environ, RANK="1", LOCAL_RANK="1", WORLD_SIZE="2")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2", "--n", "512",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")], r.stdout
+
+
 @pytest.mark.gpu
 def test_our_arm_contract(gpu):
     d = _run(["--n", "4096", "--steps", "1", "--warmup", "1", "--no-cpu-baseline"])
